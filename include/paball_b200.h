@@ -1,0 +1,118 @@
+/*
+ * paball_b200.h — C ABI of the B200-native SlingBAG Pro hot path.
+ *
+ * The reference (`paball`, pure Python/numpy) has no FFI: its single internal
+ * seam is radiator._run_model(cloud, ctx, f, real, stage)
+ * (/root/reference/pkg/src/paball/radiator.py:290), reached from
+ * simulate_signals (:362), simulate_at_rate (:368) and backward (:419), plus
+ * the driver's Adam update (optimizer.py:203-209) and cloud compaction
+ * (model.py:239-244 via optimizer.py:255-256).  The entry points below are
+ * what a binding of that seam needs (INTEGRATION.md shows the ctypes stub).
+ *
+ * Conventions
+ *  - All array pointers are DEVICE pointers unless stated; sizes are element
+ *    counts; `stream` is a cudaStream_t passed as void* (NULL = legacy stream).
+ *  - Every function returns 0 on success, 1 on a bad argument, 4 when a CUDA
+ *    launch failed.  Nothing throws across the boundary.
+ *  - Device status words (int) collect per-pass error bits:
+ *      2  ball coincident with a detector   -> SimulationError (radiator.py:190-193)
+ *      8  non-finite gradient               -> OptimizationError (optimizer.py:284-294)
+ *  - Ball clouds are packed once per change by pab_pack into processing order
+ *    (lane groups of 32 Morton-ordered balls).  Record sizes: pab_record_sizes.
+ *  - Detector auxiliary data `det_aux` is [n_det][9] doubles: receive
+ *    direction (unit, = -outward normal), element axes e1, e2.
+ *  - Directivity: dir_kind 0 none (reference semantics), 1 cos^p (dir_param =
+ *    p), 2 square element of width dir_param metres.
+ *  - Acquisition: v sound speed, t0/dt the FULL-rate grid, f the decimation
+ *    factor, n_out = ceil(n_samples / f) the decimated sample count.
+ */
+#ifndef PABALL_B200_H
+#define PABALL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+int pab_version(void);
+int pab_device_info(int device, int* sm_count, int* cc_major, int* cc_minor, int* max_smem_optin);
+const char* pab_last_cuda_error(void);
+int pab_record_sizes(int* ball_a, int* ball_b, int* group_meta);
+
+/* Spatial sort keys: key[i] = morton30(quantised pos[i]) << 32 | i.
+ * Replaces: nothing (the reference visits balls in input order, radiator.py:185). */
+int pab_morton_keys(const double* pos /*[n][3]*/, int64_t n, double lox, double loy, double loz,
+                    double extent, int64_t* keys, void* stream);
+
+/* Pack a cloud (caller order, FP64 SoA) into processing-order records.
+ * perm[i] = caller index of the i-th processed ball.  rec_a/rec_b hold
+ * ceil(n/32)*32 records of 16 bytes, group_meta ceil(n/32) records of 32 bytes.
+ * Replaces: PointCloud field coercion (model.py:186-205) at the radiator boundary. */
+int pab_pack(const double* pos, const double* p0, const double* a0, const int32_t* perm, int64_t n,
+             void* rec_a, void* rec_b, void* group_meta, void* stream);
+
+/* Forward model: partial_rows[partitions][n_det][n_out] (FP32) for the given
+ * detector set.  ops_total += in-window samples (the reference op counter).
+ * Replaces: radiator._block_pass forward (radiator.py:157-261). */
+size_t pab_forward_smem_bytes(int n_out, int warps, int tile_rows);
+int pab_forward(const void* rec_a, const void* rec_b, const void* group_meta, int64_t n_groups,
+                const double* det_pos /*[n_det][3]*/, const double* det_aux /*[n_det][9]*/, int n_det,
+                double v, double t0, double dt, int f, int n_out, double cutoff, int dir_kind,
+                double dir_param, int groups_per_cell, int partitions, int warps, int tile_rows,
+                float* partial_rows, unsigned long long* ops_total, int* status, void* stream);
+
+/* Sum forward partitions; with `real` (nullable) write res = sim - real and
+ * per-detector FP64 sum of squares to loss_rows, else write sim.
+ * Replaces: radiator.py:263-264 (residual, loss part) and the block merge :339-344. */
+int pab_residual(const float* partial_rows, int partitions, int n_det, int n_out, const float* real,
+                 float* out, double* loss_rows, void* stream);
+
+/* Adjoint: per-ball partial gradient sums grad_partial[chunks][5][n_groups*32]
+ * from res[n_det][n_out] * res_sign (res_sign = -1 with `real` gives the
+ * zero-pressure filter probe, optimizer.py:251-253).  stage 0 filter (p0),
+ * 1 coarse (p0, a0), 2 fine (p0, a0, position).
+ * Replaces: radiator.py:266-287 (gather + reductions). */
+int pab_adjoint(const void* rec_a, const void* rec_b, const void* group_meta, int64_t n_groups,
+                const double* det_pos, const double* det_aux, int n_det, double v, double t0, double dt,
+                int f, int n_out, double cutoff, int dir_kind, double dir_param, const float* res,
+                float res_sign, int stage, int chunks, int warps, double* grad_partial,
+                unsigned long long* ops_total, int* status, void* stream);
+
+/* Sum chunk partials in order, multiply by `scale` (2 / (n_det_total * n_out)),
+ * scatter to caller order: d_p0[n], d_a0[n] (nullable), d_pos[n][3] (nullable).
+ * Replaces: radiator.py:345-348, 356-358. */
+int pab_grad_finalize(const double* grad_partial, int chunks, int64_t n_groups, const void* rec_b, double scale,
+                      int stage, double* d_p0, double* d_a0, double* d_pos, int* status, void* stream);
+
+/* Pure decimation of FP32 rows: dst[r][k] = src[r][k*f], k < ceil(n_in/f).
+ * Replaces: radiator.downsample (radiator.py:382-390). */
+int pab_decimate(const float* src, int n_rows, int n_in, int f, float* dst, void* stream);
+
+/* One Adam update of `count` FP64 values with bias corrections bc1 = 1-0.9^t,
+ * bc2 = 1-0.999^t; use_floor applies max(value, floor_value).
+ * Replaces: optimizer._adam_update (optimizer.py:203-209) and :298-304. */
+int pab_adam(double* param, const double* grad, double* m, double* v, int64_t count, double lr, double bc1,
+             double bc2, double floor_value, int use_floor, void* stream);
+
+/* Stable compaction: idx_out <- ascending indices i with key[i] < 0 (mode 0),
+ * <= 0 (mode 1) or != 0 (mode 2); *count_dev <- their number.
+ * Replaces: the boolean subset in optimizer.py:255-256 / model.py:239-244. */
+size_t pab_compact_workspace_bytes(int64_t n);
+int pab_compact(const double* key, int64_t n, int mode, int32_t* idx_out, int* count_dev, void* workspace,
+                void* stream);
+
+/* *out = sum_i (a[i] - b[i])^2 in FP64 (b nullable), fixed summation order.
+ * Replaces: radiator.loss (radiator.py:393-402). */
+size_t pab_sumsq_workspace_bytes(int64_t n);
+int pab_sumsq_diff_f64(const double* a, const double* b, int64_t n, double* out, void* workspace, void* stream);
+
+/* dst[r][c] = src[idx[r]][c] for r < m, c < width (FP64). */
+int pab_gather_f64(const double* src, int width, const int32_t* idx, int64_t m, double* dst, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PABALL_B200_H */

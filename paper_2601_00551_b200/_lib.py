@@ -1,0 +1,78 @@
+"""ctypes binding of the in-tree sm_100a library ``libpaball_b200.so``.
+
+The library is the product: if it is missing or cannot be loaded, every
+compute entry point raises.  There is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpaball_b200.so")
+
+_vp, _i, _i64, _d, _f = C.c_void_p, C.c_int, C.c_int64, C.c_double, C.c_float
+_SIGS = {
+    "pab_version": ([], _i),
+    "pab_device_info": ([_i, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)], _i),
+    "pab_last_cuda_error": ([], C.c_char_p),
+    "pab_record_sizes": ([C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)], _i),
+    "pab_morton_keys": ([_vp, _i64, _d, _d, _d, _d, _vp, _vp], _i),
+    "pab_pack": ([_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp], _i),
+    "pab_forward_smem_bytes": ([_i, _i, _i], C.c_size_t),
+    "pab_forward": ([_vp, _vp, _vp, _i64, _vp, _vp, _i, _d, _d, _d, _i, _i, _d, _i, _d, _i, _i, _i, _i,
+                     _vp, _vp, _vp, _vp], _i),
+    "pab_residual": ([_vp, _i, _i, _i, _vp, _vp, _vp, _vp], _i),
+    "pab_adjoint": ([_vp, _vp, _vp, _i64, _vp, _vp, _i, _d, _d, _d, _i, _i, _d, _i, _d, _vp, _f, _i, _i, _i,
+                     _vp, _vp, _vp, _vp], _i),
+    "pab_grad_finalize": ([_vp, _i, _i64, _vp, _d, _i, _vp, _vp, _vp, _vp, _vp], _i),
+    "pab_decimate": ([_vp, _i, _i, _i, _vp, _vp], _i),
+    "pab_adam": ([_vp, _vp, _vp, _vp, _i64, _d, _d, _d, _d, _i, _vp], _i),
+    "pab_compact_workspace_bytes": ([_i64], C.c_size_t),
+    "pab_compact": ([_vp, _i64, _i, _vp, _vp, _vp, _vp], _i),
+    "pab_gather_f64": ([_vp, _i, _vp, _i64, _vp, _vp], _i),
+    "pab_sumsq_workspace_bytes": ([_i64], C.c_size_t),
+    "pab_sumsq_diff_f64": ([_vp, _vp, _i64, _vp, _vp, _vp], _i),
+}
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+
+
+class LibraryError(RuntimeError):
+    pass
+
+
+def load(path: str = LIB_PATH):
+    """Load (once) and type the shared library; raise if unavailable."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise LibraryError(
+            f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(nvcc, sm_100a).  There is no CPU fallback.")
+    lib = C.CDLL(path)
+    for name, (args, res) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def call(name: str, *args) -> None:
+    """Invoke an entry point and turn non-zero return codes into errors."""
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != 0:
+        if rc == 1:
+            raise ValueError(f"{name}: invalid argument (rc=1)")
+        err = lib.pab_last_cuda_error().decode()
+        raise LibraryError(f"{name}: CUDA launch failed (rc={rc}): {err}")
+
+
+def ptr(t) -> int | None:
+    """Device/host address of a torch tensor (None for None)."""
+    return None if t is None else t.data_ptr()

@@ -1,0 +1,275 @@
+// Shared device code for the SlingBAG Pro forward/adjoint kernels (sm_100a).
+//
+// Physics (reference radiator.py:1-12, 157-287): a ball (position r_b, peak
+// pressure p0, Gaussian radius a0) seen from a detector at distance d gives
+//   s(t) = (p0 D / 2d) [u- G(u-) + u+ G(u+)],  u-+ = d -+ v t,  G = exp(-u^2/2a0^2)
+// evaluated only where |u| <= cutoff * a0, on sample k of the full-rate grid
+// (t = t0 + k dt); on an f-decimated grid sample J sits at k = J f.
+//
+// Numerics: per-(group, detector) geometry in FP64, per-pair
+// setup in FP32 relative to the group centre, per-sample math in FP32:
+//   tau = (d - v t0) / (v dt) = kc + phi,  kc integer, |phi| <= 1/2
+//   x   = tau - k = phi - m,  m = k - kc (exact small integer)
+//   y   = x * s,  s = v dt sqrt(log2(e)/2) / a0   =>  G = 2^(-y^2)
+//   u G = (v dt / s) y G = kappa y G,  kappa = a0 sqrt(2 ln 2)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pab {
+
+constexpr int kWarp = 32;
+constexpr float kSqrtHalfLog2e = 0.84932180028801907f;   // sqrt(log2(e) / 2)
+constexpr float kSqrt2Ln2 = 1.17741002251547469f;        // sqrt(2 ln 2) = kappa / a0
+constexpr float kTwoLn2 = 1.38629436111989061f;          // kappa^2 / a0^2
+constexpr float kSqrt2Ln2Cubed = 1.63221961130884960f;   // (kappa / a0)^3
+
+// status bits written by kernels (host raises the reference error classes)
+constexpr int kStatusCoincident = 2;   // SimulationError (radiator.py:190-193)
+constexpr int kStatusNonFinite = 8;    // OptimizationError (optimizer.py:284-294)
+
+// directivity kinds
+constexpr int kDirNone = 0;
+constexpr int kDirCosPower = 1;
+constexpr int kDirElement = 2;
+
+// adjoint stages
+constexpr int kStageFilter = 0;   // p0 only; caller passes res = -real
+constexpr int kStageCoarse = 1;   // p0, a0
+constexpr int kStageFine = 2;     // p0, a0, position
+
+struct Acq {
+  double vdt, inv_vdt, vt0;   // v*dt, 1/(v*dt), v*t0 (full-rate grid)
+  int f, n_out;               // decimation factor, samples on the decimated grid
+  float cutoff;               // support half-width in sigmas
+  float vdt_f, inv_vdt_f;
+  int dir_kind;
+  float dir_param;            // cos power p, or element width w (m)
+};
+
+// Ball records in processing (sorted) order; 32 consecutive records form a
+// lane group sharing an FP64 centre.  Padding records have orig < 0.
+struct BallA { float dx, dy, dz, a0; };          // offset from group centre, radius
+struct BallB { float p0, r2, pad; int orig; };   // pressure, |offset|^2, original index
+
+struct GroupMeta { double cx, cy, cz; float radius, a0max; };
+
+// Per (lane group, detector) geometry, computed in FP64 once and broadcast.
+struct GroupDet {
+  float Sx, Sy, Sz;   // detector - group centre
+  float Sn, isn;      // |S|, 1/|S|
+  float phg;          // frac(tau_g), tau_g = (|S| - v t0) / (v dt)
+  int kg;             // floor(tau_g)
+  int slow;           // detector close to the group: exact FP64 per-pair path
+};
+
+struct Detector {
+  double px, py, pz;
+  float fx, fy, fz;   // receive direction (unit; = -outward normal)
+  float e1x, e1y, e1z, e2x, e2y, e2z;   // element axes (kDirElement)
+};
+
+__device__ __forceinline__ Detector load_detector(const double* __restrict__ pos,
+                                                  const double* __restrict__ aux, int j) {
+  Detector D;
+  D.px = pos[3 * j + 0]; D.py = pos[3 * j + 1]; D.pz = pos[3 * j + 2];
+  const double* a = aux + 9 * j;
+  D.fx = (float)a[0]; D.fy = (float)a[1]; D.fz = (float)a[2];
+  D.e1x = (float)a[3]; D.e1y = (float)a[4]; D.e1z = (float)a[5];
+  D.e2x = (float)a[6]; D.e2y = (float)a[7]; D.e2z = (float)a[8];
+  return D;
+}
+
+__device__ __forceinline__ GroupDet group_det(const GroupMeta& g, double px, double py, double pz,
+                                              const Acq& a) {
+  GroupDet r;
+  const double Sx = px - g.cx, Sy = py - g.cy, Sz = pz - g.cz;
+  const double Sn = sqrt(Sx * Sx + Sy * Sy + Sz * Sz);
+  const double tau = (Sn - a.vt0) * a.inv_vdt;
+  const double kf = floor(tau);
+  r.Sx = (float)Sx; r.Sy = (float)Sy; r.Sz = (float)Sz;
+  r.Sn = (float)Sn;
+  r.isn = (float)(1.0 / Sn);
+  r.phg = (float)(tau - kf);
+  r.kg = (int)kf;
+  r.slow = (Sn <= 2.0 * (double)g.radius + 1e-9) ? 1 : 0;
+  return r;
+}
+
+__device__ __forceinline__ GroupDet shfl_gd(const GroupDet& g, int src) {
+  GroupDet r;
+  r.Sx = __shfl_sync(0xffffffffu, g.Sx, src);
+  r.Sy = __shfl_sync(0xffffffffu, g.Sy, src);
+  r.Sz = __shfl_sync(0xffffffffu, g.Sz, src);
+  r.Sn = __shfl_sync(0xffffffffu, g.Sn, src);
+  r.isn = __shfl_sync(0xffffffffu, g.isn, src);
+  r.phg = __shfl_sync(0xffffffffu, g.phg, src);
+  r.kg = __shfl_sync(0xffffffffu, g.kg, src);
+  r.slow = __shfl_sync(0xffffffffu, g.slow, src);
+  return r;
+}
+
+__device__ __forceinline__ int floor_div(int a, int b) {
+  int q = a / b;
+  return (a % b != 0 && ((a < 0) != (b < 0))) ? q - 1 : q;
+}
+__device__ __forceinline__ int ceil_div(int a, int b) { return -floor_div(-a, b); }
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Per (ball, detector) quantities.
+struct Pair {
+  int kc;             // anchor full-rate sample (nearest to tau)
+  float phi;          // tau - kc
+  float d;            // distance
+  float rx, ry, rz;   // r_ball - r_det
+  float base;         // p0 / (2 d)
+  float D;            // directivity weight
+  float amp;          // base * D
+  float sc;           // y per unit x  (v dt sqrt(log2e/2) / a0)
+  float rho;          // support half-width in full-rate samples
+  int jlo, jhi;       // u- window on the decimated grid, clipped (empty if jlo > jhi)
+  int nlo, nhi;       // u+ window (near field), usually empty
+  int nkc;            // u+ anchor
+  float nphi;         // u+ fraction
+  int coincident;
+};
+
+// Directivity weight and (optionally) its derivatives w.r.t. the ball position
+// (dDdr) and a0 (dDda0).  cos_power: D = max(cos,0)^p, cos = face . rhat.
+// element: D = sinc(w s1 / 2a0) sinc(w s2 / 2a0), s_k = e_k . rhat.
+__device__ __forceinline__ float directivity(const Acq& a, const Detector& det, float rx, float ry,
+                                             float rz, float d, float a0, bool want_grad,
+                                             float* dDdr, float* dDda0) {
+  if (a.dir_kind == kDirNone) return 1.0f;
+  const float id = 1.0f / d;
+  const float hx = rx * id, hy = ry * id, hz = rz * id;
+  if (a.dir_kind == kDirCosPower) {
+    const float c = det.fx * hx + det.fy * hy + det.fz * hz;
+    if (c <= 0.0f) {
+      if (want_grad) { dDdr[0] = dDdr[1] = dDdr[2] = 0.0f; *dDda0 = 0.0f; }
+      return 0.0f;
+    }
+    const float p = a.dir_param;
+    float D, dDdc;
+    if (p == 2.0f) { D = c * c; dDdc = 2.0f * c; }
+    else if (p == 1.0f) { D = c; dDdc = 1.0f; }
+    else { D = __powf(c, p); dDdc = p * D / c; }
+    if (want_grad) {
+      dDdr[0] = dDdc * (det.fx - c * hx) * id;
+      dDdr[1] = dDdc * (det.fy - c * hy) * id;
+      dDdr[2] = dDdc * (det.fz - c * hz) * id;
+      *dDda0 = 0.0f;
+    }
+    return D;
+  }
+  // element (square piston, far-field weight at the pulse's spectral peak)
+  const float s1 = det.e1x * hx + det.e1y * hy + det.e1z * hz;
+  const float s2 = det.e2x * hx + det.e2y * hy + det.e2z * hz;
+  const float sc = a.dir_param / (2.0f * a0);
+  const float x1 = sc * s1, x2 = sc * s2;
+  float f1, g1, f2, g2;
+  if (fabsf(x1) < 1e-3f) { f1 = 1.0f - x1 * x1 * (1.0f / 6.0f); g1 = -x1 * (1.0f / 3.0f); }
+  else { float sn, cs; sincosf(x1, &sn, &cs); f1 = sn / x1; g1 = (cs - f1) / x1; }
+  if (fabsf(x2) < 1e-3f) { f2 = 1.0f - x2 * x2 * (1.0f / 6.0f); g2 = -x2 * (1.0f / 3.0f); }
+  else { float sn, cs; sincosf(x2, &sn, &cs); f2 = sn / x2; g2 = (cs - f2) / x2; }
+  if (want_grad) {
+    const float a1 = g1 * f2 * sc, a2 = f1 * g2 * sc;
+    dDdr[0] = (a1 * (det.e1x - s1 * hx) + a2 * (det.e2x - s2 * hx)) * id;
+    dDdr[1] = (a1 * (det.e1y - s1 * hy) + a2 * (det.e2y - s2 * hy)) * id;
+    dDdr[2] = (a1 * (det.e1z - s1 * hz) + a2 * (det.e2z - s2 * hz)) * id;
+    *dDda0 = -(a1 * s1 + a2 * s2) / a0;
+  }
+  return f1 * f2;
+}
+
+// Per-pair setup.  gd: group/detector geometry; gm: the ball's group (slow
+// path only); A/B: the ball record.
+__device__ __forceinline__ Pair make_pair(const Acq& a, const GroupDet& gd, const GroupMeta& gm,
+                                          const Detector& det, const BallA& A, const BallB& B,
+                                          bool want_grad, float* dDdr, float* dDda0) {
+  Pair p;
+  p.coincident = 0;
+  float tr;   // tau - kg (FP32, small)
+  int kbase;
+  if (!gd.slow) {
+    const float sd = gd.Sx * A.dx + gd.Sy * A.dy + gd.Sz * A.dz;
+    const float num = B.r2 - 2.0f * sd;               // d^2 - |S|^2
+    const float e = num * gd.isn * gd.isn;
+    const float dd = num * gd.isn / (1.0f + sqrtf(1.0f + e));   // d - |S|
+    p.d = gd.Sn + dd;
+    tr = gd.phg + dd * a.inv_vdt_f;
+    kbase = gd.kg;
+    p.rx = A.dx - gd.Sx; p.ry = A.dy - gd.Sy; p.rz = A.dz - gd.Sz;
+  } else {
+    // exact FP64 distance when the detector sits near/inside the group
+    const double bx = gm.cx + (double)A.dx, by = gm.cy + (double)A.dy, bz = gm.cz + (double)A.dz;
+    const double dx = bx - det.px, dy = by - det.py, dz = bz - det.pz;
+    const double d = sqrt(dx * dx + dy * dy + dz * dz);
+    if (d < 1e-12) p.coincident = 1;
+    const double tau = (d - a.vt0) * a.inv_vdt;
+    const double kf = floor(tau);
+    kbase = (int)kf;
+    tr = (float)(tau - kf);
+    p.d = (float)(d > 1e-30 ? d : 1e-30);
+    p.rx = (float)dx; p.ry = (float)dy; p.rz = (float)dz;
+  }
+  const float kr = rintf(tr);
+  p.kc = kbase + (int)kr;
+  p.phi = tr - kr;
+  p.base = B.p0 / (2.0f * p.d);
+  p.D = directivity(a, det, p.rx, p.ry, p.rz, p.d, A.a0, want_grad, dDdr, dDda0);
+  p.amp = (B.p0 * p.D) / (2.0f * p.d);
+  p.sc = a.vdt_f * kSqrtHalfLog2e / A.a0;
+  p.rho = a.cutoff * A.a0 * a.inv_vdt_f;
+  // u- window: full-rate k in [kc + ceil(phi - rho), kc + floor(phi + rho)]
+  {
+    const int klo = p.kc + (int)ceilf(p.phi - p.rho);
+    const int khi = p.kc + (int)floorf(p.phi + p.rho);
+    p.jlo = max(ceil_div(klo, a.f), 0);
+    p.jhi = min(floor_div(khi, a.f), a.n_out - 1);
+  }
+  // u+ window: tau+ = -(d + v t0) / (v dt); non-empty only in the near field
+  p.nlo = 1; p.nhi = 0; p.nkc = 0; p.nphi = 0.0f;
+  const double taup = -((double)p.d + a.vt0) * a.inv_vdt;
+  if (taup + (double)p.rho >= 0.0) {
+    const double kp = rint(taup);
+    p.nkc = (int)kp;
+    p.nphi = (float)(taup - kp);
+    const int klo = p.nkc + (int)ceilf(p.nphi - p.rho);
+    const int khi = p.nkc + (int)floorf(p.nphi + p.rho);
+    p.nlo = max(ceil_div(klo, a.f), 0);
+    p.nhi = min(floor_div(khi, a.f), a.n_out - 1);
+  }
+  if (B.orig < 0) { p.jlo = 1; p.jhi = 0; p.nlo = 1; p.nhi = 0; }
+  return p;
+}
+
+// Decimated-sample range a lane group can touch for one detector: centre
+// tau_g -+ (radius / v dt + rho_max + 1), plus [0, ..] when a u+ term can exist.
+__device__ __forceinline__ void group_range(const Acq& a, const GroupDet& gd, const GroupMeta& gm,
+                                            int* lo, int* hi) {
+  const float rho = a.cutoff * gm.a0max * a.inv_vdt_f;
+  const float span = gm.radius * a.inv_vdt_f + rho + 2.0f;
+  const float c = gd.phg;
+  int klo = gd.kg + (int)floorf(c - span);
+  int khi = gd.kg + (int)ceilf(c + span);
+  if (gd.slow) {   // FP32 S is coarse near the detector: widen generously
+    klo = min(klo, -(int)ceilf(rho) - 2);
+  }
+  // near field: u+ = d + v t0 + k v dt can vanish for k >= 0
+  const float dmin = gd.Sn - gm.radius;
+  const float taup_max = -(dmin + (float)a.vt0) * a.inv_vdt_f;
+  if (taup_max + rho + 1.0f >= 0.0f) {
+    klo = min(klo, (int)floorf(-(gd.Sn + gm.radius + (float)a.vt0) * a.inv_vdt_f - rho - 2.0f));
+    khi = max(khi, (int)ceilf(taup_max + rho + 2.0f));
+  }
+  *lo = max(floor_div(klo, a.f), 0);
+  *hi = min(ceil_div(khi, a.f), a.n_out - 1);
+}
+
+}  // namespace pab

@@ -1,0 +1,131 @@
+// Ball binning: spatial sort keys and lane-group packing.
+//
+// The reference brute-forces every 512-ball chunk against every sensor block
+// (radiator.py:185-196).  Here balls are visited in Morton order so that 32
+// consecutive balls (a lane group) are spatially compact: their arrival
+// windows at any detector overlap, which bounds the per-warp sample tile of
+// the forward kernel and the residual segment of the adjoint.  The order is a
+// performance choice only: any permutation gives the same sums up to the
+// (deterministic) summation order.
+#include "pab_common.cuh"
+
+namespace pab {
+
+__device__ __forceinline__ uint32_t spread3(uint32_t v) {   // 10 bits -> every 3rd bit
+  v &= 0x3ffu;
+  v = (v | (v << 16)) & 0x030000FFu;
+  v = (v | (v << 8)) & 0x0300F00Fu;
+  v = (v | (v << 4)) & 0x030C30C3u;
+  v = (v | (v << 2)) & 0x09249249u;
+  return v;
+}
+
+// key = (morton30 << 33) | (a0 bucket << 27... ) is not used: a0 enters as the
+// low-order tiebreak through the index only.  key = morton30 << 32 | index.
+__global__ void morton_keys_kernel(const double* __restrict__ pos, int64_t n, double lox, double loy,
+                                   double loz, double inv_ext, int64_t* __restrict__ keys) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double s = 1023.0 * inv_ext;
+  const uint32_t qx = (uint32_t)fmin(fmax((pos[3 * i + 0] - lox) * s, 0.0), 1023.0);
+  const uint32_t qy = (uint32_t)fmin(fmax((pos[3 * i + 1] - loy) * s, 0.0), 1023.0);
+  const uint32_t qz = (uint32_t)fmin(fmax((pos[3 * i + 2] - loz) * s, 0.0), 1023.0);
+  const uint64_t code = (uint64_t)(spread3(qx) | (spread3(qy) << 1) | (spread3(qz) << 2));
+  keys[i] = (int64_t)((code << 32) | (uint64_t)i);
+}
+
+__device__ __forceinline__ double warp_min(double v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_maxf(float v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// One warp per lane group: bounding-box centre (FP64), FP32 offsets, radius,
+// max a0.  Padding lanes (i >= n) become inert records (orig = -1, p0 = 0).
+__global__ void pack_kernel(const double* __restrict__ pos, const double* __restrict__ p0,
+                            const double* __restrict__ a0, const int32_t* __restrict__ perm, int64_t n,
+                            int64_t n_groups, BallA* __restrict__ ra, BallB* __restrict__ rb,
+                            GroupMeta* __restrict__ gm) {
+  const int lane = threadIdx.x & 31;
+  const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (g >= n_groups) return;
+  const int64_t i = g * kWarp + lane;
+  const bool live = i < n;
+  int b = 0;
+  double x = 0, y = 0, z = 0, pp = 0, aa = 1.0;
+  if (live) {
+    b = perm[i];
+    x = pos[3 * (int64_t)b + 0]; y = pos[3 * (int64_t)b + 1]; z = pos[3 * (int64_t)b + 2];
+    pp = p0[b]; aa = a0[b];
+  }
+  const double big = 1e300;
+  const double cx = 0.5 * (warp_min(live ? x : big) + warp_max(live ? x : -big));
+  const double cy = 0.5 * (warp_min(live ? y : big) + warp_max(live ? y : -big));
+  const double cz = 0.5 * (warp_min(live ? z : big) + warp_max(live ? z : -big));
+  BallA A;
+  BallB B;
+  if (live) {
+    A.dx = (float)(x - cx); A.dy = (float)(y - cy); A.dz = (float)(z - cz); A.a0 = (float)aa;
+    B.p0 = (float)pp;
+    B.r2 = A.dx * A.dx + A.dy * A.dy + A.dz * A.dz;
+    B.pad = 0.0f;
+    B.orig = b;
+  } else {
+    A.dx = A.dy = A.dz = 0.0f; A.a0 = 1.0f;
+    B.p0 = 0.0f; B.r2 = 0.0f; B.pad = 0.0f; B.orig = -1;
+  }
+  const float rad = warp_maxf(live ? sqrtf(B.r2) : 0.0f);
+  const float amax = warp_maxf(live ? A.a0 : 0.0f);
+  ra[i] = A;
+  rb[i] = B;
+  if (lane == 0) {
+    GroupMeta m;
+    m.cx = cx; m.cy = cy; m.cz = cz;
+    m.radius = rad * 1.000001f + 1e-12f;
+    m.a0max = amax;
+    gm[g] = m;
+  }
+}
+
+}  // namespace pab
+
+using namespace pab;
+
+extern "C" {
+
+int pab_morton_keys(const double* pos, int64_t n, double lox, double loy, double loz, double extent,
+                    int64_t* keys, void* stream) {
+  if (n <= 0) return 0;
+  if (!pos || !keys || !(extent > 0.0)) return 1;
+  const int threads = 256;
+  morton_keys_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0, (cudaStream_t)stream>>>(
+      pos, n, lox, loy, loz, 1.0 / extent, keys);
+  return cudaGetLastError() == cudaSuccess ? 0 : 4;
+}
+
+int pab_pack(const double* pos, const double* p0, const double* a0, const int32_t* perm, int64_t n,
+             void* rec_a, void* rec_b, void* group_meta, void* stream) {
+  if (n <= 0) return 0;
+  if (!pos || !p0 || !a0 || !perm || !rec_a || !rec_b || !group_meta) return 1;
+  const int64_t n_groups = (n + kWarp - 1) / kWarp;
+  const int warps = 8;
+  pack_kernel<<<(unsigned)((n_groups + warps - 1) / warps), warps * kWarp, 0, (cudaStream_t)stream>>>(
+      pos, p0, a0, perm, n, n_groups, (BallA*)rec_a, (BallB*)rec_b, (GroupMeta*)group_meta);
+  return cudaGetLastError() == cudaSuccess ? 0 : 4;
+}
+
+int pab_record_sizes(int* ball_a, int* ball_b, int* group_meta) {
+  *ball_a = (int)sizeof(BallA);
+  *ball_b = (int)sizeof(BallB);
+  *group_meta = (int)sizeof(GroupMeta);
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,385 @@
+"""Device-resident state and launch orchestration for the forward/adjoint path.
+
+PyTorch is used for device memory, streams and ``torch.distributed``; all
+arithmetic on the path runs in the sm_100a library (``_lib``).
+
+Multi-GPU: one process per GPU, detectors sharded in
+contiguous blocks; the ball cloud, its Adam state and every per-ball decision
+are replicated.  The forward is detector-local; the two exchanges per
+iteration are the scalar loss and the per-ball gradient all-reduce (NCCL).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import call, ptr
+from .model import OptimizationError, SimulationError
+from .parallel import Shard, allreduce_scalar, allreduce_sum_, current_shard, gather_rows  # noqa: F401
+
+STATUS_COINCIDENT = 2
+STATUS_NONFINITE = 8
+
+FORWARD_WARPS = 8
+FORWARD_TILE_ROWS = 160
+ADJOINT_WARPS = 8
+GROUP = 32
+
+
+def cuda_device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise _lib.LibraryError("a CUDA device is required: this package has no CPU path")
+    _lib.load()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+_SM_COUNT: dict = {}
+
+
+def sm_count(dev: torch.device) -> int:
+    if dev.index not in _SM_COUNT:
+        _SM_COUNT[dev.index] = torch.cuda.get_device_properties(dev).multi_processor_count
+    return _SM_COUNT[dev.index]
+
+
+# ---------------------------------------------------------------------------
+# Acquisition / directivity parameters of one call
+# ---------------------------------------------------------------------------
+
+DIR_CODES = {"none": 0, "cos_power": 1, "element": 2}
+
+
+@dataclass(frozen=True)
+class Acq:
+    v: float
+    t0: float
+    dt: float            # full-rate grid
+    n_samples: int       # full-rate count
+    f: int
+    cutoff: float
+    dir_kind: int
+    dir_param: float
+
+    @property
+    def n_out(self) -> int:
+        return -(-self.n_samples // self.f) if self.f > 1 else self.n_samples
+
+
+def detector_aux(positions: np.ndarray, normals, directivity) -> np.ndarray:
+    """[J, 9]: receive direction (-outward normal), element axes e1, e2."""
+    J = positions.shape[0]
+    aux = np.zeros((J, 9))
+    if directivity.kind == "none":
+        return aux
+    if normals is None:
+        raise ValueError(f"directivity {directivity.kind!r} needs SensorArray.normals")
+    face = -np.asarray(normals, dtype=np.float64)
+    face /= np.linalg.norm(face, axis=1, keepdims=True)
+    aux[:, 0:3] = face
+    ref = np.zeros_like(face)
+    ref[:, 0] = 1.0
+    ref[np.abs(face[:, 0]) > 0.9] = [0.0, 1.0, 0.0]
+    e1 = ref - np.sum(ref * face, axis=1, keepdims=True) * face
+    e1 /= np.linalg.norm(e1, axis=1, keepdims=True)
+    aux[:, 3:6] = e1
+    aux[:, 6:9] = np.cross(face, e1)
+    return aux
+
+
+class DeviceDetectors:
+    """This rank's contiguous block of detectors, resident on the GPU."""
+
+    def __init__(self, positions: np.ndarray, normals, directivity, sound_speed: float,
+                 dev: torch.device, shard: Shard):
+        positions = np.asarray(positions, dtype=np.float64).reshape(-1, 3)
+        self.n_total = positions.shape[0]
+        self.shard = shard
+        lo, hi = shard.range(self.n_total)
+        self.lo, self.hi = lo, hi
+        self.n_local = hi - lo
+        aux = detector_aux(positions, normals, directivity)
+        self.pos = torch.from_numpy(np.ascontiguousarray(positions[lo:hi])).to(dev)
+        self.aux = torch.from_numpy(np.ascontiguousarray(aux[lo:hi])).to(dev)
+        self.sound_speed = float(sound_speed)
+
+
+# ---------------------------------------------------------------------------
+# Ball cloud on device
+# ---------------------------------------------------------------------------
+
+
+class DeviceCloud:
+    """FP64 SoA cloud in caller order plus packed processing-order records."""
+
+    def __init__(self, pos: torch.Tensor, p0: torch.Tensor, a0: torch.Tensor):
+        self.dev = pos.device
+        self.pos = pos.contiguous()
+        self.p0 = p0.contiguous()
+        self.a0 = a0.contiguous()
+        self.perm = None
+        self._packed = False
+        self._stats = None
+
+    @classmethod
+    def from_host(cls, positions, p0, a0, dev) -> "DeviceCloud":
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev, non_blocking=False)
+        return cls(t(np.asarray(positions).reshape(-1, 3)), t(p0), t(a0))
+
+    @property
+    def n(self) -> int:
+        return int(self.p0.shape[0])
+
+    @property
+    def n_groups(self) -> int:
+        return (self.n + GROUP - 1) // GROUP
+
+    def invalidate(self, resort: bool = False) -> None:
+        """Parameters changed: repack before the next pass (and resort)."""
+        self._packed = False
+        self._stats = None
+        if resort:
+            self.perm = None
+
+    def sort(self) -> None:
+        n = self.n
+        if n == 0:
+            self.perm = torch.empty(0, dtype=torch.int32, device=self.dev)
+            return
+        lo = torch.amin(self.pos, dim=0)
+        hi = torch.amax(self.pos, dim=0)
+        ext = float(torch.max(hi - lo).item())
+        ext = ext if ext > 0.0 else 1.0
+        lo_h = lo.cpu().numpy()
+        keys = torch.empty(n, dtype=torch.int64, device=self.dev)
+        call("pab_morton_keys", ptr(self.pos), n, float(lo_h[0]), float(lo_h[1]), float(lo_h[2]), ext,
+             ptr(keys), _stream())
+        skeys, _ = torch.sort(keys)
+        self.perm = (skeys & 0xFFFFFFFF).to(torch.int32)
+
+    def pack(self) -> None:
+        if self._packed:
+            return
+        if self.perm is None or self.perm.shape[0] != self.n:
+            self.sort()
+        ng = self.n_groups
+        npad = ng * GROUP
+        if not hasattr(self, "rec_a") or self.rec_a.numel() < npad * 16:
+            self.rec_a = torch.empty(npad * 16, dtype=torch.uint8, device=self.dev)
+            self.rec_b = torch.empty(npad * 16, dtype=torch.uint8, device=self.dev)
+            self.gmeta = torch.empty(max(ng, 1) * 32, dtype=torch.uint8, device=self.dev)
+        if self.n:
+            call("pab_pack", ptr(self.pos), ptr(self.p0), ptr(self.a0), ptr(self.perm), self.n,
+                 ptr(self.rec_a), ptr(self.rec_b), ptr(self.gmeta), _stream())
+        self._packed = True
+        self._stats = None
+
+    def stats(self) -> tuple[float, float]:
+        """(median lane-group radius, max a0) for launch planning."""
+        if self._stats is None:
+            ng = self.n_groups
+            if ng == 0:
+                self._stats = (0.0, 0.0)
+            else:
+                meta = self.gmeta[: ng * 32].view(torch.float32).view(ng, 8)
+                r = float(torch.median(meta[:, 6]).item())
+                amax = float(torch.max(meta[:, 7]).item())
+                self._stats = (r, amax)
+        return self._stats
+
+
+# ---------------------------------------------------------------------------
+# Workspace and launch planning
+# ---------------------------------------------------------------------------
+
+
+class Workspace:
+    """Grow-only scratch tensors keyed by name."""
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.bufs: dict = {}
+
+    def get(self, name: str, numel: int, dtype) -> torch.Tensor:
+        t = self.bufs.get(name)
+        if t is None or t.numel() < numel or t.dtype != dtype:
+            t = torch.empty(max(numel, 1), dtype=dtype, device=self.dev)
+            self.bufs[name] = t
+        return t[:numel]
+
+
+_WS: dict = {}
+
+
+def workspace(dev) -> Workspace:
+    if dev.index not in _WS:
+        _WS[dev.index] = Workspace(dev)
+    return _WS[dev.index]
+
+
+@dataclass
+class ForwardPlan:
+    groups_per_cell: int
+    partitions: int
+    warps: int
+    tile_rows: int
+
+
+def plan_forward(cloud: DeviceCloud, det: DeviceDetectors, acq: Acq) -> ForwardPlan:
+    dev = cloud.dev
+    r_g, amax = cloud.stats()
+    vdt = det.sound_speed * acq.dt
+    f = acq.f
+    tile = FORWARD_TILE_ROWS
+    warps = FORWARD_WARPS
+    while warps > 1 and _lib.load().pab_forward_smem_bytes(acq.n_out, warps, tile) > 227 * 1024:
+        warps //= 2
+    rho = acq.cutoff * amax / vdt
+    avail = tile - 2.0 * rho / f - 6.0
+    if avail <= 0.0 or r_g <= 0.0:
+        C = 1 if avail <= 0.0 else 32
+    else:
+        r_cell = avail * vdt * f / 2.0
+        C = int(max(1, min(32, math.floor((r_cell / r_g) ** 3 * 0.7))))
+    n_cells = max(1, -(-cloud.n_groups // C))
+    target_ctas = 2 * sm_count(dev)
+    parts = max(1, -(-target_ctas // max(det.n_local, 1)))
+    parts = int(max(1, min(parts, n_cells // (2 * warps) if n_cells >= 2 * warps else 1)))
+    return ForwardPlan(C, parts, warps, tile)
+
+
+def plan_adjoint(cloud: DeviceCloud, det: DeviceDetectors) -> int:
+    ctas = -(-cloud.n_groups // ADJOINT_WARPS)
+    target = 4 * sm_count(cloud.dev)
+    chunks = max(1, -(-target // max(ctas, 1)))
+    return int(max(1, min(chunks, max(1, det.n_local // 16))))
+
+
+# ---------------------------------------------------------------------------
+# Passes
+# ---------------------------------------------------------------------------
+
+
+def _check_status(status: torch.Tensor) -> None:
+    s = int(status.item())
+    if s & STATUS_COINCIDENT:
+        raise SimulationError("ball coincident with a sensor (zero source-sensor distance)")
+    if s & STATUS_NONFINITE:
+        raise OptimizationError("non-finite gradient")
+
+
+class PassCounters:
+    """Device op counter + status word for one API call."""
+
+    def __init__(self, dev):
+        ws = workspace(dev)
+        self.ops = ws.get("ops", 1, torch.int64)
+        self.status = ws.get("status", 1, torch.int32)
+        self.ops.zero_()
+        self.status.zero_()
+
+    def read(self) -> int:
+        _check_status(self.status)
+        return int(self.ops.item())
+
+
+def forward_rows(cloud: DeviceCloud, det: DeviceDetectors, acq: Acq, counters: PassCounters,
+                 real_local: torch.Tensor | None = None, out: torch.Tensor | None = None):
+    """Simulate this rank's rows.  With ``real_local`` the result is the
+    residual sim - real and the per-row FP64 sum of squares is returned.
+    Returns (out [J_local, n_out] f32, loss_rows [J_local] f64 or None)."""
+    ws = workspace(cloud.dev)
+    n_out = acq.n_out
+    J = det.n_local
+    if out is None:
+        out = torch.empty((J, n_out), dtype=torch.float32, device=cloud.dev)
+    if J == 0:
+        return out, (torch.zeros(0, dtype=torch.float64, device=cloud.dev) if real_local is not None else None)
+    cloud.pack()
+    plan = plan_forward(cloud, det, acq)
+    partial = ws.get("partial_rows", plan.partitions * J * n_out, torch.float32)
+    loss_rows = ws.get("loss_rows", J, torch.float64) if real_local is not None else None
+    if cloud.n_groups > 0:
+        call("pab_forward", ptr(cloud.rec_a), ptr(cloud.rec_b), ptr(cloud.gmeta), cloud.n_groups,
+             ptr(det.pos), ptr(det.aux), J, det.sound_speed, acq.t0, acq.dt, acq.f, n_out, acq.cutoff,
+             acq.dir_kind, acq.dir_param, plan.groups_per_cell, plan.partitions, plan.warps,
+             plan.tile_rows, ptr(partial), ptr(counters.ops), ptr(counters.status), _stream())
+    else:
+        partial.zero_()
+    call("pab_residual", ptr(partial), plan.partitions, J, n_out, ptr(real_local), ptr(out),
+         ptr(loss_rows), _stream())
+    return out, loss_rows
+
+
+def adjoint_grads(cloud: DeviceCloud, det: DeviceDetectors, acq: Acq, res: torch.Tensor, res_sign: float,
+                  stage: int, scale: float, counters: PassCounters, count_ops: bool = False):
+    """Per-ball loss gradients in caller order (FP64), reduced over ranks.
+    stage: 0 filter (d_p0 only), 1 coarse, 2 fine."""
+    dev = cloud.dev
+    n = cloud.n
+    d_p0 = torch.zeros(n, dtype=torch.float64, device=dev)
+    d_a0 = torch.zeros(n, dtype=torch.float64, device=dev) if stage >= 1 else None
+    d_pos = torch.zeros((n, 3), dtype=torch.float64, device=dev) if stage >= 1 else None
+    if n > 0 and det.n_local > 0:
+        cloud.pack()
+        chunks = plan_adjoint(cloud, det)
+        ws = workspace(dev)
+        npad = cloud.n_groups * GROUP
+        gpart = ws.get("grad_partial", chunks * 5 * npad, torch.float64)
+        call("pab_adjoint", ptr(cloud.rec_a), ptr(cloud.rec_b), ptr(cloud.gmeta), cloud.n_groups,
+             ptr(det.pos), ptr(det.aux), det.n_local, det.sound_speed, acq.t0, acq.dt, acq.f, acq.n_out,
+             acq.cutoff, acq.dir_kind, acq.dir_param, ptr(res), float(res_sign), int(stage), chunks,
+             ADJOINT_WARPS, ptr(gpart), ptr(counters.ops) if count_ops else None, ptr(counters.status),
+             _stream())
+        call("pab_grad_finalize", ptr(gpart), chunks, cloud.n_groups, ptr(cloud.rec_b), float(scale), int(stage),
+             ptr(d_p0), ptr(d_a0), ptr(d_pos), ptr(counters.status), _stream())
+    if det.shard.world > 1:
+        allreduce_sum_(d_p0)
+        if d_a0 is not None:
+            allreduce_sum_(d_a0)
+            allreduce_sum_(d_pos)
+    return d_p0, d_a0, d_pos
+
+
+def decimate_rows(src: torch.Tensor, f: int) -> torch.Tensor:
+    rows, n_in = src.shape
+    n_out = -(-n_in // f)
+    dst = torch.empty((rows, n_out), dtype=torch.float32, device=src.device)
+    call("pab_decimate", ptr(src), rows, n_in, f, ptr(dst), _stream())
+    return dst
+
+
+def full_rows(local: torch.Tensor, det: DeviceDetectors) -> torch.Tensor:
+    """All ranks' rows (rank order) for API results."""
+    if det.shard.world == 1:
+        return local
+    return gather_rows(local, det.n_total)
+
+
+def current_shard_for(dev) -> Shard:
+    return current_shard()
+
+
+def sumsq_diff(a: torch.Tensor, b: torch.Tensor | None) -> float:
+    """sum (a - b)^2 over FP64 device tensors (deterministic order)."""
+    ws = workspace(a.device)
+    n = a.numel()
+    scratch = ws.get("ssd", int(_lib.load().pab_sumsq_workspace_bytes(n)) // 8 + 1, torch.float64)
+    out = ws.get("ssd_out", 1, torch.float64)
+    call("pab_sumsq_diff_f64", ptr(a), ptr(b), n, ptr(out), ptr(scratch), _stream())
+    return float(out.item())
+
+
+def mse_device(sim: np.ndarray, real: np.ndarray) -> float:
+    dev = cuda_device()
+    a = torch.from_numpy(np.ascontiguousarray(sim)).to(dev)
+    b = torch.from_numpy(np.ascontiguousarray(real)).to(dev)
+    return sumsq_diff(a, b) / a.numel()

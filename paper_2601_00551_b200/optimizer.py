@@ -1,0 +1,554 @@
+"""Reference-compatible iteration driver with device-resident state.
+
+Mirrors ``paball.optimizer`` (/root/reference/pkg/src/paball/optimizer.py):
+``Level``/``Schedule``/``SCHEDULE_PRESETS`` (:62-111), ``DensityThresholds``
+(:114-154), ``LearningRates`` (:157-165), ``OptimState``/``create_state``
+(:173-200), ``FilterReport``/``zero_gradient_filter`` (:217-258), ``step``
+(:266-306), ``density_control`` (:314-406), ``IterationTrace``/
+``run_hierarchical`` (:414-500).
+
+The cloud, Adam moments and last gradients live on the GPU between calls
+(FP64 master values; the kernels read packed FP32-offset records).  Host
+``PointCloud`` views are materialised only when ``state.cloud`` / ``state.m``
+/ ``state.v`` are read.  Per iteration the host sees one scalar (the loss).
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from collections.abc import MutableMapping
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import engine as E
+from . import radiator as R
+from ._lib import call, ptr
+from .model import CounterRng, OptimizationError, PointCloud, RngSeed, SimulationError
+
+__all__ = [
+    "Level", "Schedule", "SCHEDULE_PRESETS", "DensityThresholds", "LearningRates", "OptimState",
+    "FilterReport", "IterationTrace", "TraceRecord", "zero_gradient_filter", "create_state", "step",
+    "density_control", "run_hierarchical",
+]
+
+_PLATEAU_REL = 1e-5
+_PLATEAU_WINDOW = 50
+_COARSE_DENSITY_EVERY = 100
+_ADAM_BETA1 = 0.9
+_ADAM_BETA2 = 0.999
+_A0_RUNTIME_FLOOR = 1e-9
+
+
+# ---------------------------------------------------------------------------
+# Schedules, thresholds, learning rates (host-side configuration)
+# ---------------------------------------------------------------------------
+
+
+@dataclass(frozen=True)
+class Level:
+    f: int
+    max_iters: int
+    stage: str
+
+    def __post_init__(self) -> None:
+        if self.f < 1:
+            raise ValueError(f"decimation factor must be >= 1, got {self.f}")
+        if self.max_iters < 0:
+            raise ValueError(f"max_iters must be >= 0, got {self.max_iters}")
+        if self.stage not in ("coarse", "fine"):
+            raise ValueError(f"stage must be 'coarse' or 'fine', got {self.stage!r}")
+
+
+@dataclass(frozen=True)
+class Schedule:
+    levels: tuple
+    duplication_period: int = 200
+
+    def __post_init__(self) -> None:
+        levels = tuple(self.levels)
+        if not levels:
+            raise ValueError("schedule needs at least one level")
+        fs = [lv.f for lv in levels]
+        if any(b > a for a, b in zip(fs, fs[1:])):
+            raise ValueError(f"decimation factors must be non-increasing, got {fs}")
+        if levels[-1].f != 1 or levels[-1].stage != "fine":
+            raise ValueError("final level must be fine at the native rate (f=1)")
+        if self.duplication_period < 1:
+            raise ValueError(f"duplication_period must be >= 1, got {self.duplication_period}")
+        object.__setattr__(self, "levels", levels)
+
+
+def _preset(factors, iters):
+    stages = ["coarse"] + ["fine"] * (len(factors) - 1)
+    return Schedule(tuple(Level(f, it, st) for f, it, st in zip(factors, iters, stages)))
+
+
+SCHEDULE_PRESETS = {
+    "sim-16-4-1": _preset((16, 4, 1), (2000, 1000, 1000)),
+    "invivo-4-2-1": _preset((4, 2, 1), (1000, 500, 500)),
+}
+
+
+@dataclass(frozen=True)
+class DensityThresholds:
+    destroy_p0_frac: float = 0.02
+    split_a0: float = 2e-3
+    duplicate_grad_quantile: float = 0.90
+    a0_min: float = 1e-4
+    a0_max: float = 8e-3
+
+    def __post_init__(self) -> None:
+        vals = (self.destroy_p0_frac, self.split_a0, self.duplicate_grad_quantile, self.a0_min, self.a0_max)
+        if any(v <= 0.0 for v in vals):
+            raise ValueError("density thresholds must all be positive")
+        if not (self.a0_min < self.split_a0 < self.a0_max):
+            raise ValueError(f"need a0_min < split_a0 < a0_max, got "
+                             f"{self.a0_min} / {self.split_a0} / {self.a0_max}")
+
+    @classmethod
+    def from_spacing(cls, spacing: float, **overrides) -> "DensityThresholds":
+        kw = dict(destroy_p0_frac=0.02, split_a0=2.0 * spacing, duplicate_grad_quantile=0.90,
+                  a0_min=0.25 * spacing, a0_max=8.0 * spacing)
+        kw.update(overrides)
+        return cls(**kw)
+
+
+@dataclass(frozen=True)
+class LearningRates:
+    p0: float = 1e-2
+    a0: float = 4e-5
+    position: float = 2e-5
+
+    @classmethod
+    def from_spacing(cls, spacing: float, p0: float = 1e-2) -> "LearningRates":
+        return cls(p0=p0, a0=0.1 * spacing, position=0.05 * spacing)
+
+
+# ---------------------------------------------------------------------------
+# Device-resident optimiser state
+# ---------------------------------------------------------------------------
+
+_KEYS = ("p0", "a0", "position")
+
+
+class _DeviceMoments(MutableMapping):
+    """Host view of one moment dict; item assignment uploads to the device."""
+
+    def __init__(self, owner: "OptimState", which: str):
+        self._owner, self._which = owner, which
+
+    def _store(self) -> dict:
+        return self._owner._m if self._which == "m" else self._owner._v
+
+    def __getitem__(self, key):
+        return self._store()[key].cpu().numpy().copy()
+
+    def __setitem__(self, key, value):
+        ref = self._store()[key]
+        arr = np.asarray(value, dtype=np.float64).reshape(ref.shape)
+        self._store()[key] = torch.from_numpy(np.ascontiguousarray(arr)).to(ref.device)
+
+    def __delitem__(self, key):
+        raise TypeError("moment keys are fixed")
+
+    def __iter__(self):
+        return iter(self._store())
+
+    def __len__(self):
+        return len(self._store())
+
+
+class _DeviceGrads:
+    """last_grad on device; host ParamGradients on demand."""
+
+    def __init__(self, d_p0, d_a0, d_pos):
+        self.d_p0_t, self.d_a0_t, self.d_pos_t = d_p0, d_a0, d_pos
+
+    def host(self) -> R.ParamGradients:
+        return R.ParamGradients(self.d_p0_t.cpu().numpy(), self.d_a0_t.cpu().numpy(), self.d_pos_t.cpu().numpy())
+
+
+class OptimState:
+    """Cloud plus adaptive-moment accumulators (optimizer.py:173-193), on the GPU."""
+
+    def __init__(self, cloud: PointCloud, lr: LearningRates, seed: RngSeed, step_count: int = 0,
+                 m: dict | None = None, v: dict | None = None, last_grad=None):
+        self.lr = lr
+        self.seed = seed
+        self.step_count = int(step_count)
+        self._dev = E.cuda_device()
+        self._set_cloud(cloud)
+        n = len(cloud)
+        z = lambda shape: torch.zeros(shape, dtype=torch.float64, device=self._dev)
+        self._m = {"p0": z(n), "a0": z(n), "position": z((n, 3))}
+        self._v = {"p0": z(n), "a0": z(n), "position": z((n, 3))}
+        for src, dst in ((m, self._m), (v, self._v)):
+            for k, arr in (src or {}).items():
+                dst[k] = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).to(self._dev)
+        self._last = None
+        if last_grad is not None:
+            self.last_grad = last_grad
+
+    # -- cloud ------------------------------------------------------------
+    def _set_cloud(self, cloud: PointCloud) -> None:
+        self._dc = E.DeviceCloud.from_host(cloud.positions, cloud.p0, cloud.a0, self._dev)
+        self._a0_free = np.asarray(cloud.a0_free, dtype=np.float64).copy()
+        self._generation = int(cloud.generation)
+        self._host_cache = None
+
+    @property
+    def cloud(self) -> PointCloud:
+        if self._host_cache is None:
+            dc = self._dc
+            self._host_cache = PointCloud(dc.pos.cpu().numpy(), dc.p0.cpu().numpy(), dc.a0.cpu().numpy(),
+                                          self._a0_free.copy(), self._generation)
+        return self._host_cache
+
+    @cloud.setter
+    def cloud(self, value: PointCloud) -> None:
+        self._set_cloud(value)
+
+    @property
+    def n(self) -> int:
+        return self._dc.n
+
+    @property
+    def m(self):
+        return _DeviceMoments(self, "m")
+
+    @property
+    def v(self):
+        return _DeviceMoments(self, "v")
+
+    @property
+    def last_grad(self):
+        return None if self._last is None else self._last.host()
+
+    @last_grad.setter
+    def last_grad(self, g) -> None:
+        if g is None:
+            self._last = None
+            return
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(self._dev)
+        self._last = _DeviceGrads(t(g.d_p0), t(g.d_a0), t(g.d_position))
+
+    def _touched(self, resort: bool = False) -> None:
+        self._host_cache = None
+        self._dc.invalidate(resort=resort)
+
+
+def create_state(cloud: PointCloud, lr: LearningRates | None = None, seed=0) -> OptimState:
+    if not isinstance(seed, RngSeed):
+        seed = RngSeed(seed)
+    return OptimState(cloud=cloud, lr=lr or LearningRates(), seed=seed)
+
+
+# ---------------------------------------------------------------------------
+# Zero-gradient filtering (optimizer.py:217-258)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class FilterReport:
+    g: np.ndarray
+    n_input: int
+    n_retained: int
+
+    @property
+    def no_evidence(self) -> bool:
+        return self.n_retained == 0
+
+
+def _compact_indices(key: torch.Tensor, mode: int) -> torch.Tensor:
+    """Ascending indices i with key[i] < 0 (mode 0) / <= 0 (mode 1) / != 0 (mode 2)."""
+    n = key.numel()
+    dev = key.device
+    ws = E.workspace(dev)
+    idx = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    count = ws.get("compact_count", 1, torch.int32)
+    scratch = ws.get("compact_ws", int(_lib.load().pab_compact_workspace_bytes(n)) // 4 + 1, torch.int32)
+    call("pab_compact", ptr(key), n, mode, ptr(idx), ptr(count), ptr(scratch), E._stream())
+    return idx[: int(count.item())]
+
+
+def filter_gradient(dc: E.DeviceCloud, det: E.DeviceDetectors, acq: E.Acq, real_local: torch.Tensor,
+                    counters: E.PassCounters) -> torch.Tensor:
+    """g_i = dL/dp0 at p0 = 0: forward rows vanish, res = -real exactly."""
+    n_total = det.n_total * acq.n_out
+    d_p0, _, _ = E.adjoint_grads(dc, det, acq, real_local, -1.0, 0, 2.0 / n_total, counters, count_ops=True)
+    return d_p0
+
+
+def zero_gradient_filter(cloud, ctx, real, f: int, strict: bool = True):
+    """Keep only balls whose pressure wants to grow away from zero."""
+    if len(cloud) == 0:
+        raise ValueError("cannot filter an empty cloud")
+    if f < 1:
+        raise ValueError(f"decimation factor must be >= 1, got {f}")
+    if np.any(np.asarray(cloud.a0) <= 0.0):
+        raise ValueError("all a0 must be > 0 for forward simulation")
+    real_k = R.downsample(real, f) if f > 1 else real
+    det = R.device_detectors(ctx)
+    dev = det.pos.device
+    acq = R._acq(ctx, f)
+    if real_k.data.shape[1] != acq.n_out:
+        raise ValueError(f"supervision has {real_k.data.shape[1]} samples, expected {acq.n_out} at factor {f}")
+    dc = E.DeviceCloud.from_host(cloud.positions, np.zeros(len(cloud)), cloud.a0, dev)
+    counters = E.PassCounters(dev)
+    g = filter_gradient(dc, det, acq, R.device_supervision(real_k.data, det), counters)
+    idx = _compact_indices(g, 0 if strict else 1)
+    R._add_ops(counters.read())
+    keep = idx.cpu().numpy().astype(np.int64)
+    retained = cloud.subset(keep) if isinstance(cloud, PointCloud) else type(cloud).subset(cloud, keep)
+    return retained, FilterReport(g=g.cpu().numpy(), n_input=len(cloud), n_retained=len(retained))
+
+
+# ---------------------------------------------------------------------------
+# One optimisation step (optimizer.py:266-306)
+# ---------------------------------------------------------------------------
+
+
+def _adam_(param: torch.Tensor, grad: torch.Tensor, m: torch.Tensor, v: torch.Tensor, lr: float, t: int,
+           floor: float | None = None) -> None:
+    bc1 = 1.0 - _ADAM_BETA1 ** t
+    bc2 = 1.0 - _ADAM_BETA2 ** t
+    call("pab_adam", ptr(param), ptr(grad), ptr(m), ptr(v), param.numel(), float(lr), bc1, bc2,
+         float(floor if floor is not None else 0.0), 1 if floor is not None else 0, E._stream())
+
+
+def _device_step(state: OptimState, det: E.DeviceDetectors, acq: E.Acq, real_local: torch.Tensor,
+                 stage: str) -> float:
+    dc = state._dc
+    counters = E.PassCounters(dc.dev)
+    res, loss_rows = E.forward_rows(dc, det, acq, counters, real_local=real_local)
+    n_total = det.n_total * acq.n_out
+    stage_code = 2 if stage == "fine" else 1
+    d_p0, d_a0, d_pos = E.adjoint_grads(dc, det, acq, res, 1.0, stage_code, 2.0 / n_total, counters)
+    loss_sum = float(loss_rows.sum().item())
+    if det.shard.world > 1:
+        loss_sum = E.allreduce_scalar(loss_sum, dc.dev)
+    loss_value = loss_sum / n_total
+    status = int(counters.status.item())
+    if status & E.STATUS_COINCIDENT:
+        raise SimulationError("ball coincident with a sensor (zero source-sensor distance)")
+    if not math.isfinite(loss_value) or status & E.STATUS_NONFINITE:
+        raise OptimizationError(
+            f"non-finite loss or gradient at step {state.step_count}: loss={loss_value}, "
+            f"balls={dc.n}, p0 range=({float(dc.p0.min())}, {float(dc.p0.max())}), "
+            f"a0 range=({float(dc.a0.min())}, {float(dc.a0.max())})")
+    R._add_ops(int(counters.ops.item()))
+    state.step_count += 1
+    t = state.step_count
+    _adam_(dc.p0, d_p0, state._m["p0"], state._v["p0"], state.lr.p0, t)
+    _adam_(dc.a0, d_a0, state._m["a0"], state._v["a0"], state.lr.a0, t, floor=_A0_RUNTIME_FLOOR)
+    if stage == "fine":
+        _adam_(dc.pos, d_pos, state._m["position"], state._v["position"], state.lr.position, t)
+    state._last = _DeviceGrads(d_p0, d_a0, d_pos)
+    state._touched()
+    return loss_value
+
+
+def step(state: OptimState, ctx, real_k, f: int, stage: str):
+    """One adaptive-moment update; returns (state, pre-update loss)."""
+    expected = ctx.grid.decimated(f).n_samples if f > 1 else ctx.grid.n_samples
+    if real_k.data.shape[1] != expected:
+        raise ValueError(f"supervision not decimated to factor {f}: has {real_k.data.shape[1]} samples, "
+                         f"expected {expected}")
+    if stage not in ("coarse", "fine"):
+        raise ValueError(f"stage must be 'coarse' or 'fine', got {stage!r}")
+    det = R.device_detectors(ctx)
+    acq = R._acq(ctx, f)
+    if state.n == 0:
+        raise OptimizationError("all points destroyed")
+    loss_value = _device_step(state, det, acq, R.device_supervision(real_k.data, det), stage)
+    return state, loss_value
+
+
+# ---------------------------------------------------------------------------
+# Adaptive density control (optimizer.py:314-406)
+# ---------------------------------------------------------------------------
+
+
+def density_control(state: OptimState, thresholds: DensityThresholds, stage: str) -> OptimState:
+    """Destroy weak / out-of-range balls, split oversized ones, duplicate the
+    top decile by position-gradient norm (fine).  Runs every 100-200
+    iterations on the host copies (O(n)); SplitMix64 streams are bit-exact
+    with the reference (CounterRng.spawn(generation))."""
+    n = state.n
+    if n == 0:
+        state._generation += 1
+        state._host_cache = None
+        return state
+    dc = state._dc
+    pos_all, p0_all, a0_all = dc.pos.cpu().numpy(), dc.p0.cpu().numpy(), dc.a0.cpu().numpy()
+    m_h = {k: t.cpu().numpy() for k, t in state._m.items()}
+    v_h = {k: t.cpu().numpy() for k, t in state._v.items()}
+    rng = CounterRng(state.seed).spawn(state._generation)
+    median_p0 = float(np.median(p0_all))
+    weak = p0_all < thresholds.destroy_p0_frac * median_p0
+    bad = (a0_all < thresholds.a0_min) | (a0_all > thresholds.a0_max)
+    surv = np.flatnonzero(~(weak | bad))
+    pos, p0, a0, free = pos_all[surv], p0_all[surv], a0_all[surv], state._a0_free[surv]
+    m = {k: x[surv] for k, x in m_h.items()}
+    v = {k: x[surv] for k, x in v_h.items()}
+    gnorm = None
+    if state._last is not None:
+        gnorm = np.linalg.norm(state._last.d_pos_t.cpu().numpy(), axis=1)[surv]
+    split = a0 > thresholds.split_a0
+    sidx = np.flatnonzero(split)
+    parts = [[pos[~split]], [p0[~split]], [a0[~split]], [free[~split]]]
+    if sidx.size:
+        off = 0.5 * a0[sidx, None] * rng.unit_vectors(sidx.size)
+        parts[0].append(np.concatenate([pos[sidx] + off, pos[sidx] - off]))
+        parts[1].append(np.concatenate([0.5 * p0[sidx]] * 2))
+        parts[2].append(np.concatenate([a0[sidx] / math.sqrt(2.0)] * 2))
+        parts[3].append(np.concatenate([free[sidx]] * 2))
+    m = {k: x[~split] for k, x in m.items()}
+    v = {k: x[~split] for k, x in v.items()}
+    if stage == "fine" and gnorm is not None and gnorm[~split].size:
+        gn = gnorm[~split]
+        k_dup = min(math.ceil((1.0 - thresholds.duplicate_grad_quantile) * gn.size), gn.size)
+        if k_dup > 0:
+            order = np.sort(np.argsort(-gn, kind="stable")[:k_dup])
+            kp = (parts[0][0], parts[1][0], parts[2][0], parts[3][0])
+            jitter = (kp[2][order, None] / 4.0) * rng.unit_vectors(order.size)
+            parts[0].append(kp[0][order] + jitter)
+            parts[1].append(kp[1][order])
+            parts[2].append(kp[2][order])
+            parts[3].append(kp[3][order])
+    n_kept = parts[0][0].shape[0]
+    new = PointCloud(np.concatenate(parts[0]), np.concatenate(parts[1]), np.concatenate(parts[2]),
+                     np.concatenate(parts[3]), generation=state._generation + 1)
+    n_new = len(new)
+    state._set_cloud(new)
+    for key in _KEYS:
+        fresh = (n_new - n_kept,) + m[key].shape[1:]
+        up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(state._dev)
+        state._m[key] = up(np.concatenate([m[key], np.zeros(fresh)]))
+        state._v[key] = up(np.concatenate([v[key], np.zeros(fresh)]))
+    state._last = None
+    return state
+
+
+# ---------------------------------------------------------------------------
+# Hierarchical driver (optimizer.py:414-500)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class TraceRecord:
+    step: int
+    time_s: float
+    loss: float
+    ball_count: int
+    level: int
+
+
+@dataclass
+class IterationTrace:
+    records: list = field(default_factory=list)
+
+    def record(self, step: int, time_s: float, loss: float, ball_count: int, level: int) -> None:
+        if self.records and step <= self.records[-1].step:
+            raise ValueError("trace steps must increase monotonically")
+        self.records.append(TraceRecord(step, time_s, loss, ball_count, level))
+
+    def to_csv(self, path) -> None:
+        with open(path, "w", encoding="utf-8") as fh:
+            fh.write("step,time_s,loss,ball_count,level\n")
+            for r in self.records:
+                fh.write(f"{r.step},{r.time_s:.6f},{r.loss:.12g},{r.ball_count},{r.level}\n")
+
+    @classmethod
+    def from_csv(cls, path) -> "IterationTrace":
+        trace = cls()
+        with open(path, "r", encoding="utf-8") as fh:
+            header = fh.readline().strip()
+            if header != "step,time_s,loss,ball_count,level":
+                raise ValueError(f"unexpected trace header: {header!r}")
+            for line in fh:
+                s, t, l, b, lv = line.strip().split(",")
+                trace.record(int(s), float(t), float(l), int(b), int(lv))
+        return trace
+
+
+def _filter_state_(state: OptimState, det, acq, real_local, strict: bool = True) -> None:
+    """Builder-defined periodic filter (config 3): reference predicate on the
+    current cloud at the current factor; survivors keep params and moments."""
+    dc = state._dc
+    probe = E.DeviceCloud(dc.pos, torch.zeros_like(dc.p0), dc.a0)
+    probe.perm = dc.perm
+    counters = E.PassCounters(dc.dev)
+    g = filter_gradient(probe, det, acq, real_local, counters)
+    counters.read()
+    idx = _compact_indices(g, 0 if strict else 1)
+    m = idx.numel()
+    if m == state.n:
+        return
+    ws_gather = lambda src, width: _gather(src, width, idx)
+    new = E.DeviceCloud(ws_gather(dc.pos, 3).view(m, 3), ws_gather(dc.p0, 1), ws_gather(dc.a0, 1))
+    state._dc = new
+    for d in (state._m, state._v):
+        d["p0"] = ws_gather(d["p0"], 1)
+        d["a0"] = ws_gather(d["a0"], 1)
+        d["position"] = ws_gather(d["position"], 3).view(m, 3)
+    keep = idx.cpu().numpy()
+    state._a0_free = state._a0_free[keep]
+    state._host_cache = None
+    state._last = None
+
+
+def _gather(src: torch.Tensor, width: int, idx: torch.Tensor) -> torch.Tensor:
+    m = idx.numel()
+    out = torch.empty(m * width, dtype=torch.float64, device=src.device)
+    call("pab_gather_f64", ptr(src.contiguous()), width, ptr(idx), m, ptr(out), E._stream())
+    return out
+
+
+def run_hierarchical(init: PointCloud, ctx, real, schedule: Schedule, thresholds: DensityThresholds, *,
+                     lr: LearningRates | None = None, seed=0, callback=None, state: OptimState | None = None,
+                     filter_every: int | None = None, plateau: bool = True):
+    """Every schedule level in order on progressively finer supervision.
+
+    Extensions (off by default = reference behaviour): ``filter_every`` applies
+    the zero-gradient filter to the live cloud every k iterations (BASELINE
+    config 3); ``plateau=False`` disables the 50-iteration plateau stop.
+    """
+    if state is None:
+        state = create_state(init.copy(), lr=lr, seed=seed)
+    trace = IterationTrace()
+    t_start = time.perf_counter()
+    det = R.device_detectors(ctx)
+    full = R.device_supervision(real.data, det)
+    global_step = 0
+    for li, level in enumerate(schedule.levels):
+        if state.n == 0:
+            raise OptimizationError("all points destroyed")
+        acq = R._acq(ctx, level.f)
+        real_local = full if level.f == 1 else E.decimate_rows(full, level.f)
+        period = _COARSE_DENSITY_EVERY if level.stage == "coarse" else schedule.duplication_period
+        losses = []
+        for it in range(level.max_iters):
+            loss_value = _device_step(state, det, acq, real_local, level.stage)
+            global_step += 1
+            losses.append(loss_value)
+            trace.record(global_step, time.perf_counter() - t_start, loss_value, state.n, li)
+            if callback is not None:
+                callback(state, global_step, li, loss_value)
+            if filter_every and (it + 1) % filter_every == 0:
+                _filter_state_(state, det, acq, real_local)
+                if state.n == 0:
+                    raise OptimizationError("all points destroyed")
+            if (it + 1) % period == 0:
+                state = density_control(state, thresholds, level.stage)
+                if state.n == 0:
+                    raise OptimizationError("all points destroyed")
+            if plateau and len(losses) > _PLATEAU_WINDOW:
+                past = losses[-1 - _PLATEAU_WINDOW]
+                if abs(past - loss_value) < _PLATEAU_REL * max(abs(past), 1e-300):
+                    break
+    return state.cloud, trace

@@ -1,0 +1,399 @@
+"""GPU parity of the forward/adjoint against the FP64 oracle and the
+reference's golden vectors, plus the reference's own radiator tests
+(reference pkg/tests/test_radiator.py) re-run on the CUDA path.
+
+Tolerances (north_star, BASELINE.json): signals relative L2 <= 1e-4,
+gradients relative L2 <= 1e-3.  Where the reference asserts FP64 exactness
+the FP32 bound is stated next to the assertion.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import radiator as OR
+from pab_helpers import golden, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+SIG_TOL = 1e-4
+GRAD_TOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2601_00551_b200 as P
+    return P
+
+
+def single_ball_ctx(P):
+    cloud = P.PointCloud([[0.0, 0.0, 0.0]], [1.0], [0.5e-3])
+    array = P.SensorArray(positions=[[0.03, 0.0, 0.0]], sound_speed=1500.0)
+    return cloud, P.ForwardContext(array, P.TimeGrid(0.0, 1e-8, 4096))
+
+
+def seeded_instance(P, key="cand"):
+    g = golden("radiator.npz")
+    array = P.SensorArray(g["si_sensors"], 1500.0, normals=g["si_normals"])
+    ctx = P.ForwardContext(array, P.TimeGrid(0.0, 5e-8, 256))
+    cand = P.PointCloud(g["si_cand_pos"], g["si_cand_p0"], g["si_cand_a0"])
+    truth = P.PointCloud(g["si_true_pos"], g["si_true_p0"], g["si_true_a0"])
+    real = P.SignalSet(ctx.grid, g["si_real"])
+    return ctx, cand, truth, real, g
+
+
+# ----------------------------------------------------------------- forward
+
+class TestSimulate:
+    def test_empty_cloud_all_zero(self, P):
+        _, ctx = single_ball_ctx(P)
+        out = P.simulate_signals(P.PointCloud.empty(), ctx)
+        assert not out.data.any() and out.data.shape == (1, 4096)
+
+    def test_n_shape_zero_crossing_and_symmetry(self, P):
+        cloud, ctx = single_ball_ctx(P)
+        s = P.simulate_signals(cloud, ctx).data[0]
+        assert abs(s[2000]) < 1e-10
+        i_hi, i_lo = np.argmax(s), np.argmin(s)
+        assert i_hi < 2000 < i_lo
+        assert abs((i_hi + i_lo) / 2 - 2000) <= 1.0
+
+    def test_matches_closed_form(self, P):
+        cloud, ctx = single_ball_ctx(P)
+        s = P.simulate_signals(cloud, ctx).data[0]
+        ref = OR.single_ball_kernel(0.03, 1.0, 0.5e-3, ctx.grid.times(), 1500.0)
+        # reference: atol 1e-13*max in FP64; FP32 per-sample math: 2e-6*max
+        np.testing.assert_allclose(s, ref, rtol=0, atol=2e-6 * np.abs(ref).max())
+        assert rel_l2(s, ref) < 1e-6
+        assert rel_l2(s, golden("radiator.npz")["single_rows"][0]) < 1e-6
+
+    def test_p0_linearity_exact(self, P):
+        cloud, ctx = single_ball_ctx(P)
+        s1 = P.simulate_signals(cloud, ctx).data
+        doubled = cloud.copy()
+        doubled.p0 *= 2.0
+        np.testing.assert_array_equal(P.simulate_signals(doubled, ctx).data, 2.0 * s1)
+
+    def test_superposition(self, P):
+        ctx, cloud, truth, _, _ = seeded_instance(P)
+        both = P.PointCloud.concatenate([cloud, truth])
+        s_both = P.simulate_signals(both, ctx).data
+        s_sum = P.simulate_signals(cloud, ctx).data + P.simulate_signals(truth, ctx).data
+        # reference 1e-9*scale (FP64); FP32 summation: 1e-6*scale
+        np.testing.assert_allclose(s_both, s_sum, rtol=0, atol=1e-6 * np.abs(s_both).max())
+
+    def test_radial_shift_moves_arrival(self, P):
+        cloud, ctx = single_ball_ctx(P)
+        s0 = P.simulate_signals(cloud, ctx).data[0]
+        moved = cloud.copy()
+        moved.positions[0, 0] -= 3e-3
+        s1 = P.simulate_signals(moved, ctx).data[0]
+        shift = np.argmax(np.correlate(s1, s0, mode="full")) - (len(s0) - 1)
+        assert abs(shift - 3e-3 / (1500.0 * 1e-8)) <= 1.0
+
+    def test_truncation_insensitivity(self, P):
+        ctx, cloud, _, _, _ = seeded_instance(P)
+        wide = P.ForwardContext(ctx.array, ctx.grid, cutoff_sigma=12.0)
+        s6 = P.simulate_signals(cloud, ctx).data
+        s12 = P.simulate_signals(cloud, wide).data
+        diff = np.abs(s12 - s6)
+        bound = 6.0 * np.exp(-18.0) / np.exp(-0.5)
+        # reference bound plus FP32 summation noise (2e-6 of peak)
+        assert diff.max() <= (bound + 2e-6) * np.abs(s12).max()
+        assert np.linalg.norm(diff) <= 2e-6 * np.linalg.norm(s12)
+
+    def test_ball_on_sensor_rejected(self, P):
+        array = P.SensorArray(positions=[[0.0, 0.0, 0.0]])
+        ctx = P.ForwardContext(array, P.TimeGrid(0.0, 1e-8, 16))
+        with pytest.raises(P.SimulationError):
+            P.simulate_signals(P.PointCloud([[0.0, 0.0, 0.0]], [1.0], [1e-3]), ctx)
+
+    def test_nonpositive_a0_rejected(self, P):
+        _, ctx = single_ball_ctx(P)
+        with pytest.raises(ValueError):
+            P.simulate_signals(P.PointCloud([[0, 0, 0]], [1.0], [0.0]), ctx)
+
+    def test_cutoff_sigma_floor(self, P):
+        _, ctx = single_ball_ctx(P)
+        with pytest.raises(ValueError):
+            P.ForwardContext(ctx.array, ctx.grid, cutoff_sigma=3.0)
+
+    def test_seeded_forward_matches_golden(self, P):
+        ctx, cloud, _, _, g = seeded_instance(P)
+        assert rel_l2(P.simulate_signals(cloud, ctx).data, g["si_cand_rows"]) < SIG_TOL
+        assert rel_l2(P.simulate_signals(cloud, P.ForwardContext(ctx.array, ctx.grid, 12.0)).data,
+                      g["si_cand_rows_cut12"]) < SIG_TOL
+
+    @pytest.mark.parametrize("f", [2, 4, 16])
+    def test_decimated_forward_matches_golden(self, P, f):
+        ctx, cloud, _, _, g = seeded_instance(P)
+        out = P.simulate_at_rate(cloud, ctx, f)
+        assert out.grid == ctx.grid.decimated(f)
+        assert rel_l2(out.data, g[f"si_cand_rows_f{f}"]) < SIG_TOL
+
+    def test_near_field_u_plus_term(self, P):
+        """Ball within the truncated support of a detector: the u+ term
+        (reference radiator.py:197-208) must be included."""
+        pos = np.array([[0.4e-3, 0.0, 0.0], [2e-3, 1e-3, 0.0]])
+        array = P.SensorArray(positions=[[0.0, 0.0, 0.0], [5e-3, 0.0, 0.0]])
+        ctx = P.ForwardContext(array, P.TimeGrid(0.0, 2e-8, 400))
+        cloud = P.PointCloud(pos, [1.0, 0.7], [0.2e-3, 0.15e-3])
+        got = P.simulate_signals(cloud, ctx).data
+        want, _, _, _ = OR.run_model(pos, [1.0, 0.7], [0.2e-3, 0.15e-3], array.positions, None,
+                                     1500.0, 0.0, 2e-8, 400, 1)
+        assert rel_l2(got, want) < SIG_TOL
+
+
+class TestLoss:
+    def test_perfect_match(self, P):
+        _, _, _, real, _ = seeded_instance(P)
+        assert P.loss(real, real) == 0.0
+
+    def test_constant_offset(self, P):
+        _, _, _, real, _ = seeded_instance(P)
+        shifted = P.SignalSet(real.grid, real.data + 0.25)
+        assert abs(P.loss(shifted, real) - 0.0625) < 1e-15
+
+    def test_matches_two_pass_oracle(self, P):
+        rng = P.CounterRng(55)
+        grid = P.TimeGrid(0.0, 1e-8, 300)
+        a = P.SignalSet(grid, rng.uniform(-1, 1, 1200).reshape(4, 300))
+        b = P.SignalSet(grid, rng.uniform(-1, 1, 1200).reshape(4, 300))
+        want = float(np.sum((a.data - b.data) ** 2) / 1200)
+        assert abs(P.loss(a, b) - want) <= 1e-12 * want
+
+    def test_shape_mismatch(self, P):
+        _, _, _, real, _ = seeded_instance(P)
+        with pytest.raises(ValueError):
+            P.loss(real, P.downsample(real, 2))
+
+
+class TestBackward:
+    def test_perfect_fit_zero_gradients(self, P):
+        ctx, _, truth, _, _ = seeded_instance(P)
+        real = P.simulate_signals(truth, ctx)
+        L, g = P.backward(truth, ctx, real, stage="fine")
+        assert L == 0.0
+        assert not g.d_p0.any() and not g.d_a0.any() and not g.d_position.any()
+
+    @pytest.mark.parametrize("stage", ["fine", "coarse"])
+    def test_gradients_match_golden(self, P, stage):
+        ctx, cloud, _, real, g = seeded_instance(P)
+        L, gr = P.backward(cloud, ctx, real, stage=stage)
+        assert abs(L - float(g[f"si_{stage}_loss"])) <= 1e-4 * float(g[f"si_{stage}_loss"])
+        assert rel_l2(gr.d_p0, g[f"si_{stage}_dp0"]) < GRAD_TOL
+        assert rel_l2(gr.d_a0, g[f"si_{stage}_da0"]) < GRAD_TOL
+        if stage == "fine":
+            assert rel_l2(gr.d_position, g["si_fine_dpos"]) < GRAD_TOL
+        else:
+            assert not gr.d_position.any()
+
+    def test_decimated_supervision(self, P):
+        ctx, cloud, _, real, g = seeded_instance(P)
+        L4, gr = P.backward(cloud, ctx, P.downsample(real, 4), stage="fine")
+        assert np.isfinite(L4) and L4 > 0
+        assert abs(L4 - float(g["si_f4_loss"])) <= 1e-4 * L4
+        assert rel_l2(gr.d_position, g["si_f4_dpos"]) < GRAD_TOL
+
+    def test_mismatched_grid_rejected(self, P):
+        ctx, cloud, _, real, _ = seeded_instance(P)
+        odd = P.SignalSet(P.TimeGrid(1e-7, real.grid.dt, real.grid.n_samples), real.data)
+        with pytest.raises(ValueError):
+            P.backward(cloud, ctx, odd)
+
+    def test_stage_validated(self, P):
+        ctx, cloud, _, real, _ = seeded_instance(P)
+        with pytest.raises(ValueError):
+            P.backward(cloud, ctx, real, stage="medium")
+
+    def test_above_1024_balls_matches_fixed_reference(self, P):
+        """the unfixed reference is wrong past 1024 balls; the
+        CUDA path matches the key-fixed one."""
+        g = golden("bugfix.npz")
+        ctx = P.ForwardContext(P.SensorArray(g["sensors"]), P.TimeGrid(0.0, 5e-8, 512))
+        cloud = P.PointCloud(g["pos"], g["p0"], g["a0"])
+        L, gr = P.backward(cloud, ctx, P.SignalSet(ctx.grid, g["real"]), stage="fine")
+        assert abs(L - float(g["loss"])) <= 1e-4 * L
+        assert abs(L - float(g["loss_unfixed"])) > abs(L - float(g["loss"]))
+        assert rel_l2(gr.d_p0, g["dp0"]) < GRAD_TOL
+        assert rel_l2(gr.d_a0, g["da0"]) < GRAD_TOL
+        assert rel_l2(gr.d_position, g["dpos"]) < GRAD_TOL
+
+
+class TestSimulateAtRate:
+    def test_f1_equals_full(self, P):
+        ctx, cloud, _, _, _ = seeded_instance(P)
+        np.testing.assert_array_equal(P.simulate_at_rate(cloud, ctx, 1).data, P.simulate_signals(cloud, ctx).data)
+
+    @pytest.mark.parametrize("f", [2, 4, 16])
+    def test_equals_decimated_full_rate(self, P, f):
+        # reference: bit-exact in FP64.  Here every sample's contributions are
+        # computed identically at any f (absolute-index u), but the FP32
+        # summation grouping follows the decimated tiling: bound 1e-6 of peak.
+        ctx, cloud, _, _, _ = seeded_instance(P)
+        coarse = P.simulate_at_rate(cloud, ctx, f)
+        dec = P.downsample(P.simulate_signals(cloud, ctx), f)
+        np.testing.assert_allclose(coarse.data, dec.data, rtol=0, atol=1e-6 * np.abs(dec.data).max())
+        assert coarse.grid == dec.grid
+
+    def test_cost_scales_inversely_with_factor(self, P):
+        g = golden("radiator.npz")
+        array = P.SensorArray(g["si_sensors"])
+        ctx = P.ForwardContext(array, P.TimeGrid(0.0, 5e-8, 1024))
+        cloud = P.PointCloud(g["si_cand_pos"], g["si_cand_p0"], g["si_cand_a0"])
+        costs = {}
+        for f in (1, 4):
+            P.reset_op_count()
+            P.simulate_at_rate(cloud, ctx, f)
+            costs[f] = P.op_count()
+        assert 3.0 < costs[1] / costs[4] < 5.0
+
+    def test_op_count_matches_reference(self, P):
+        ctx, cloud, _, _, g = seeded_instance(P)
+        for f, key in ((1, "si_ops_f1"), (4, "si_ops_f4")):
+            P.reset_op_count()
+            P.simulate_at_rate(cloud, ctx, f)
+            assert abs(P.op_count() - int(g[key])) <= 2
+
+    def test_ops_paused_restores_counter(self, P):
+        ctx, cloud, _, _, _ = seeded_instance(P)
+        P.reset_op_count(1234)
+        with P.ops_paused():
+            P.simulate_signals(cloud, ctx)
+        assert P.op_count() == 1234
+
+
+class TestDeterminism:
+    def test_thread_count_invariance_and_rerun_bitwise(self, P):
+        ctx, cloud, _, real, _ = seeded_instance(P)
+        saved = P.get_num_threads()
+        try:
+            P.set_num_threads(1)
+            s1 = P.simulate_signals(cloud, ctx).data
+            L1, g1 = P.backward(cloud, ctx, real, stage="fine")
+            P.set_num_threads(4)
+            s4 = P.simulate_signals(cloud, ctx).data
+            L4, g4 = P.backward(cloud, ctx, real, stage="fine")
+        finally:
+            P.set_num_threads(saved)
+        np.testing.assert_array_equal(s1, s4)
+        assert L1 == L4
+        np.testing.assert_array_equal(g1.d_p0, g4.d_p0)
+        np.testing.assert_array_equal(g1.d_position, g4.d_position)
+
+    def test_cloud_order_only_changes_rounding(self, P):
+        ctx, cloud, _, real, _ = seeded_instance(P)
+        perm = np.arange(len(cloud))[::-1].copy()
+        L1, g1 = P.backward(cloud, ctx, real)
+        L2, g2 = P.backward(cloud.subset(perm), ctx, real)
+        assert abs(L1 - L2) <= 1e-6 * L1
+        assert rel_l2(g2.d_position, g1.d_position[perm]) < 1e-5
+
+
+# ----------------------------------------------------------- directivity
+
+def _oracle_backward(pos, p0, a0, sens, normals, grid, real, stage, kind):
+    return OR.run_model(pos, p0, a0, sens, normals, 1500.0, grid.t0, grid.dt, grid.n_samples, 1,
+                        real=real, stage=stage, kind=kind)
+
+
+@pytest.mark.parametrize("kind", [("cos_power", 2.0), ("cos_power", 3.0), ("element", 5e-4)])
+def test_directivity_forward_and_gradients_match_oracle(P, kind):
+    ctx, cloud, truth, _, g = seeded_instance(P)
+    d = P.Directivity(kind[0], power=kind[1] if kind[0] == "cos_power" else 2.0,
+                      width=kind[1] if kind[0] == "element" else 5e-4)
+    dctx = P.ForwardContext(ctx.array, ctx.grid, directivity=d)
+    rows, _, _, _ = OR.run_model(truth.positions, truth.p0, truth.a0, ctx.array.positions, ctx.array.normals,
+                                 1500.0, 0.0, 5e-8, 256, 1, kind=kind)
+    sim = P.simulate_signals(truth, dctx)
+    assert rel_l2(sim.data, rows) < SIG_TOL
+    real = P.SignalSet(ctx.grid, rows)
+    _, L, (gp0, ga0, gpos), _ = _oracle_backward(cloud.positions, cloud.p0, cloud.a0, ctx.array.positions,
+                                                 ctx.array.normals, ctx.grid, rows, "fine", kind)
+    Lg, gr = P.backward(cloud, dctx, real, stage="fine")
+    assert abs(Lg - L) <= 1e-4 * L
+    assert rel_l2(gr.d_p0, gp0) < GRAD_TOL
+    assert rel_l2(gr.d_a0, ga0) < GRAD_TOL
+    assert rel_l2(gr.d_position, gpos) < GRAD_TOL
+
+
+def test_directivity_none_equals_default(P):
+    ctx, cloud, _, real, _ = seeded_instance(P)
+    a = P.simulate_signals(cloud, ctx).data
+    b = P.simulate_signals(cloud, P.ForwardContext(ctx.array, ctx.grid, directivity=P.Directivity("none"))).data
+    np.testing.assert_array_equal(a, b)
+
+
+# ----------------------------------------------------------- configs
+
+def _toy(P, kind=("none",)):
+    from paper_2601_00551_b200 import scenes
+    sc = scenes.toy_config()
+    d = P.Directivity("none") if kind[0] == "none" else P.Directivity(kind[0], power=kind[1])
+    return sc, P.ForwardContext(sc.array, sc.grid, directivity=d)
+
+
+def test_toy_forward_matches_reference(P):
+    g = golden("toy.npz")
+    sc, ctx = _toy(P)
+    assert rel_l2(P.simulate_signals(sc.truth, ctx).data, g["real"]) < SIG_TOL
+
+
+def test_toy_filter_keeps_reference_set(P):
+    """32^3 grid filter at f=1: the surviving set equals the reference's."""
+    g = golden("toy.npz")
+    sc, ctx = _toy(P)
+    kept, rep = P.zero_gradient_filter(sc.init, ctx, P.SignalSet(ctx.grid, g["real"]), f=1)
+    want = g["filter_g"] < 0
+    got = rep.g < 0
+    flips = int(np.count_nonzero(got != want))
+    assert flips == 0, f"{flips} filter decisions differ"
+    assert rep.n_retained == int(g["n_kept"]) == len(kept)
+    assert rel_l2(rep.g, g["filter_g"]) < GRAD_TOL
+
+
+@pytest.mark.parametrize("kind", [("none",), ("cos_power", 2.0)])
+def test_toy_backward_matches_oracle(P, kind):
+    sc, ctx = _toy(P, kind)
+    truth = sc.truth
+    real, _, _, _ = OR.run_model(truth.positions, truth.p0, truth.a0, sc.array.positions, sc.array.normals,
+                                 1500.0, 0.0, sc.grid.dt, 1024, 1, kind=kind, threads=4)
+    got = P.simulate_signals(truth, ctx).data
+    assert rel_l2(got, real) < SIG_TOL
+    rng = np.random.default_rng(7)
+    sel = rng.choice(len(sc.init), 3000, replace=False)
+    cand = sc.init.subset(np.sort(sel))
+    _, L, (gp0, ga0, gpos), _ = OR.run_model(cand.positions, cand.p0, cand.a0, sc.array.positions,
+                                             sc.array.normals, 1500.0, 0.0, sc.grid.dt, 1024, 1, real=real,
+                                             stage="fine", kind=kind, threads=4)
+    Lg, gr = P.backward(cand, ctx, P.SignalSet(ctx.grid, real), stage="fine")
+    assert abs(Lg - L) <= 1e-4 * L
+    assert rel_l2(gr.d_p0, gp0) < GRAD_TOL
+    assert rel_l2(gr.d_a0, ga0) < GRAD_TOL
+    assert rel_l2(gr.d_position, gpos) < GRAD_TOL
+
+
+def test_microbench_slice_matches_oracle(P):
+    """Config 2 shapes (40 MHz x 4096, a0 ~ U[0.05, 0.2] mm, cos^2) on a
+    20k-ball x 64-detector slice the oracle finishes in seconds."""
+    from paper_2601_00551_b200 import scenes
+    sc = scenes.microbench_config(n_balls=20000, n_det=1024)
+    sens = sc.array.positions[::16]
+    nrm = sc.array.normals[::16]
+    arr = P.SensorArray(sens, 1500.0, normals=nrm)
+    ctx = P.ForwardContext(arr, sc.grid, directivity=P.Directivity("cos_power", power=2.0))
+    t = sc.truth
+    kind = ("cos_power", 2.0)
+    real, _, _, ops = OR.run_model(t.positions, t.p0, t.a0, sens, nrm, 1500.0, 0.0, sc.grid.dt, 4096, 1,
+                                   kind=kind, threads=8)
+    P.reset_op_count()
+    got = P.simulate_signals(t, ctx).data
+    assert rel_l2(got, real) < SIG_TOL
+    assert abs(P.op_count() - ops) <= 1e-4 * ops
+    c = sc.init
+    _, L, (gp0, ga0, gpos), _ = OR.run_model(c.positions, c.p0, c.a0, sens, nrm, 1500.0, 0.0, sc.grid.dt, 4096,
+                                             1, real=real, stage="fine", kind=kind, threads=8)
+    Lg, gr = P.backward(c, ctx, P.SignalSet(sc.grid, real), stage="fine")
+    assert abs(Lg - L) <= 1e-4 * L
+    assert rel_l2(gr.d_p0, gp0) < GRAD_TOL
+    assert rel_l2(gr.d_a0, ga0) < GRAD_TOL
+    assert rel_l2(gr.d_position, gpos) < GRAD_TOL
