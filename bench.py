@@ -1,0 +1,322 @@
+"""Benchmark of the forward + adjoint hot path (BASELINE.json metric).
+
+Workload: BASELINE config 2 ("microbench"): 1,000,000 balls uniform in a
+20 mm cube, a0 ~ U[0.05, 0.2] mm, 1024 detectors on a jittered ellipsoid cap
+with cos^2 directivity, 40 MHz x 4096 samples; seeded synthetic inputs
+(paper_2601_00551_b200.scenes).  One step = one fine backward pass = forward
+rows + residual/loss + adjoint + gradient finalisation (+ NCCL all-reduce of
+the per-ball gradients for N > 1).  Metric: ball-detector pair evaluations
+per second, pairs = N_balls x N_detectors per step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Under torchrun each rank owns a contiguous detector block (strong scaling:
+the configuration is fixed, the per-GPU work shrinks as 1/N).
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ball-detector pair evals/s (fwd+adjoint) per iteration"
+UNIT = "pairs/s"
+FLOPS_FWD = 7      # per in-window sample
+FLOPS_ADJ_FINE = 12
+EX2_PER_SAMPLE = 1
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n-balls", type=int, default=1_000_000)
+    ap.add_argument("--n-det", type=int, default=1024)
+    ap.add_argument("--n-samples", type=int, default=4096)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-balls", type=int, default=20000, help="oracle sample: balls x 64 detectors")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def config_dict(args, world):
+    return {"workload": "config2-microbench: fwd+fine-adjoint", "n_balls": args.n_balls,
+            "n_detectors": args.n_det, "n_samples": args.n_samples, "sampling_hz": 40e6,
+            "a0_mm": [0.05, 0.2], "directivity": "cos^2", "parallelism": f"detector-shard x{world}",
+            "l2": "flushed between timed steps (256 MiB write)", "inputs": "device-resident"}
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (B200_PROFILING.md recipe)
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle port of the reference algorithm) on a bounded sample
+# ---------------------------------------------------------------------------
+
+def cpu_reference_pairs_per_s(scene, n_sample: int, steps: int = 1, threads: int | None = None,
+                              n_det: int = 64):
+    """SURVEY.md §6 microbench slice: a strided ball subset x a strided
+    detector subset of config 2 (pairs/s is linear in N*J*W)."""
+    from oracle import radiator as OR   # the reference's CPU algorithm (restated); baseline only
+    threads = threads or os.cpu_count() or 1
+    c, t = scene.init, scene.truth
+    stride = max(1, scene.array.positions.shape[0] // n_det)
+    sens, nrm = scene.array.positions[::stride], scene.array.normals[::stride]
+    kind = ("cos_power", 2.0)
+    sel = np.linspace(0, len(c) - 1, n_sample).astype(np.int64)
+    real, _, _, _ = OR.run_model(t.positions[sel], t.p0[sel], t.a0[sel], sens, nrm, 1500.0, 0.0, scene.grid.dt,
+                                 scene.grid.n_samples, 1, kind=kind, threads=threads)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        OR.run_model(c.positions[sel], c.p0[sel], c.a0[sel], sens, nrm, 1500.0, 0.0, scene.grid.dt,
+                     scene.grid.n_samples, 1, real=real, stage="fine", kind=kind, threads=threads)
+        times.append(time.perf_counter() - t0)
+    pairs = n_sample * sens.shape[0]
+    return pairs / min(times), threads, f"{n_sample} balls (strided subset) x {sens.shape[0]} detectors, " \
+                                        f"fine backward (fwd+adj), best of {steps}"
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from paper_2601_00551_b200 import scenes
+    scene = scenes.microbench_config(n_balls=args.n_balls, n_det=args.n_det, n_samples=args.n_samples)
+    vals = []
+    for _ in range(args.warmup + args.steps):
+        v, cores, sample = cpu_reference_pairs_per_s(scene, args.cpu_balls, steps=1)
+        vals.append(v)
+    v = statistics.median(vals[args.warmup:]) if args.steps else vals[-1]
+    ms = args.n_balls * args.n_det / v * 1e3
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded CounterRng, BASELINE config 2)",
+            "config": config_dict(args, world), "impl": "reference",
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": "reference CPU algorithm = oracle/radiator.py (FP64 numpy port of paball radiator, "
+                    "key-fixed); ms_per_step extrapolated linearly to the full N*J"}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# Our arm
+# ---------------------------------------------------------------------------
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    import paper_2601_00551_b200 as P
+    from paper_2601_00551_b200 import engine as E
+    from paper_2601_00551_b200 import radiator as R
+    from paper_2601_00551_b200 import scenes
+
+    scene = scenes.microbench_config(n_balls=args.n_balls, n_det=args.n_det, n_samples=args.n_samples)
+    ctx = P.ForwardContext(scene.array, scene.grid, directivity=P.Directivity("cos_power", power=2.0))
+    det = R.device_detectors(ctx)
+    acq = R._acq(ctx, 1)
+    n_total = det.n_total * acq.n_out
+
+    # supervision: forward of the truth cloud, resident on device (this rank's rows)
+    truth = E.DeviceCloud.from_host(scene.truth.positions, scene.truth.p0, scene.truth.a0, dev)
+    counters = E.PassCounters(dev)
+    real_local, _ = E.forward_rows(truth, det, acq, counters)
+    real_local = real_local.clone()
+    cloud = E.DeviceCloud.from_host(scene.init.positions, scene.init.p0, scene.init.a0, dev)
+    cloud.pack()
+    res_buf = torch.empty_like(real_local)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def one_step(ev=None):
+        c = E.PassCounters(dev)
+        if ev:
+            ev[0].record(stream)
+        res, loss_rows = E.forward_rows(cloud, det, acq, c, real_local=real_local, out=res_buf)
+        if ev:
+            ev[1].record(stream)
+        g = E.adjoint_grads(cloud, det, acq, res, 1.0, 2, 2.0 / n_total, c)
+        if ev:
+            ev[2].record(stream)
+        return c, loss_rows, g
+
+    for _ in range(args.warmup):
+        c, _, _ = one_step()
+    torch.cuda.synchronize()
+    ops_per_step = c.read()
+
+    # kernel-level events: forward+residual, adjoint+finalize(+allreduce)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with sampler:
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            one_step(evs[k])
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    fwd_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    adj_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    step_ms = [e[0].elapsed_time(e[2]) for e in evs]
+    mean_step = sum(step_ms) / len(step_ms)
+    t = torch.tensor([mean_step], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    pairs = args.n_balls * det.n_total
+    value = pairs / (ms_max * 1e-3)
+
+    # end to end through the public API: host (pinned) cloud + supervision in,
+    # loss + gradients out, every step
+    e2e = None
+    if args.e2e_steps > 0:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+        host_cloud = P.PointCloud(pin(scene.init.positions), pin(scene.init.p0), pin(scene.init.a0))
+        real_full = E.full_rows(real_local, det).double().cpu()
+        host_real = P.SignalSet(scene.grid, real_full.pin_memory().numpy())
+        P.backward(host_cloud, ctx, host_real, stage="fine")
+        e2e_ms = []
+        for _ in range(args.e2e_steps):
+            R._sup_cache.clear()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            P.backward(host_cloud, ctx, host_real, stage="fine")
+            torch.cuda.synchronize()
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        tt = torch.tensor([statistics.median(e2e_ms)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        n = args.n_balls
+        h2d = n * 5 * 8 + det.n_total * acq.n_out * 8 // world * world
+        d2h = n * 5 * 8 + 8
+        e2e = {"value": pairs / (float(tt.item()) * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": float(tt.item()),
+               "path": "paper_2601_00551_b200.backward(PointCloud, ForwardContext, SignalSet, 'fine') "
+                       "with pinned host numpy inputs; supervision re-uploaded every step"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # roofline of the dominant kernel (FP32 CUDA-core bound)
+    probe = os.path.join(ROOT, "tools", "probe", "libfp32_peak.so")
+    peak_flops, peak_ex2, peak_kind = None, None, "measured (tools/probe FFMA2 chains, this GPU)"
+    try:
+        lib = ctypes.CDLL(probe)
+        fl, ex = ctypes.c_double(), ctypes.c_double()
+        if lib.probe_fp32_peak(3, ctypes.byref(fl), ctypes.byref(ex)) == 0:
+            peak_flops, peak_ex2 = fl.value, ex.value
+    except OSError:
+        pass
+    if peak_flops is None:
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        peak_flops, peak_ex2, peak_kind = sms * 256 * 1.965e9, sms * 16 * 1.965e9, "nominal at 1965 MHz"
+    fwd_mean = sum(fwd_ms) / len(fwd_ms)
+    adj_mean = sum(adj_ms) / len(adj_ms)
+    samples = ops_per_step   # in-window samples evaluated by the forward (== adjoint)
+    kern = {"forward": (fwd_mean, FLOPS_FWD * samples), "adjoint_fine": (adj_mean, FLOPS_ADJ_FINE * samples)}
+    dom = max(kern, key=lambda k: kern[k][0])
+    ach = kern[dom][1] / (kern[dom][0] * 1e-3)
+    path_flops = (FLOPS_FWD + FLOPS_ADJ_FINE) * samples / (ms_max * 1e-3)
+    roofline = {"bound": "fp32", "achieved": ach / 1e12, "peak": peak_flops / 1e12, "unit": "TFLOP/s",
+                "frac": ach / peak_flops, "traffic": None, "kernel": dom, "peak_source": peak_kind,
+                "algorithmic": f"{FLOPS_FWD if dom == 'forward' else FLOPS_ADJ_FINE} FP32 flops x "
+                               f"{samples} in-window samples per launch",
+                "path_fwd_adj": {"achieved": path_flops / 1e12, "frac": path_flops / peak_flops,
+                                 "ex2_per_s": 2 * samples / (ms_max * 1e-3), "ex2_peak": peak_ex2,
+                                 "ex2_frac": 2 * samples / (ms_max * 1e-3) / peak_ex2},
+                "kernel_ms": {"forward+residual": fwd_mean, "adjoint+finalize": adj_mean}}
+
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        v, cores, sample = cpu_reference_pairs_per_s(scene, args.cpu_balls, steps=1)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32 per-sample, f64 per-ball accumulation",
+            "data": "synthetic (seeded CounterRng, BASELINE config 2)", "config": config_dict(args, world),
+            "in_window_samples_per_step": samples, "samples_per_pair": samples / pairs,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": sampler.summary(),
+            "gpu_launches": 4 * args.steps}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

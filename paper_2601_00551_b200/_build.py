@@ -47,5 +47,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_probe() -> str:
+    """FP32/ex2 peak probe used by bench.py for the roofline denominator
+    (measurement tooling, not part of the product library)."""
+    src = os.path.join(ROOT, "tools", "probe", "fp32_peak.cu")
+    out = os.path.join(ROOT, "tools", "probe", "libfp32_peak.so")
+    cmd = [nvcc(), *ARCH, "-O3", "-shared", "-Xcompiler", "-fPIC", "-o", out, src]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("nvcc failed (probe):\n" + res.stdout + res.stderr)
+    return out
+
+
 if __name__ == "__main__":
     build(force=True, verbose=True)
