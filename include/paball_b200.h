@@ -41,14 +41,16 @@ int pab_device_info(int device, int* sm_count, int* cc_major, int* cc_minor, int
 const char* pab_last_cuda_error(void);
 int pab_record_sizes(int* ball_a, int* ball_b, int* group_meta);
 
-/* Spatial sort keys: key[i] = morton30(quantised pos[i]) << 32 | i.
+/* Processing-order sort keys: key[i] = a0_bucket << 58 | morton30(pos[i]) << 28 | i
+ * (a0 buckets: a0_buckets equal bins of [a0lo, a0hi]; n < 2^28).
  * Replaces: nothing (the reference visits balls in input order, radiator.py:185). */
-int pab_morton_keys(const double* pos /*[n][3]*/, int64_t n, double lox, double loy, double loz,
-                    double extent, int64_t* keys, void* stream);
+int pab_morton_keys(const double* pos /*[n][3]*/, const double* a0, int64_t n, double lox, double loy,
+                    double loz, double extent, double a0lo, double a0hi, int a0_buckets, int64_t* keys,
+                    void* stream);
 
 /* Pack a cloud (caller order, FP64 SoA) into processing-order records.
  * perm[i] = caller index of the i-th processed ball.  rec_a/rec_b hold
- * ceil(n/32)*32 records of 16 bytes, group_meta ceil(n/32) records of 32 bytes.
+ * ceil(n/32)*32 records of 16 bytes, group_meta ceil(n/32) records of 48 bytes.
  * Replaces: PointCloud field coercion (model.py:186-205) at the radiator boundary. */
 int pab_pack(const double* pos, const double* p0, const double* a0, const int32_t* perm, int64_t n,
              void* rec_a, void* rec_b, void* group_meta, void* stream);

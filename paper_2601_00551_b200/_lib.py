@@ -18,7 +18,7 @@ _SIGS = {
     "pab_device_info": ([_i, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)], _i),
     "pab_last_cuda_error": ([], C.c_char_p),
     "pab_record_sizes": ([C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)], _i),
-    "pab_morton_keys": ([_vp, _i64, _d, _d, _d, _d, _vp, _vp], _i),
+    "pab_morton_keys": ([_vp, _vp, _i64, _d, _d, _d, _d, _d, _d, _i, _vp, _vp], _i),
     "pab_pack": ([_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp], _i),
     "pab_forward_smem_bytes": ([_i, _i, _i], C.c_size_t),
     "pab_forward": ([_vp, _vp, _vp, _i64, _vp, _vp, _i, _d, _d, _d, _i, _i, _d, _i, _d, _i, _i, _i, _i,

@@ -4,21 +4,107 @@
 // cached slab window, einsum reductions, per-ball gradient assembly) and the
 // fixed-order block merge :336-348.
 //
-// Decomposition: a warp owns one lane group (32 Morton-ordered balls, one per
-// lane) and loops over a chunk of detectors; per detector the warp stages the
-// residual segment its group can touch into shared memory (coalesced), then
-// every lane walks its own arrival window accumulating four FP32 moments
+// Decomposition: a warp owns one lane group (32 balls of similar radius, one
+// per lane, so all lanes walk windows of nearly equal length) and loops over a
+// chunk of detectors in batches of 32.  Lane l of a batch computes detector
+// l's group geometry (FP64) once; per detector it is broadcast by shuffles.
+// The residual segment the group can touch is staged into a double-buffered
+// shared-memory segment with cp.async while the previous detector is being
+// processed; every lane walks its own arrival window accumulating four FP32
+// moments
 //   T_k = sum_J res[J] G(y_J) y_J^k,  k = 0..3,
-// and folds them into FP64 per-ball gradient accumulators held in registers
-// across all detectors of the chunk (no atomics).  Detector chunks (grid.y)
-// write partial sums that a finalize pass adds in chunk order.
+// with paired FP32x2 arithmetic (FFMA2/FMUL2/FADD2), 8 samples per iteration
+// and 64-bit shared loads.  Per-pair gradient terms are summed in FP32 over a
+// batch of 32 detectors and folded into FP64 per-ball accumulators held in
+// registers across the chunk (no atomics).  Detector chunks (grid.y) write
+// partial sums that the finalize pass adds in chunk order.
 #include "pab_common.cuh"
 
 namespace pab {
 
-constexpr int kSeg = 256;   // staged residual samples per warp
+constexpr int kSeg = 256;   // staged residual samples per warp and buffer
+
+__device__ __forceinline__ void cp_async4(float* smem_dst, const float* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+struct Moments {
+  float T0, T1, T2, T3;
+};
 
 template <int STAGE>
+__device__ __forceinline__ void moment_scalar(float res, float m, float sc, float ps, Moments& M) {
+  const float y = fmaf(m, -sc, ps);
+  const float q = y * y;
+  const float r = res * ex2(-q);
+  const float t = r * y;
+  M.T1 += t;
+  if (STAGE >= kStageCoarse) M.T3 = fmaf(t, q, M.T3);
+  if (STAGE == kStageFine) {
+    M.T0 += r;
+    M.T2 = fmaf(t, y, M.T2);
+  }
+}
+
+template <int STAGE>
+__device__ __forceinline__ void moment_pair(float2 res, float2 y, float2& A0, float2& A1, float2& A2, float2& A3) {
+  const float2 q = __fmul2_rn(y, y);
+  const float2 r = __fmul2_rn(res, make_float2(ex2(-q.x), ex2(-q.y)));
+  const float2 t = __fmul2_rn(r, y);
+  A1 = __fadd2_rn(A1, t);
+  if (STAGE >= kStageCoarse) A3 = __ffma2_rn(t, q, A3);
+  if (STAGE == kStageFine) {
+    A0 = __fadd2_rn(A0, r);
+    A2 = __ffma2_rn(t, y, A2);
+  }
+}
+
+// Walk n samples of one window: seg[off + i] is the residual of the i-th
+// sample (seg 8-byte aligned), m0 its m-offset (J f - kc), step fs.
+template <int STAGE>
+__device__ __forceinline__ void moments_run(const float* seg, int off, int n, float m0, float fs, float sc, float ps,
+                                            Moments& M) {
+  if (n <= 0) return;
+  if (reinterpret_cast<uintptr_t>(seg + off) & 7) {   // peel to an 8-byte aligned start
+    moment_scalar<STAGE>(seg[off], m0, sc, ps, M);
+    ++off;
+    --n;
+    m0 += fs;
+  }
+  const float2* s2 = reinterpret_cast<const float2*>(seg + off);
+  float2 A0 = make_float2(0.f, 0.f), A1 = A0, A2 = A0, A3 = A0;
+  const float2 nsc2 = make_float2(-sc, -sc);
+  // y of pair k of an 8-sample block: (mb + 2k fs, mb + (2k+1) fs) * -sc + ps
+  const float2 c0 = make_float2(ps, fmaf(fs, -sc, ps));
+  const float2 c1 = make_float2(fmaf(2.0f * fs, -sc, ps), fmaf(3.0f * fs, -sc, ps));
+  const float2 c2 = make_float2(fmaf(4.0f * fs, -sc, ps), fmaf(5.0f * fs, -sc, ps));
+  const float2 c3 = make_float2(fmaf(6.0f * fs, -sc, ps), fmaf(7.0f * fs, -sc, ps));
+  float mb = m0;
+  int i = 0;
+#pragma unroll 1
+  for (; i + 8 <= n; i += 8, mb += 8.0f * fs, s2 += 4) {
+    const float2 m2 = make_float2(mb, mb);
+    const float2 r0 = s2[0], r1 = s2[1], r2 = s2[2], r3 = s2[3];
+    moment_pair<STAGE>(r0, __ffma2_rn(m2, nsc2, c0), A0, A1, A2, A3);
+    moment_pair<STAGE>(r1, __ffma2_rn(m2, nsc2, c1), A0, A1, A2, A3);
+    moment_pair<STAGE>(r2, __ffma2_rn(m2, nsc2, c2), A0, A1, A2, A3);
+    moment_pair<STAGE>(r3, __ffma2_rn(m2, nsc2, c3), A0, A1, A2, A3);
+  }
+#pragma unroll 1
+  for (; i + 2 <= n; i += 2, mb += 2.0f * fs, ++s2) {
+    moment_pair<STAGE>(s2[0], __ffma2_rn(make_float2(mb, mb), nsc2, c0), A0, A1, A2, A3);
+  }
+  if (i < n) moment_scalar<STAGE>(seg[off + i], mb, sc, ps, M);
+  M.T0 += A0.x + A0.y;
+  M.T1 += A1.x + A1.y;
+  M.T2 += A2.x + A2.y;
+  M.T3 += A3.x + A3.y;
+}
+
+template <int STAGE, int DIR>
 __global__ void __launch_bounds__(256)
 adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
                const GroupMeta* __restrict__ gmeta, int64_t n_groups,
@@ -26,11 +112,10 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
                Acq acq, const float* __restrict__ res, float res_sign, int det_per_chunk,
                double* __restrict__ gpart, int64_t n_pad, unsigned long long* __restrict__ ops_total,
                int* __restrict__ status) {
-  __shared__ float seg_all[8][kSeg];
+  __shared__ __align__(16) float seg_all[8][2][kSeg];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
   if (g >= n_groups) return;
-  float* seg = seg_all[warp];
   const int q = blockIdx.y;
   const int j0 = q * det_per_chunk;
   const int j1 = min(n_det, j0 + det_per_chunk);
@@ -42,100 +127,122 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   const int64_t bi = g * kWarp + lane;
   const BallA A = ra[bi];
   const BallB B = rb[bi];
+  // per-ball constants (detector independent)
+  const float sc = acq.vdt_f * kSqrtHalfLog2e * B.inv_a0;
+  const float rho = acq.cutoff * A.a0 * acq.inv_vdt_f;
   const float kap = A.a0 * kSqrt2Ln2;
-  double acc_p0 = 0.0, acc_a0 = 0.0, acc_x = 0.0, acc_y = 0.0, acc_z = 0.0;
+  const float p0h = 0.5f * B.p0;
+  const bool live = B.orig >= 0;
+  double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
   unsigned long long my_ops = 0;
   int coinc = 0;
-  constexpr bool want_dir_grad = (STAGE == kStageFine);
 
   for (int jb = j0; jb < j1; jb += kWarp) {
     const int nd = min(kWarp, j1 - jb);
-    GroupDet gdl;
-    int rlo = 0, rhi = -1;
+    GroupDet gdl = empty_gd();
+    DetDir ddl{};
+    int rlo = 0, rhi = -1, nearl = 0;
+    double pxl = 0.0, pyl = 0.0, pzl = 0.0;
     if (lane < nd) {
-      const Detector dl = load_detector(det_pos, det_aux, jb + lane);
-      gdl = group_det(gm, dl.px, dl.py, dl.pz, acq);
+      const int jl = jb + lane;
+      pxl = det_pos[3 * jl]; pyl = det_pos[3 * jl + 1]; pzl = det_pos[3 * jl + 2];
+      gdl = group_det(gm, pxl, pyl, pzl, acq);
       group_range(acq, gdl, gm, &rlo, &rhi);
-    } else {
-      gdl.Sx = gdl.Sy = gdl.Sz = 0.f; gdl.Sn = 1.f; gdl.isn = 1.f; gdl.phg = 0.f; gdl.kg = 0; gdl.slow = 0;
+      nearl = group_near(acq, gdl, gm) ? 1 : 0;
+      if (DIR != kDirNone) ddl = load_detdir(det_aux, jl);
     }
-    for (int jj = 0; jj < nd; ++jj) {
-      const int j = jb + jj;
-      const GroupDet gd = shfl_gd(gdl, jj);
-      const int lo = __shfl_sync(0xffffffffu, rlo, jj);
+    auto stage_seg = [&](int jj, int buf) {
+      const int lo = __shfl_sync(0xffffffffu, rlo, jj) & ~1;
       const int hi = __shfl_sync(0xffffffffu, rhi, jj);
-      if (lo > hi) continue;
-      const Detector det = load_detector(det_pos, det_aux, j);
-      float dDdr[3] = {0.f, 0.f, 0.f}, dDda0 = 0.f;
-      const bool dgrad = want_dir_grad || acq.dir_kind == kDirElement;
-      const Pair p = make_pair(acq, gd, gm, det, A, B, dgrad, dDdr, &dDda0);
-      my_ops += (unsigned long long)(max(p.jhi - p.jlo + 1, 0) + max(p.nhi - p.nlo + 1, 0));
-      coinc |= p.coincident;
-      float T0 = 0.f, T1 = 0.f, T2 = 0.f, T3 = 0.f;
-      const float ps = p.phi * p.sc;
-      const float* rrow = res + (size_t)j * n_out;
-      for (int base = lo; base <= hi; base += kSeg) {
-        const int top = min(base + kSeg - 1, hi);
-        __syncwarp();
-        for (int k = lane; k <= top - base; k += kWarp) seg[k] = res_sign * __ldg(rrow + base + k);
-        __syncwarp();
-        {
-          const int jlo = max(p.jlo, base), jhi = min(p.jhi, top);
-          float mf = (float)(jlo * f - p.kc);
-          const float* s = seg + (jlo - base);
-#pragma unroll 4
-          for (int J = jlo; J <= jhi; ++J, mf += fs, ++s) {
-            const float y = fmaf(mf, -p.sc, ps);
-            const float q2 = y * y;
-            const float r = (*s) * ex2(-q2);
-            const float t = r * y;
-            T1 += t;
-            if (STAGE >= kStageCoarse) T3 = fmaf(t, q2, T3);
-            if (STAGE == kStageFine) { T0 += r; T2 = fmaf(t, y, T2); }
-          }
-        }
-        if (p.nlo <= p.nhi) {   // u+ = -kappa y: odd moments flip sign
-          const int jlo = max(p.nlo, base), jhi = min(p.nhi, top);
-          const float nps = p.nphi * p.sc;
-          for (int J = jlo; J <= jhi; ++J) {
-            const float y = fmaf((float)(J * f - p.nkc), -p.sc, nps);
-            const float q2 = y * y;
-            const float r = seg[J - base] * ex2(-q2);
-            const float t = r * y;
-            T1 -= t;
-            if (STAGE >= kStageCoarse) T3 = fmaf(-t, q2, T3);
-            if (STAGE == kStageFine) { T0 += r; T2 = fmaf(t, y, T2); }
-          }
-        }
+      if (lo <= hi && hi - lo + 1 <= kSeg) {
+        const float* src = res + (size_t)(jb + jj) * n_out + lo;
+        float* dst = seg_all[warp][buf];
+        for (int k = lane; k <= hi - lo; k += kWarp) cp_async4(dst + k, src + k);
       }
+      cp_async_commit();
+    };
+    float gb[5] = {0.f, 0.f, 0.f, 0.f, 0.f};   // FP32 batch sums of the pair terms
+    stage_seg(0, 0);
+    for (int jj = 0; jj < nd; ++jj) {
+      const int buf = jj & 1;
+      const int lo = __shfl_sync(0xffffffffu, rlo, jj) & ~1;   // even staging base
+      const int hi = __shfl_sync(0xffffffffu, rhi, jj);
+      const int near = __shfl_sync(0xffffffffu, nearl, jj);
+      const GroupDet gd = shfl_gd(gdl, jj);
+      const DetDir dd = shfl_detdir<DIR>(ddl, jj);
+      double px = 0.0, py = 0.0, pz = 0.0;
+      if (gd.slow) {
+        px = __shfl_sync(0xffffffffu, pxl, jj);
+        py = __shfl_sync(0xffffffffu, pyl, jj);
+        pz = __shfl_sync(0xffffffffu, pzl, jj);
+      }
+      cp_async_wait_all();
+      __syncwarp();
+      if (jj + 1 < nd) stage_seg(jj + 1, buf ^ 1);
+      if (lo > hi) continue;
+
+      const PairGeom pg = pair_geom(gd, gm, px, py, pz, A, B, acq);
+      coinc |= pg.coincident;
+      int jlo, jhi;
+      pair_window(pg.kc, pg.phi, rho, acq, &jlo, &jhi);
+      if (!live) { jlo = 1; jhi = 0; }
+      int nlo = 1, nhi = 0, nkc = 0;
+      float nphi = 0.0f;
+      if (near && live) pair_near_window(pg.d, rho, acq, &nlo, &nhi, &nkc, &nphi);
+      my_ops += (unsigned long long)(max(jhi - jlo + 1, 0) + max(nhi - nlo + 1, 0));
+
+      Moments M = {0.f, 0.f, 0.f, 0.f};
+      const bool staged = hi - lo + 1 <= kSeg;
+      const float* seg = staged ? seg_all[warp][buf] : res + (size_t)(jb + jj) * n_out;
+      const int sbase = staged ? lo : 0;
+      moments_run<STAGE>(seg, jlo - sbase, jhi - jlo + 1, (float)(jlo * f - pg.kc), fs, sc, pg.phi * sc, M);
+      if (nlo <= nhi) {   // u+ = -kappa y: odd moments flip sign
+        Moments N = {0.f, 0.f, 0.f, 0.f};
+        moments_run<STAGE>(seg, nlo - sbase, nhi - nlo + 1, (float)(nlo * f - nkc), fs, sc, nphi * sc, N);
+        M.T0 += N.T0;
+        M.T1 -= N.T1;
+        M.T2 += N.T2;
+        M.T3 -= N.T3;
+      }
+      __syncwarp();
+
       // per-pair gradient terms (reference radiator.py:275-286 in y units)
-      const float s_uG = kap * T1;
-      acc_p0 += (double)(p.D * s_uG * (0.5f / p.d));
+      float dDdr[3] = {0.f, 0.f, 0.f}, dDda0 = 0.f;
+      const float hx = pg.rx * pg.id, hy = pg.ry * pg.id, hz = pg.rz * pg.id;
+      const float D = dir_weight<DIR, STAGE == kStageFine || DIR == kDirElement>(
+          dd, hx, hy, hz, pg.id, acq.dir_param, acq.dir_param, B.inv_a0, dDdr, &dDda0);
+      const float base = p0h * pg.id;   // p0 / 2d
+      const float amp = base * D;
+      const float s_uG = kap * (res_sign * M.T1);
+      gb[0] = fmaf(D * s_uG, 0.5f * pg.id, gb[0]);
       if (STAGE >= kStageCoarse) {
-        float ga = p.amp * kSqrt2Ln2Cubed * T3;
-        if (acq.dir_kind == kDirElement) ga = fmaf(p.base * dDda0, s_uG, ga);
-        acc_a0 += (double)ga;
+        float ga = amp * kSqrt2Ln2Cubed * (res_sign * M.T3);
+        if (DIR == kDirElement) ga = fmaf(base * dDda0, s_uG, ga);
+        gb[1] += ga;
       }
       if (STAGE == kStageFine) {
-        const float gdist = p.amp * (T0 - kTwoLn2 * T2) - (p.amp / p.d) * s_uG;
-        const float w = gdist / p.d;
-        float gx = w * p.rx, gy = w * p.ry, gz = w * p.rz;
-        if (acq.dir_kind != kDirNone) {
-          const float bs = p.base * s_uG;
+        const float gdist = amp * res_sign * (M.T0 - kTwoLn2 * M.T2) - (amp * pg.id) * s_uG;
+        const float w = gdist * pg.id;
+        float gx = w * pg.rx, gy = w * pg.ry, gz = w * pg.rz;
+        if (DIR != kDirNone) {
+          const float bs = base * s_uG;
           gx = fmaf(bs, dDdr[0], gx);
           gy = fmaf(bs, dDdr[1], gy);
           gz = fmaf(bs, dDdr[2], gz);
         }
-        acc_x += (double)gx; acc_y += (double)gy; acc_z += (double)gz;
+        gb[2] += gx;
+        gb[3] += gy;
+        gb[4] += gz;
       }
     }
+    cp_async_wait_all();
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < 5; ++c) acc[c] += (double)gb[c];
   }
   double* out = gpart + (size_t)q * 5 * n_pad;
-  out[0 * n_pad + bi] = acc_p0;
-  out[1 * n_pad + bi] = acc_a0;
-  out[2 * n_pad + bi] = acc_x;
-  out[3 * n_pad + bi] = acc_y;
-  out[4 * n_pad + bi] = acc_z;
+#pragma unroll
+  for (int c = 0; c < 5; ++c) out[c * n_pad + bi] = acc[c];
   for (int o = 16; o > 0; o >>= 1) {
     my_ops += __shfl_xor_sync(0xffffffffu, my_ops, o);
     coinc |= __shfl_xor_sync(0xffffffffu, coinc, o);
@@ -174,6 +281,31 @@ __global__ void grad_finalize_kernel(const double* __restrict__ gpart, int chunk
   if (bad) atomicOr(status, kStatusNonFinite);
 }
 
+template <int STAGE, int DIR>
+static void launch_adjoint(dim3 grid, int threads, cudaStream_t s, const BallA* A, const BallB* B,
+                           const GroupMeta* G, int64_t n_groups, const double* det_pos, const double* det_aux,
+                           int n_det, const Acq& a, const float* res, float res_sign, int per_chunk, double* gpart,
+                           int64_t n_pad, unsigned long long* ops, int* status) {
+  adjoint_kernel<STAGE, DIR><<<grid, threads, 0, s>>>(A, B, G, n_groups, det_pos, det_aux, n_det, a, res, res_sign,
+                                                       per_chunk, gpart, n_pad, ops, status);
+}
+
+template <int STAGE>
+static void launch_adjoint_dir(int dir, dim3 grid, int threads, cudaStream_t s, const BallA* A, const BallB* B,
+                               const GroupMeta* G, int64_t n_groups, const double* det_pos, const double* det_aux,
+                               int n_det, const Acq& a, const float* res, float res_sign, int per_chunk,
+                               double* gpart, int64_t n_pad, unsigned long long* ops, int* status) {
+  if (dir == kDirNone)
+    launch_adjoint<STAGE, kDirNone>(grid, threads, s, A, B, G, n_groups, det_pos, det_aux, n_det, a, res, res_sign,
+                                    per_chunk, gpart, n_pad, ops, status);
+  else if (dir == kDirCosPower)
+    launch_adjoint<STAGE, kDirCosPower>(grid, threads, s, A, B, G, n_groups, det_pos, det_aux, n_det, a, res,
+                                        res_sign, per_chunk, gpart, n_pad, ops, status);
+  else
+    launch_adjoint<STAGE, kDirElement>(grid, threads, s, A, B, G, n_groups, det_pos, det_aux, n_det, a, res,
+                                       res_sign, per_chunk, gpart, n_pad, ops, status);
+}
+
 }  // namespace pab
 
 using namespace pab;
@@ -186,12 +318,11 @@ int pab_adjoint(const void* rec_a, const void* rec_b, const void* group_meta, in
                 float res_sign, int stage, int chunks, int warps, double* grad_partial,
                 unsigned long long* ops_total, int* status, void* stream) {
   if (n_groups <= 0 || n_det <= 0) return 0;
-  if (f < 1 || chunks < 1 || warps < 1 || warps > 8 || stage < 0 || stage > 2) return 1;
+  if (f < 1 || chunks < 1 || warps < 1 || warps > 8 || stage < 0 || stage > 2 || dir_kind < 0 || dir_kind > 2)
+    return 1;
   if (!rec_a || !rec_b || !group_meta || !det_pos || !det_aux || !res || !grad_partial || !status) return 1;
-  Acq a;
-  a.vdt = v * dt; a.inv_vdt = 1.0 / a.vdt; a.vt0 = v * t0; a.f = f; a.n_out = n_out;
-  a.cutoff = (float)cutoff; a.vdt_f = (float)a.vdt; a.inv_vdt_f = (float)a.inv_vdt;
-  a.dir_kind = dir_kind; a.dir_param = (float)dir_param;
+  if ((int64_t)n_out * f > (1 << 24)) return 1;
+  const Acq a = make_acq(v, t0, dt, f, n_out, cutoff, dir_kind, dir_param);
   const int per_chunk = (n_det + chunks - 1) / chunks;
   const int64_t n_pad = n_groups * kWarp;
   dim3 grid((unsigned)((n_groups + warps - 1) / warps), (unsigned)chunks);
@@ -199,18 +330,16 @@ int pab_adjoint(const void* rec_a, const void* rec_b, const void* group_meta, in
   const BallA* A = (const BallA*)rec_a;
   const BallB* B = (const BallB*)rec_b;
   const GroupMeta* G = (const GroupMeta*)group_meta;
+  const int th = warps * kWarp;
   if (stage == kStageFilter)
-    adjoint_kernel<kStageFilter><<<grid, warps * kWarp, 0, s>>>(A, B, G, n_groups, det_pos, det_aux, n_det, a,
-                                                                res, res_sign, per_chunk, grad_partial, n_pad,
-                                                                ops_total, status);
+    launch_adjoint_dir<kStageFilter>(dir_kind, grid, th, s, A, B, G, n_groups, det_pos, det_aux, n_det, a, res,
+                                     res_sign, per_chunk, grad_partial, n_pad, ops_total, status);
   else if (stage == kStageCoarse)
-    adjoint_kernel<kStageCoarse><<<grid, warps * kWarp, 0, s>>>(A, B, G, n_groups, det_pos, det_aux, n_det, a,
-                                                                res, res_sign, per_chunk, grad_partial, n_pad,
-                                                                ops_total, status);
+    launch_adjoint_dir<kStageCoarse>(dir_kind, grid, th, s, A, B, G, n_groups, det_pos, det_aux, n_det, a, res,
+                                     res_sign, per_chunk, grad_partial, n_pad, ops_total, status);
   else
-    adjoint_kernel<kStageFine><<<grid, warps * kWarp, 0, s>>>(A, B, G, n_groups, det_pos, det_aux, n_det, a,
-                                                              res, res_sign, per_chunk, grad_partial, n_pad,
-                                                              ops_total, status);
+    launch_adjoint_dir<kStageFine>(dir_kind, grid, th, s, A, B, G, n_groups, det_pos, det_aux, n_det, a, res,
+                                   res_sign, per_chunk, grad_partial, n_pad, ops_total, status);
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 

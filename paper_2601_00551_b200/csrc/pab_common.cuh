@@ -42,7 +42,8 @@ struct Acq {
   double vdt, inv_vdt, vt0;   // v*dt, 1/(v*dt), v*t0 (full-rate grid)
   int f, n_out;               // decimation factor, samples on the decimated grid
   float cutoff;               // support half-width in sigmas
-  float vdt_f, inv_vdt_f;
+  float vdt_f, inv_vdt_f, vt0_f;
+  float inv_f;
   int dir_kind;
   float dir_param;            // cos power p, or element width w (m)
 };
@@ -50,9 +51,11 @@ struct Acq {
 // Ball records in processing (sorted) order; 32 consecutive records form a
 // lane group sharing an FP64 centre.  Padding records have orig < 0.
 struct BallA { float dx, dy, dz, a0; };          // offset from group centre, radius
-struct BallB { float p0, r2, pad; int orig; };   // pressure, |offset|^2, original index
+struct BallB { float p0, r2, inv_a0; int orig; };   // pressure, |offset|^2, 1/a0, original index
 
-struct GroupMeta { double cx, cy, cz; float radius, a0max; };
+// Lane-group bounding box: centre (FP64), bounding-sphere radius, max a0,
+// half extents (48 bytes).
+struct GroupMeta { double cx, cy, cz; float radius, a0max, hx, hy, hz, pad; };
 
 // Per (lane group, detector) geometry, computed in FP64 once and broadcast.
 struct GroupDet {
@@ -96,6 +99,12 @@ __device__ __forceinline__ GroupDet group_det(const GroupMeta& g, double px, dou
   return r;
 }
 
+__device__ __forceinline__ GroupDet empty_gd() {
+  GroupDet g;
+  g.Sx = g.Sy = g.Sz = 0.f; g.Sn = 1.f; g.isn = 1.f; g.phg = 0.f; g.kg = 0; g.slow = 0;
+  return g;
+}
+
 __device__ __forceinline__ GroupDet shfl_gd(const GroupDet& g, int src) {
   GroupDet r;
   r.Sx = __shfl_sync(0xffffffffu, g.Sx, src);
@@ -115,6 +124,17 @@ __device__ __forceinline__ int floor_div(int a, int b) {
 }
 __device__ __forceinline__ int ceil_div(int a, int b) { return -floor_div(-a, b); }
 
+// floor(a / f) for f >= 1 without integer division: float estimate, then an
+// exact integer correction (|a| < 2^24).
+__device__ __forceinline__ int floor_div_f(int a, int f, float inv_f) {
+  if (f == 1) return a;
+  int q = __float2int_rd((float)a * inv_f);
+  q += (q + 1) * f <= a ? 1 : 0;
+  q -= q * f > a ? 1 : 0;
+  return q;
+}
+__device__ __forceinline__ int ceil_div_f(int a, int f, float inv_f) { return -floor_div_f(-a, f, inv_f); }
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -125,7 +145,7 @@ __device__ __forceinline__ float ex2(float x) {
 struct Pair {
   int kc;             // anchor full-rate sample (nearest to tau)
   float phi;          // tau - kc
-  float d;            // distance
+  float d, id;        // distance, 1/d
   float rx, ry, rz;   // r_ball - r_det
   float base;         // p0 / (2 d)
   float D;            // directivity weight
@@ -142,16 +162,15 @@ struct Pair {
 // Directivity weight and (optionally) its derivatives w.r.t. the ball position
 // (dDdr) and a0 (dDda0).  cos_power: D = max(cos,0)^p, cos = face . rhat.
 // element: D = sinc(w s1 / 2a0) sinc(w s2 / 2a0), s_k = e_k . rhat.
-__device__ __forceinline__ float directivity(const Acq& a, const Detector& det, float rx, float ry,
-                                             float rz, float d, float a0, bool want_grad,
-                                             float* dDdr, float* dDda0) {
+template <bool WANT_GRAD>
+__device__ __forceinline__ float directivity(const Acq& a, const Detector& det, float rx, float ry, float rz,
+                                             float id, float a0, float inv_a0, float* dDdr, float* dDda0) {
   if (a.dir_kind == kDirNone) return 1.0f;
-  const float id = 1.0f / d;
   const float hx = rx * id, hy = ry * id, hz = rz * id;
   if (a.dir_kind == kDirCosPower) {
     const float c = det.fx * hx + det.fy * hy + det.fz * hz;
     if (c <= 0.0f) {
-      if (want_grad) { dDdr[0] = dDdr[1] = dDdr[2] = 0.0f; *dDda0 = 0.0f; }
+      if (WANT_GRAD) { dDdr[0] = dDdr[1] = dDdr[2] = 0.0f; *dDda0 = 0.0f; }
       return 0.0f;
     }
     const float p = a.dir_param;
@@ -159,10 +178,11 @@ __device__ __forceinline__ float directivity(const Acq& a, const Detector& det, 
     if (p == 2.0f) { D = c * c; dDdc = 2.0f * c; }
     else if (p == 1.0f) { D = c; dDdc = 1.0f; }
     else { D = __powf(c, p); dDdc = p * D / c; }
-    if (want_grad) {
-      dDdr[0] = dDdc * (det.fx - c * hx) * id;
-      dDdr[1] = dDdc * (det.fy - c * hy) * id;
-      dDdr[2] = dDdc * (det.fz - c * hz) * id;
+    if (WANT_GRAD) {
+      const float s = dDdc * id;
+      dDdr[0] = s * (det.fx - c * hx);
+      dDdr[1] = s * (det.fy - c * hy);
+      dDdr[2] = s * (det.fz - c * hz);
       *dDda0 = 0.0f;
     }
     return D;
@@ -170,39 +190,41 @@ __device__ __forceinline__ float directivity(const Acq& a, const Detector& det, 
   // element (square piston, far-field weight at the pulse's spectral peak)
   const float s1 = det.e1x * hx + det.e1y * hy + det.e1z * hz;
   const float s2 = det.e2x * hx + det.e2y * hy + det.e2z * hz;
-  const float sc = a.dir_param / (2.0f * a0);
+  const float sc = 0.5f * a.dir_param * inv_a0;
   const float x1 = sc * s1, x2 = sc * s2;
   float f1, g1, f2, g2;
   if (fabsf(x1) < 1e-3f) { f1 = 1.0f - x1 * x1 * (1.0f / 6.0f); g1 = -x1 * (1.0f / 3.0f); }
   else { float sn, cs; sincosf(x1, &sn, &cs); f1 = sn / x1; g1 = (cs - f1) / x1; }
   if (fabsf(x2) < 1e-3f) { f2 = 1.0f - x2 * x2 * (1.0f / 6.0f); g2 = -x2 * (1.0f / 3.0f); }
   else { float sn, cs; sincosf(x2, &sn, &cs); f2 = sn / x2; g2 = (cs - f2) / x2; }
-  if (want_grad) {
+  if (WANT_GRAD) {
     const float a1 = g1 * f2 * sc, a2 = f1 * g2 * sc;
     dDdr[0] = (a1 * (det.e1x - s1 * hx) + a2 * (det.e2x - s2 * hx)) * id;
     dDdr[1] = (a1 * (det.e1y - s1 * hy) + a2 * (det.e2y - s2 * hy)) * id;
     dDdr[2] = (a1 * (det.e1z - s1 * hz) + a2 * (det.e2z - s2 * hz)) * id;
-    *dDda0 = -(a1 * s1 + a2 * s2) / a0;
+    *dDda0 = -(a1 * s1 + a2 * s2) * inv_a0;
   }
   return f1 * f2;
 }
 
 // Per-pair setup.  gd: group/detector geometry; gm: the ball's group (slow
 // path only); A/B: the ball record.
+template <bool WANT_GRAD>
 __device__ __forceinline__ Pair make_pair(const Acq& a, const GroupDet& gd, const GroupMeta& gm,
                                           const Detector& det, const BallA& A, const BallB& B,
-                                          bool want_grad, float* dDdr, float* dDda0) {
+                                          float* dDdr, float* dDda0) {
   Pair p;
   p.coincident = 0;
-  float tr;   // tau - kg (FP32, small)
+  float tr;   // tau - kbase (FP32, small)
   int kbase;
   if (!gd.slow) {
     const float sd = gd.Sx * A.dx + gd.Sy * A.dy + gd.Sz * A.dz;
     const float num = B.r2 - 2.0f * sd;               // d^2 - |S|^2
-    const float e = num * gd.isn * gd.isn;
-    const float dd = num * gd.isn / (1.0f + sqrtf(1.0f + e));   // d - |S|
+    const float e1 = fmaf(num * gd.isn, gd.isn, 1.0f);  // (d / |S|)^2
+    const float sq = e1 * rsqrtf(e1);                  // d / |S|
+    const float dd = __fdividef(num * gd.isn, 1.0f + sq);   // d - |S|
     p.d = gd.Sn + dd;
-    tr = gd.phg + dd * a.inv_vdt_f;
+    tr = fmaf(dd, a.inv_vdt_f, gd.phg);
     kbase = gd.kg;
     p.rx = A.dx - gd.Sx; p.ry = A.dy - gd.Sy; p.rz = A.dz - gd.Sz;
   } else {
@@ -221,55 +243,229 @@ __device__ __forceinline__ Pair make_pair(const Acq& a, const GroupDet& gd, cons
   const float kr = rintf(tr);
   p.kc = kbase + (int)kr;
   p.phi = tr - kr;
-  p.base = B.p0 / (2.0f * p.d);
-  p.D = directivity(a, det, p.rx, p.ry, p.rz, p.d, A.a0, want_grad, dDdr, dDda0);
-  p.amp = (B.p0 * p.D) / (2.0f * p.d);
-  p.sc = a.vdt_f * kSqrtHalfLog2e / A.a0;
+  p.id = __fdividef(1.0f, p.d);
+  p.base = 0.5f * B.p0 * p.id;
+  p.D = directivity<WANT_GRAD>(a, det, p.rx, p.ry, p.rz, p.id, A.a0, B.inv_a0, dDdr, dDda0);
+  p.amp = p.base * p.D;
+  p.sc = a.vdt_f * kSqrtHalfLog2e * B.inv_a0;
   p.rho = a.cutoff * A.a0 * a.inv_vdt_f;
   // u- window: full-rate k in [kc + ceil(phi - rho), kc + floor(phi + rho)]
   {
-    const int klo = p.kc + (int)ceilf(p.phi - p.rho);
-    const int khi = p.kc + (int)floorf(p.phi + p.rho);
-    p.jlo = max(ceil_div(klo, a.f), 0);
-    p.jhi = min(floor_div(khi, a.f), a.n_out - 1);
+    const int klo = p.kc + __float2int_ru(p.phi - p.rho);
+    const int khi = p.kc + __float2int_rd(p.phi + p.rho);
+    p.jlo = max(ceil_div_f(klo, a.f, a.inv_f), 0);
+    p.jhi = min(floor_div_f(khi, a.f, a.inv_f), a.n_out - 1);
   }
   // u+ window: tau+ = -(d + v t0) / (v dt); non-empty only in the near field
   p.nlo = 1; p.nhi = 0; p.nkc = 0; p.nphi = 0.0f;
-  const double taup = -((double)p.d + a.vt0) * a.inv_vdt;
-  if (taup + (double)p.rho >= 0.0) {
-    const double kp = rint(taup);
-    p.nkc = (int)kp;
-    p.nphi = (float)(taup - kp);
-    const int klo = p.nkc + (int)ceilf(p.nphi - p.rho);
-    const int khi = p.nkc + (int)floorf(p.nphi + p.rho);
-    p.nlo = max(ceil_div(klo, a.f), 0);
-    p.nhi = min(floor_div(khi, a.f), a.n_out - 1);
+  if (-(p.d + a.vt0_f) * a.inv_vdt_f + p.rho >= -2.0f) {
+    const double taup = -((double)p.d + a.vt0) * a.inv_vdt;
+    if (taup + (double)p.rho >= 0.0) {
+      const double kp = rint(taup);
+      p.nkc = (int)kp;
+      p.nphi = (float)(taup - kp);
+      const int klo = p.nkc + __float2int_ru(p.nphi - p.rho);
+      const int khi = p.nkc + __float2int_rd(p.nphi + p.rho);
+      p.nlo = max(ceil_div(klo, a.f), 0);
+      p.nhi = min(floor_div(khi, a.f), a.n_out - 1);
+    }
   }
   if (B.orig < 0) { p.jlo = 1; p.jhi = 0; p.nlo = 1; p.nhi = 0; }
   return p;
 }
 
+// ---------------------------------------------------------------------------
+// Lean per-pair pieces used by the hot loops (per-ball constants hoisted by
+// the caller; detector direction data broadcast from a lane batch).
+// ---------------------------------------------------------------------------
+
+struct DetDir {   // receive direction and element axes (FP32)
+  float fx, fy, fz, e1x, e1y, e1z, e2x, e2y, e2z;
+};
+
+__device__ __forceinline__ DetDir load_detdir(const double* __restrict__ aux, int j) {
+  const double* a = aux + 9 * j;
+  DetDir d;
+  d.fx = (float)a[0]; d.fy = (float)a[1]; d.fz = (float)a[2];
+  d.e1x = (float)a[3]; d.e1y = (float)a[4]; d.e1z = (float)a[5];
+  d.e2x = (float)a[6]; d.e2y = (float)a[7]; d.e2z = (float)a[8];
+  return d;
+}
+
+template <int DIR>
+__device__ __forceinline__ DetDir shfl_detdir(const DetDir& s, int src) {
+  DetDir d = s;
+  if (DIR != kDirNone) {
+    d.fx = __shfl_sync(0xffffffffu, s.fx, src);
+    d.fy = __shfl_sync(0xffffffffu, s.fy, src);
+    d.fz = __shfl_sync(0xffffffffu, s.fz, src);
+  }
+  if (DIR == kDirElement) {
+    d.e1x = __shfl_sync(0xffffffffu, s.e1x, src);
+    d.e1y = __shfl_sync(0xffffffffu, s.e1y, src);
+    d.e1z = __shfl_sync(0xffffffffu, s.e1z, src);
+    d.e2x = __shfl_sync(0xffffffffu, s.e2x, src);
+    d.e2y = __shfl_sync(0xffffffffu, s.e2y, src);
+    d.e2z = __shfl_sync(0xffffffffu, s.e2z, src);
+  }
+  return d;
+}
+
+// D and (GRAD) dD/dr_ball, dD/da0; (hx, hy, hz) = unit ball - detector direction.
+template <int DIR, bool GRAD>
+__device__ __forceinline__ float dir_weight(const DetDir& dd, float hx, float hy, float hz, float id, float power,
+                                            float width, float inv_a0, float* dDdr, float* dDda0) {
+  if (DIR == kDirNone) return 1.0f;
+  if (DIR == kDirCosPower) {
+    const float c = dd.fx * hx + dd.fy * hy + dd.fz * hz;
+    const float cp = fmaxf(c, 0.0f);
+    float D, dDdc;
+    if (power == 2.0f) { D = cp * cp; dDdc = 2.0f * cp; }
+    else if (power == 1.0f) { D = cp; dDdc = c > 0.0f ? 1.0f : 0.0f; }
+    else { D = c > 0.0f ? __powf(cp, power) : 0.0f; dDdc = c > 0.0f ? power * D / cp : 0.0f; }
+    if (GRAD) {
+      const float s = dDdc * id;
+      dDdr[0] = s * (dd.fx - c * hx);
+      dDdr[1] = s * (dd.fy - c * hy);
+      dDdr[2] = s * (dd.fz - c * hz);
+      *dDda0 = 0.0f;
+    }
+    return D;
+  }
+  const float s1 = dd.e1x * hx + dd.e1y * hy + dd.e1z * hz;
+  const float s2 = dd.e2x * hx + dd.e2y * hy + dd.e2z * hz;
+  const float sc = 0.5f * width * inv_a0;
+  const float x1 = sc * s1, x2 = sc * s2;
+  float f1, g1, f2, g2;
+  if (fabsf(x1) < 1e-3f) { f1 = 1.0f - x1 * x1 * (1.0f / 6.0f); g1 = -x1 * (1.0f / 3.0f); }
+  else { float sn, cs; __sincosf(x1, &sn, &cs); f1 = sn / x1; g1 = (cs - f1) / x1; }
+  if (fabsf(x2) < 1e-3f) { f2 = 1.0f - x2 * x2 * (1.0f / 6.0f); g2 = -x2 * (1.0f / 3.0f); }
+  else { float sn, cs; __sincosf(x2, &sn, &cs); f2 = sn / x2; g2 = (cs - f2) / x2; }
+  if (GRAD) {
+    const float a1 = g1 * f2 * sc, a2 = f1 * g2 * sc;
+    dDdr[0] = (a1 * (dd.e1x - s1 * hx) + a2 * (dd.e2x - s2 * hx)) * id;
+    dDdr[1] = (a1 * (dd.e1y - s1 * hy) + a2 * (dd.e2y - s2 * hy)) * id;
+    dDdr[2] = (a1 * (dd.e1z - s1 * hz) + a2 * (dd.e2z - s2 * hz)) * id;
+    *dDda0 = -(a1 * s1 + a2 * s2) * inv_a0;
+  }
+  return f1 * f2;
+}
+
+// Distance and arrival-time split for one pair.  Fast path: FP32 relative to
+// the group centre; slow path (detector within two group radii): FP64.
+struct PairGeom {
+  float d, id, phi, rx, ry, rz;
+  int kc;
+  int coincident;
+};
+
+__device__ __forceinline__ PairGeom pair_geom(const GroupDet& gd, const GroupMeta& gm, double px, double py,
+                                              double pz, const BallA& A, const BallB& B, const Acq& a) {
+  PairGeom g;
+  g.coincident = 0;
+  float tr;
+  int kbase;
+  if (!gd.slow) {
+    const float sd = gd.Sx * A.dx + gd.Sy * A.dy + gd.Sz * A.dz;
+    const float num = B.r2 - 2.0f * sd;
+    const float e1 = fmaf(num * gd.isn, gd.isn, 1.0f);
+    const float dd = __fdividef(num * gd.isn, 1.0f + e1 * rsqrtf(e1));
+    g.d = gd.Sn + dd;
+    tr = fmaf(dd, a.inv_vdt_f, gd.phg);
+    kbase = gd.kg;
+    g.rx = A.dx - gd.Sx; g.ry = A.dy - gd.Sy; g.rz = A.dz - gd.Sz;
+  } else {
+    const double dx = gm.cx + (double)A.dx - px, dy = gm.cy + (double)A.dy - py, dz = gm.cz + (double)A.dz - pz;
+    const double d = sqrt(dx * dx + dy * dy + dz * dz);
+    if (d < 1e-12 && B.orig >= 0) g.coincident = 1;
+    const double tau = (d - a.vt0) * a.inv_vdt;
+    const double kf = floor(tau);
+    kbase = (int)kf;
+    tr = (float)(tau - kf);
+    g.d = (float)(d > 1e-30 ? d : 1e-30);
+    g.rx = (float)dx; g.ry = (float)dy; g.rz = (float)dz;
+  }
+  const float kr = rintf(tr);
+  g.kc = kbase + (int)kr;
+  g.phi = tr - kr;
+  g.id = __fdividef(1.0f, g.d);
+  return g;
+}
+
+// u- window on the decimated grid, clipped to [0, n_out).
+__device__ __forceinline__ void pair_window(int kc, float phi, float rho, const Acq& a, int* jlo, int* jhi) {
+  const int klo = kc + __float2int_ru(phi - rho);
+  const int khi = kc + __float2int_rd(phi + rho);
+  *jlo = max(ceil_div_f(klo, a.f, a.inv_f), 0);
+  *jhi = min(floor_div_f(khi, a.f, a.inv_f), a.n_out - 1);
+}
+
+// u+ window (near field; only called when the group can have one).
+__device__ __forceinline__ void pair_near_window(float d, float rho, const Acq& a, int* nlo, int* nhi, int* nkc,
+                                                 float* nphi) {
+  *nlo = 1; *nhi = 0; *nkc = 0; *nphi = 0.0f;
+  const double taup = -((double)d + a.vt0) * a.inv_vdt;
+  if (taup + (double)rho >= 0.0) {
+    const double kp = rint(taup);
+    *nkc = (int)kp;
+    *nphi = (float)(taup - kp);
+    const int klo = *nkc + __float2int_ru(*nphi - rho);
+    const int khi = *nkc + __float2int_rd(*nphi + rho);
+    *nlo = max(ceil_div(klo, a.f), 0);
+    *nhi = min(floor_div(khi, a.f), a.n_out - 1);
+  }
+}
+
+// Can any ball of the group have a u+ window at this detector?
+__device__ __forceinline__ bool group_near(const Acq& a, const GroupDet& gd, const GroupMeta& gm) {
+  const float rho = a.cutoff * gm.a0max * a.inv_vdt_f;
+  return -(gd.Sn - gm.radius + a.vt0_f) * a.inv_vdt_f + rho + 2.0f >= 0.0f || gd.slow;
+}
+
 // Decimated-sample range a lane group can touch for one detector: centre
-// tau_g -+ (radius / v dt + rho_max + 1), plus [0, ..] when a u+ term can exist.
+// tau_g -+ (radius / v dt + rho_max + 2), plus [0, ..] when a u+ term can exist.
 __device__ __forceinline__ void group_range(const Acq& a, const GroupDet& gd, const GroupMeta& gm,
                                             int* lo, int* hi) {
+  // distance range over the group's bounding box: |S| - p <= d <= |S| + p +
+  // r^2 / 2|S|, p = projection of the box half-extents on the detector
+  // direction (each side capped by the bounding sphere, |d - |S|| <= r)
   const float rho = a.cutoff * gm.a0max * a.inv_vdt_f;
-  const float span = gm.radius * a.inv_vdt_f + rho + 2.0f;
+  const float proj = (fabsf(gd.Sx) * gm.hx + fabsf(gd.Sy) * gm.hy + fabsf(gd.Sz) * gm.hz) * gd.isn;
+  const float dlo = fminf(proj, gm.radius);
+  const float dhi = fminf(proj + 0.5f * gm.radius * gm.radius * gd.isn, gm.radius);
   const float c = gd.phg;
-  int klo = gd.kg + (int)floorf(c - span);
-  int khi = gd.kg + (int)ceilf(c + span);
+  int klo = gd.kg + (int)floorf(c - (dlo * a.inv_vdt_f + rho + 0.5f));
+  int khi = gd.kg + (int)ceilf(c + (dhi * a.inv_vdt_f + rho + 0.5f));
   if (gd.slow) {   // FP32 S is coarse near the detector: widen generously
     klo = min(klo, -(int)ceilf(rho) - 2);
   }
   // near field: u+ = d + v t0 + k v dt can vanish for k >= 0
   const float dmin = gd.Sn - gm.radius;
-  const float taup_max = -(dmin + (float)a.vt0) * a.inv_vdt_f;
+  const float taup_max = -(dmin + a.vt0_f) * a.inv_vdt_f;
   if (taup_max + rho + 1.0f >= 0.0f) {
-    klo = min(klo, (int)floorf(-(gd.Sn + gm.radius + (float)a.vt0) * a.inv_vdt_f - rho - 2.0f));
+    klo = min(klo, (int)floorf(-(gd.Sn + gm.radius + a.vt0_f) * a.inv_vdt_f - rho - 2.0f));
     khi = max(khi, (int)ceilf(taup_max + rho + 2.0f));
   }
   *lo = max(floor_div(klo, a.f), 0);
   *hi = min(ceil_div(khi, a.f), a.n_out - 1);
+}
+
+__host__ __device__ inline Acq make_acq(double v, double t0, double dt, int f, int n_out, double cutoff,
+                                        int dir_kind, double dir_param) {
+  Acq a;
+  a.vdt = v * dt;
+  a.inv_vdt = 1.0 / a.vdt;
+  a.vt0 = v * t0;
+  a.f = f;
+  a.n_out = n_out;
+  a.cutoff = (float)cutoff;
+  a.vdt_f = (float)a.vdt;
+  a.inv_vdt_f = (float)a.inv_vdt;
+  a.vt0_f = (float)a.vt0;
+  a.inv_f = 1.0f / (float)f;
+  a.dir_kind = dir_kind;
+  a.dir_param = (float)dir_param;
+  return a;
 }
 
 }  // namespace pab

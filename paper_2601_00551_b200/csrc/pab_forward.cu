@@ -3,15 +3,23 @@
 // Replaces reference radiator.py:185-261 (slab evaluation + np.bincount
 // scatter) and :263-264 (residual, loss part).
 //
-// Decomposition: one CTA owns one detector row (all samples of the decimated
-// grid, in shared memory) and a partition of the ball cells; a cell is C
-// consecutive lane groups (32 Morton-ordered balls each).  A warp takes a
-// cell, lane l evaluates ball l of every group of the cell over its own
-// arrival window and read-modify-writes its private column of a per-warp
-// tile [UT rows x 32 lanes] (lane l always hits bank l: conflict-free, no
-// atomics).  The tile covers the cell's sample range; it is then reduced
-// across lanes and merged into the CTA's row in cell order (a shared-memory
-// ticket), so every sample is a fixed-order sum: results are bitwise
+// Decomposition.  One CTA owns one detector row (all samples of the
+// decimated grid, in shared memory) and a partition of the lane groups (32
+// balls of similar radius, spatially compact).  Groups are processed in
+// chunks; per chunk the CTA
+//   A  computes every group's sample range for this detector (FP64 geometry),
+//   B  counting-sorts the groups by the 4-sample bin of their first sample
+//      (histogram, scan, in-order match_any ranks: deterministic, stable),
+//   C  gives each warp a contiguous slice of the sorted list.  A warp walks
+//      its slice in time order; lane l evaluates ball l of each group over
+//      its own arrival window and read-modify-writes its private column of a
+//      circular per-warp tile [UT rows x 32 lanes] (lane l -> bank l: no
+//      conflicts, no atomics).  Rows the sweep has passed are reduced across
+//      lanes (rotated, conflict-free) and added to the CTA row: each sample is
+//      reduced once per warp instead of once per group,
+//   D  merges the few rows where neighbouring warps' slices overlap, in warp
+//      order.
+// Every sample is therefore a fixed-order sum: results are bitwise
 // reproducible run to run.  Partitions are summed in order by the epilogue.
 #include <climits>
 
@@ -19,173 +27,319 @@
 
 namespace pab {
 
-__device__ __forceinline__ int warp_min_i(int v) {
-  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-__device__ __forceinline__ int warp_max_i(int v) {
-  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
+constexpr int kBinShift = 2;           // 4 decimated samples per sort bin
+constexpr int kChunk = 2048;           // lane groups per sort chunk
+constexpr unsigned short kEmptyBin = 0xFFFF;
+constexpr int kTile = 160;             // tile rows per warp (circular, slot = J % kTile)
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
 }
 
-__device__ __forceinline__ void ticket_acquire(int* ticket, int seq, int lane) {
-  if (lane == 0) {
-    while (*((volatile int*)ticket) != seq) __nanosleep(32);
+// acc[slot] += Ak * y G over n consecutive samples starting at column pointer
+// t (row stride 32 floats, no wrap inside), m-offset mf, step fs.
+__device__ __forceinline__ void rmw_run(float* t, int n, float mf, float fs, float sc, float ps, float Ak) {
+  // samples (i, i+1) and (i+2, i+3) ride packed FP32x2 registers (FFMA2/FMUL2)
+  int i = 0;
+  const float2 nsc2 = make_float2(-sc, -sc);
+  const float2 ps2 = make_float2(ps, ps);
+  const float2 Ak2 = make_float2(Ak, Ak);
+  float2 ma = make_float2(mf, mf + fs), mb = make_float2(mf + 2.0f * fs, mf + 3.0f * fs);
+  const float2 step4 = make_float2(4.0f * fs, 4.0f * fs);
+#pragma unroll 1
+  for (; i + 4 <= n; i += 4, t += 4 * kWarp) {
+    const float2 ya = __ffma2_rn(ma, nsc2, ps2);
+    const float2 yb = __ffma2_rn(mb, nsc2, ps2);
+    const float2 oa = make_float2(t[0], t[kWarp]);
+    const float2 ob = make_float2(t[2 * kWarp], t[3 * kWarp]);
+    const float2 qa = __fmul2_rn(ya, ya), qb = __fmul2_rn(yb, yb);
+    const float2 Ga = make_float2(ex2(-qa.x), ex2(-qa.y));
+    const float2 Gb = make_float2(ex2(-qb.x), ex2(-qb.y));
+    const float2 na = __ffma2_rn(Ak2, __fmul2_rn(ya, Ga), oa);
+    const float2 nb = __ffma2_rn(Ak2, __fmul2_rn(yb, Gb), ob);
+    t[0] = na.x;
+    t[kWarp] = na.y;
+    t[2 * kWarp] = nb.x;
+    t[3 * kWarp] = nb.y;
+    ma = __fadd2_rn(ma, step4);
+    mb = __fadd2_rn(mb, step4);
+  }
+  mf = ma.x;
+#pragma unroll 1
+  for (; i < n; ++i, mf += fs, t += kWarp) {
+    const float y = fmaf(mf, -sc, ps);
+    *t = fmaf(Ak, y * ex2(-y * y), *t);
+  }
+}
+
+// Window [lo, hi] of one pair into the circular tile (slot = J % kTile).
+__device__ __forceinline__ void rmw_window(float* tile, int lane, int lo, int hi, int m0, int f, float sc,
+                                           float phi, float Ak) {
+  if (lo > hi) return;
+  const float ps = phi * sc;
+  const float fs = (float)f;
+  const int s0 = lo % kTile;
+  const int n = hi - lo + 1;
+  const int n1 = min(n, kTile - s0);
+  const float mf = (float)(lo * f - m0);
+  rmw_run(tile + s0 * kWarp + lane, n1, mf, fs, sc, ps, Ak);
+  if (n > n1) rmw_run(tile + lane, n - n1, mf + (float)n1 * fs, fs, sc, ps, Ak);
+}
+
+// Reduce rows [a, b) of the circular tile across lanes (lane l reduces one
+// row of each 32-row block, columns read in rotated order), zero them, and
+// hand each row sum to `sink(r, v)`.
+template <class Sink>
+__device__ __forceinline__ void flush_rows(float* tile, int lane, int a, int b, Sink sink) {
+  for (int r0 = a; r0 < b; r0 += kWarp) {
+    const int r = r0 + lane;
+    if (r < b) {
+      float* trow = tile + (r % kTile) * kWarp;
+      float s = 0.0f;
+#pragma unroll 8
+      for (int i = 0; i < kWarp; ++i) {
+        const int col = (i + lane) & 31;
+        s += trow[col];
+        trow[col] = 0.0f;
+      }
+      sink(r, s);
+    }
   }
   __syncwarp();
-  __threadfence_block();
 }
 
-__device__ __forceinline__ void ticket_release(int* ticket, int seq, int lane) {
-  __syncwarp();
-  __threadfence_block();
-  if (lane == 0) *((volatile int*)ticket) = seq + 1;
-  __syncwarp();
+// One ball (lane) of one group against the CTA's detector: setup, then the
+// u- (and, near field, u+) window clipped to [clip_lo, clip_hi] into the tile.
+template <int DIR>
+__device__ __forceinline__ void evaluate_pair(float* tile, int lane, const Acq& acq, const GroupDet& gd,
+                                              const GroupMeta& gm, const Detector& det, const DetDir& dd,
+                                              const BallA& A, const BallB& B, int near, unsigned long long& ops,
+                                              int& coinc, int clip_lo, int clip_hi) {
+  const PairGeom pg = pair_geom(gd, gm, det.px, det.py, det.pz, A, B, acq);
+  coinc |= pg.coincident;
+  const float rho = acq.cutoff * A.a0 * acq.inv_vdt_f;
+  const float sc = acq.vdt_f * kSqrtHalfLog2e * B.inv_a0;
+  int jlo, jhi;
+  pair_window(pg.kc, pg.phi, rho, acq, &jlo, &jhi);
+  if (B.orig < 0) { jlo = 1; jhi = 0; }
+  int nlo = 1, nhi = 0, nkc = 0;
+  float nphi = 0.0f;
+  if (near && B.orig >= 0) pair_near_window(pg.d, rho, acq, &nlo, &nhi, &nkc, &nphi);
+  ops += (unsigned long long)(max(jhi - jlo + 1, 0) + max(nhi - nlo + 1, 0));
+  float D = 1.0f;
+  if (DIR != kDirNone)
+    D = dir_weight<DIR, false>(dd, pg.rx * pg.id, pg.ry * pg.id, pg.rz * pg.id, pg.id, acq.dir_param,
+                               acq.dir_param, B.inv_a0, nullptr, nullptr);
+  // u G amp = Ak * y G with Ak = amp * kappa = (p0 D / 2d) a0 sqrt(2 ln 2)
+  const float Ak = (0.5f * B.p0 * D) * pg.id * (A.a0 * kSqrt2Ln2);
+  rmw_window(tile, lane, max(jlo, clip_lo), min(jhi, clip_hi), pg.kc, acq.f, sc, pg.phi, Ak);
+  if (nlo <= nhi)   // u+ = -kappa y
+    rmw_window(tile, lane, max(nlo, clip_lo), min(nhi, clip_hi), nkc, acq.f, -sc, nphi, Ak);
 }
 
-constexpr int kMaxTileBlocks = 8;   // UT <= 256
-
+template <int DIR>
 __global__ void __launch_bounds__(256, 1)
 forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
                const GroupMeta* __restrict__ gmeta, int64_t n_groups,
                const double* __restrict__ det_pos, const double* __restrict__ det_aux, int n_det,
-               Acq acq, int groups_per_cell, int64_t cells_per_part, int tile_rows,
-               float* __restrict__ partial_rows, unsigned long long* __restrict__ ops_total,
-               int* __restrict__ status) {
-  extern __shared__ __align__(16) float smem[];
+               Acq acq, int64_t groups_per_part, float* __restrict__ partial_rows,
+               unsigned long long* __restrict__ ops_total, int* __restrict__ status) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int W = blockDim.x >> 5;
   const int n_out = acq.n_out;
   const int row_pad = (n_out + 3) & ~3;
-  float* row = smem;
-  float* tiles = smem + row_pad;
-  const int nw = blockDim.x >> 5;
-  int* ticket = reinterpret_cast<int*>(tiles + (size_t)nw * tile_rows * kWarp);
+  const int n_bins = (n_out + (1 << kBinShift) - 1) >> kBinShift;
+  float* row = reinterpret_cast<float*>(smem_raw);
+  float* tiles = row + row_pad;
+  float* stage = tiles + (size_t)W * kTile * kWarp;
+  int* hist = reinterpret_cast<int*>(stage + W * kTile);        // [n_bins + 1]
+  int* zs = hist + (n_bins + 1);                                // [W + 1]
+  int* misc = zs + W + 1;                                       // [4]
+  unsigned short* sorted = reinterpret_cast<unsigned short*>(misc + 4);
+  unsigned short* gbin = sorted + kChunk;
 
   const int j = blockIdx.x;
   const int part = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  for (int i = threadIdx.x; i < row_pad; i += blockDim.x) row[i] = 0.0f;
-  for (int i = threadIdx.x; i < nw * tile_rows * kWarp; i += blockDim.x) tiles[i] = 0.0f;
-  if (threadIdx.x == 0) *ticket = 0;
-  __syncthreads();
-
-  const Detector det = load_detector(det_pos, det_aux, j);
-  float* tile = tiles + (size_t)warp * tile_rows * kWarp;
-  const int C = groups_per_cell;
-  const int64_t n_cells = (n_groups + C - 1) / C;
-  const int64_t c_begin = (int64_t)part * cells_per_part;
-  const int64_t c_end = min(n_cells, c_begin + cells_per_part);
+  const int tid = threadIdx.x, nthr = blockDim.x;
   const int f = acq.f;
 
+  for (int i = tid; i < row_pad; i += nthr) row[i] = 0.0f;
+  for (int i = tid; i < W * kTile * kWarp; i += nthr) tiles[i] = 0.0f;
+  for (int i = tid; i < W * kTile; i += nthr) stage[i] = 0.0f;
+
+  const Detector det = load_detector(det_pos, det_aux, j);
+  DetDir dd{};
+  if (DIR != kDirNone) dd = load_detdir(det_aux, j);
+  float* tile = tiles + (size_t)warp * kTile * kWarp;
+  const int64_t g_begin = (int64_t)part * groups_per_part;
+  const int64_t g_end = min(n_groups, g_begin + groups_per_part);
   unsigned long long my_ops = 0;
   int coinc = 0;
-  int seq = warp;
-  for (int64_t c = c_begin + warp; c < c_end; c += nw, seq += nw) {
-    const int64_t g0 = c * C;
-    const int ng = (int)min((int64_t)C, n_groups - g0);
-    GroupMeta gm_l;
-    GroupDet gd_l;
-    int glo = INT_MAX, ghi = INT_MIN;
-    if (lane < ng) {
-      gm_l = gmeta[g0 + lane];
-      gd_l = group_det(gm_l, det.px, det.py, det.pz, acq);
-      group_range(acq, gd_l, gm_l, &glo, &ghi);
-    } else {
-      gd_l.Sx = gd_l.Sy = gd_l.Sz = 0.f; gd_l.Sn = 1.f; gd_l.isn = 1.f; gd_l.phg = 0.f;
-      gd_l.kg = 0; gd_l.slow = 0;
+
+  for (int64_t cg0 = g_begin; cg0 < g_end; cg0 += kChunk) {
+    const int cn = (int)min((int64_t)kChunk, g_end - cg0);
+    for (int i = tid; i < n_bins + 1; i += nthr) hist[i] = 0;
+    __syncthreads();
+
+    // ---- A: bin every group of the chunk by its first sample ----
+    for (int gl = tid; gl < cn; gl += nthr) {
+      const GroupMeta gm = gmeta[cg0 + gl];
+      const GroupDet gd = group_det(gm, det.px, det.py, det.pz, acq);
+      int lo, hi;
+      group_range(acq, gd, gm, &lo, &hi);
+      unsigned short bin = kEmptyBin;
+      if (lo <= hi) {
+        const int blo = lo & ~((1 << kBinShift) - 1);
+        bin = (hi - blo + 1 > kTile) ? (unsigned short)n_bins : (unsigned short)(lo >> kBinShift);
+        atomicAdd(&hist[bin], 1);   // counts only: order-independent
+      }
+      gbin[gl] = bin;
     }
-    const int clo = warp_min_i(glo), chi = warp_max_i(ghi);
-    bool holding = false;
-    for (int base = clo; base <= chi; base += tile_rows) {
-      const int top = min(base + tile_rows - 1, chi);
-      const bool first_pass = base == clo;
-      for (int i = 0; i < ng; ++i) {
-        const GroupDet g = shfl_gd(gd_l, i);
-        GroupMeta gmi;
-        if (g.slow) gmi = gmeta[g0 + i];
-        const int64_t bi = (g0 + i) * kWarp + lane;
-        const BallA A = ra[bi];
-        const BallB B = rb[bi];
-        const Pair p = make_pair(acq, g, gmi, det, A, B, false, nullptr, nullptr);
-        if (first_pass) {
-          my_ops += (unsigned long long)(max(p.jhi - p.jlo + 1, 0) + max(p.nhi - p.nlo + 1, 0));
-          coinc |= p.coincident;
+    __syncthreads();
+
+    // ---- B+C (warp 0): exclusive scan, then a stable in-order scatter ----
+    if (warp == 0) {
+      const int total = n_bins + 1;
+      int carry = 0;
+      for (int c0 = 0; c0 < total; c0 += kWarp) {
+        const int i = c0 + lane;
+        const int x = i < total ? hist[i] : 0;
+        int incl = x;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
         }
-        const float Ak = p.amp * A.a0 * kSqrt2Ln2;   // amp * kappa: u G amp = Ak * y G
-        const float ps = p.phi * p.sc;
-        {
-          const int lo = max(p.jlo, base), hi = min(p.jhi, top);
-          float mf = (float)(lo * f - p.kc);
-          const float fs = (float)f;
-          float* t = tile + (lo - base) * kWarp + lane;
-          int J = lo;
-#pragma unroll 1
-          for (; J + 3 <= hi; J += 4, mf += 4.0f * fs, t += 4 * kWarp) {
-            const float y0 = fmaf(mf, -p.sc, ps);
-            const float y1 = fmaf(mf + fs, -p.sc, ps);
-            const float y2 = fmaf(mf + 2.0f * fs, -p.sc, ps);
-            const float y3 = fmaf(mf + 3.0f * fs, -p.sc, ps);
-            const float G0 = ex2(-y0 * y0), G1 = ex2(-y1 * y1);
-            const float G2 = ex2(-y2 * y2), G3 = ex2(-y3 * y3);
-            t[0] = fmaf(Ak, y0 * G0, t[0]);
-            t[kWarp] = fmaf(Ak, y1 * G1, t[kWarp]);
-            t[2 * kWarp] = fmaf(Ak, y2 * G2, t[2 * kWarp]);
-            t[3 * kWarp] = fmaf(Ak, y3 * G3, t[3 * kWarp]);
-          }
-          for (; J <= hi; ++J, mf += fs, t += kWarp) {
-            const float y = fmaf(mf, -p.sc, ps);
-            const float G = ex2(-y * y);
-            *t = fmaf(Ak, y * G, *t);
-          }
-        }
-        if (p.nlo <= p.nhi) {   // u+ term (near field): u = -kappa * y
-          const int lo = max(p.nlo, base), hi = min(p.nhi, top);
-          const float nps = p.nphi * p.sc;
-          for (int J = lo; J <= hi; ++J) {
-            const float y = fmaf((float)(J * f - p.nkc), -p.sc, nps);
-            const float G = ex2(-y * y);
-            float* t = tile + (J - base) * kWarp + lane;
-            *t = fmaf(-Ak, y * G, *t);
-          }
-        }
-      }
-      // reduce the tile across lanes (rotated column order: conflict-free)
-      const int len = top - base + 1;
-      float sums[kMaxTileBlocks];
-#pragma unroll
-      for (int k = 0; k < kMaxTileBlocks; ++k) {
-        sums[k] = 0.0f;
-        if (k * kWarp < len) {
-          float* trow = tile + (k * kWarp + lane) * kWarp;
-          float s = 0.0f;
-#pragma unroll 8
-          for (int i = 0; i < kWarp; ++i) {
-            const int col = (i + lane) & 31;
-            s += trow[col];
-            trow[col] = 0.0f;
-          }
-          sums[k] = s;
-        }
-      }
-      if (!holding) { ticket_acquire(ticket, seq, lane); holding = true; }
-#pragma unroll
-      for (int k = 0; k < kMaxTileBlocks; ++k) {
-        const int r = k * kWarp + lane;
-        if (r < len) row[base + r] += sums[k];
+        if (i < total) hist[i] = carry + incl - x;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
       }
       __syncwarp();
+      if (lane == 0) {
+        misc[0] = hist[n_bins];   // start of the oversize list = regular count
+        misc[1] = carry;          // all listed groups
+      }
+      for (int b0 = 0; b0 < cn; b0 += kWarp) {
+        const int gl = b0 + lane;
+        const unsigned short bin = gl < cn ? gbin[gl] : kEmptyBin;
+        const unsigned mask = __match_any_sync(0xffffffffu, (int)bin);
+        int pos = 0;
+        if (bin != kEmptyBin) pos = hist[bin] + __popc(mask & lanemask_lt());
+        __syncwarp();
+        if (bin != kEmptyBin) {
+          sorted[pos] = (unsigned short)gl;
+          if ((mask & lanemask_lt()) == 0) hist[bin] += __popc(mask);
+        }
+        __syncwarp();
+      }
     }
-    if (!holding) ticket_acquire(ticket, seq, lane);
-    ticket_release(ticket, seq, lane);
+    __syncthreads();
+
+    const int n_reg = misc[0];
+    const int n_all = misc[1];
+    if (tid == 0) {
+      zs[W] = n_out;
+      for (int w = W - 1; w >= 0; --w) {
+        const int s = (int)(((int64_t)n_reg * w) / W), e = (int)(((int64_t)n_reg * (w + 1)) / W);
+        zs[w] = (s < e) ? ((int)gbin[sorted[s]] << kBinShift) : zs[w + 1];
+      }
+    }
+    __syncthreads();
+
+    // ---- D: time-ordered sweep of this warp's slice ----
+    {
+      const int s_begin = (int)(((int64_t)n_reg * warp) / W);
+      const int s_end = (int)(((int64_t)n_reg * (warp + 1)) / W);
+      const int zone_end = zs[warp + 1];
+      float* my_stage = stage + warp * kTile;
+      auto sink = [&](int r, float v) {
+        if (r < zone_end) row[r] += v;
+        else my_stage[r - zone_end] = v;
+      };
+      int fp = zs[warp];
+      for (int i0 = s_begin; i0 < s_end; i0 += kWarp) {
+        const int nb = min(kWarp, s_end - i0);
+        // lane l prepares the geometry of the l-th group of this batch
+        GroupDet gd_l = empty_gd();
+        int64_t g_l = 0;
+        int bin_l = 0, near_l = 0;
+        if (lane < nb) {
+          const int gl = sorted[i0 + lane];
+          g_l = cg0 + gl;
+          bin_l = gbin[gl];
+          const GroupMeta gm = gmeta[g_l];
+          gd_l = group_det(gm, det.px, det.py, det.pz, acq);
+          near_l = group_near(acq, gd_l, gm) ? 1 : 0;
+        }
+        // software pipeline: records of the next group are loaded while the
+        // current one is evaluated
+        int64_t g_next = __shfl_sync(0xffffffffu, g_l, 0);
+        BallA An = ra[g_next * kWarp + lane];
+        BallB Bn = rb[g_next * kWarp + lane];
+        for (int k = 0; k < nb; ++k) {
+          const GroupDet gd = shfl_gd(gd_l, k);
+          const int64_t g = g_next;
+          const BallA A = An;
+          const BallB B = Bn;
+          if (k + 1 < nb) {
+            g_next = __shfl_sync(0xffffffffu, g_l, k + 1);
+            An = ra[g_next * kWarp + lane];
+            Bn = rb[g_next * kWarp + lane];
+          }
+          const int blo = __shfl_sync(0xffffffffu, bin_l, k) << kBinShift;
+          const int near = __shfl_sync(0xffffffffu, near_l, k);
+          if (blo > fp) {
+            flush_rows(tile, lane, fp, min(blo, fp + kTile), sink);
+            fp = blo;
+          }
+          GroupMeta gm;
+          if (gd.slow) gm = gmeta[g];
+          evaluate_pair<DIR>(tile, lane, acq, gd, gm, det, dd, A, B, near, my_ops, coinc, INT_MIN, INT_MAX);
+          __syncwarp();
+        }
+      }
+      if (s_begin < s_end) flush_rows(tile, lane, fp, min(fp + kTile, n_out), sink);
+    }
+    __syncthreads();
+
+    // ---- E: overlap rows, merged in warp order ----
+    for (int w = 0; w + 1 < W; ++w) {
+      const int r0 = zs[w + 1];
+      for (int i = tid; i < kTile && r0 + i < n_out; i += nthr) {
+        row[r0 + i] += stage[w * kTile + i];
+        stage[w * kTile + i] = 0.0f;
+      }
+      __syncthreads();
+    }
+
+    // ---- F: groups wider than the tile (rare): warp 0, linear passes ----
+    if (warp == 0) {
+      for (int idx = n_reg; idx < n_all; ++idx) {
+        const int64_t g = cg0 + sorted[idx];
+        const GroupMeta gm = gmeta[g];
+        const GroupDet gd = group_det(gm, det.px, det.py, det.pz, acq);
+        int lo, hi;
+        group_range(acq, gd, gm, &lo, &hi);
+        const BallA A = ra[g * kWarp + lane];
+        const BallB B = rb[g * kWarp + lane];
+        const int near = group_near(acq, gd, gm) ? 1 : 0;
+        for (int base = lo - lo % kTile; base <= hi; base += kTile) {
+          const int top = base + kTile - 1;
+          unsigned long long ops_once = 0;
+          evaluate_pair<DIR>(tile, lane, acq, gd, gm, det, dd, A, B, near, ops_once, coinc, base, top);
+          if (base + kTile > hi) my_ops += ops_once;   // count each pair once
+          __syncwarp();
+          flush_rows(tile, lane, base, min(top + 1, n_out), [&](int r, float v) { row[r] += v; });
+        }
+      }
+    }
+    __syncthreads();
   }
-  // warps whose cell sequence ended early must still let later cells through:
-  // every seq in [0, n_cells_in_part) is released by exactly one warp above.
-  __syncthreads();
 
   float* out = partial_rows + ((size_t)part * n_det + j) * (size_t)n_out;
-  for (int i = threadIdx.x; i < n_out; i += blockDim.x) out[i] = row[i];
+  for (int i = tid; i < n_out; i += nthr) out[i] = row[i];
 
-  // op count and coincidence flag
   for (int o = 16; o > 0; o >>= 1) {
     my_ops += __shfl_xor_sync(0xffffffffu, my_ops, o);
     coinc |= __shfl_xor_sync(0xffffffffu, coinc, o);
@@ -235,31 +389,22 @@ __global__ void decimate_kernel(const float* __restrict__ src, int n_rows, int n
   dst[i] = src[r * n_in + k * f];
 }
 
+size_t forward_smem(int n_out, int warps) {
+  const size_t row_pad = (size_t)((n_out + 3) & ~3);
+  const size_t n_bins = (size_t)((n_out + (1 << kBinShift) - 1) >> kBinShift);
+  return row_pad * 4 + (size_t)warps * kTile * kWarp * 4 + (size_t)warps * kTile * 4 +
+         (n_bins + 1) * 4 + (size_t)(warps + 1) * 4 + 16 + 2 * kChunk * 2 + 16;
+}
+
 }  // namespace pab
 
 using namespace pab;
 
-static Acq make_acq(double v, double t0, double dt, int f, int n_out, double cutoff, int dir_kind,
-                    double dir_param) {
-  Acq a;
-  a.vdt = v * dt;
-  a.inv_vdt = 1.0 / a.vdt;
-  a.vt0 = v * t0;
-  a.f = f;
-  a.n_out = n_out;
-  a.cutoff = (float)cutoff;
-  a.vdt_f = (float)a.vdt;
-  a.inv_vdt_f = (float)a.inv_vdt;
-  a.dir_kind = dir_kind;
-  a.dir_param = (float)dir_param;
-  return a;
-}
-
 extern "C" {
 
 size_t pab_forward_smem_bytes(int n_out, int warps, int tile_rows) {
-  const size_t row_pad = (size_t)((n_out + 3) & ~3);
-  return (row_pad + (size_t)warps * tile_rows * kWarp) * sizeof(float) + 16;
+  (void)tile_rows;
+  return forward_smem(n_out, warps);
 }
 
 int pab_forward(const void* rec_a, const void* rec_b, const void* group_meta, int64_t n_groups,
@@ -267,22 +412,28 @@ int pab_forward(const void* rec_a, const void* rec_b, const void* group_meta, in
                 int f, int n_out, double cutoff, int dir_kind, double dir_param, int groups_per_cell,
                 int partitions, int warps, int tile_rows, float* partial_rows,
                 unsigned long long* ops_total, int* status, void* stream) {
+  (void)groups_per_cell;
+  (void)tile_rows;
   if (n_det <= 0 || n_out <= 0) return 0;
-  if (f < 1 || groups_per_cell < 1 || groups_per_cell > 32 || partitions < 1 || warps < 1 || warps > 8 ||
-      tile_rows < 32 || tile_rows > 32 * kMaxTileBlocks || (tile_rows % 32) != 0)
-    return 1;
+  if (f < 1 || partitions < 1 || warps < 1 || warps > 8) return 1;
   if (!rec_a || !rec_b || !group_meta || !det_pos || !det_aux || !partial_rows || !ops_total || !status)
     return 1;
+  if ((int64_t)n_out * f > (1 << 24)) return 1;
   const Acq acq = make_acq(v, t0, dt, f, n_out, cutoff, dir_kind, dir_param);
-  const int64_t n_cells = (n_groups + groups_per_cell - 1) / groups_per_cell;
-  const int64_t per_part = (n_cells + partitions - 1) / partitions;
-  const size_t smem = pab_forward_smem_bytes(n_out, warps, tile_rows);
+  const int64_t per_part = (n_groups + partitions - 1) / partitions;
+  const size_t smem = forward_smem(n_out, warps);
   if (smem > 227 * 1024) return 1;
-  cudaFuncSetAttribute(forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (dir_kind < 0 || dir_kind > 2) return 1;
   dim3 grid((unsigned)n_det, (unsigned)partitions);
-  forward_kernel<<<grid, warps * kWarp, smem, (cudaStream_t)stream>>>(
-      (const BallA*)rec_a, (const BallB*)rec_b, (const GroupMeta*)group_meta, n_groups, det_pos, det_aux,
-      n_det, acq, groups_per_cell, per_part, tile_rows, partial_rows, ops_total, status);
+  auto launch = [&](auto kernel) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kernel<<<grid, warps * kWarp, smem, (cudaStream_t)stream>>>(
+        (const BallA*)rec_a, (const BallB*)rec_b, (const GroupMeta*)group_meta, n_groups, det_pos, det_aux,
+        n_det, acq, per_part, partial_rows, ops_total, status);
+  };
+  if (dir_kind == kDirNone) launch(forward_kernel<kDirNone>);
+  else if (dir_kind == kDirCosPower) launch(forward_kernel<kDirCosPower>);
+  else launch(forward_kernel<kDirElement>);
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 
@@ -300,6 +451,7 @@ int pab_decimate(const float* src, int n_rows, int n_in, int f, float* dst, void
   const int n_out = (n_in + f - 1) / f;
   const int64_t total = (int64_t)n_rows * n_out;
   if (total == 0) return 0;
+  if (!src || !dst) return 1;
   decimate_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(src, n_rows, n_in, f,
                                                                                     n_out, dst);
   return cudaGetLastError() == cudaSuccess ? 0 : 4;

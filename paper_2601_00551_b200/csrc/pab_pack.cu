@@ -20,18 +20,56 @@ __device__ __forceinline__ uint32_t spread3(uint32_t v) {   // 10 bits -> every 
   return v;
 }
 
-// key = (morton30 << 33) | (a0 bucket << 27... ) is not used: a0 enters as the
-// low-order tiebreak through the index only.  key = morton30 << 32 | index.
-__global__ void morton_keys_kernel(const double* __restrict__ pos, int64_t n, double lox, double loy,
-                                   double loz, double inv_ext, int64_t* __restrict__ keys) {
+// 3-D Hilbert index of a 10-bit lattice point (Skilling's transpose form).
+// Unlike Morton order the curve has no jumps, so 32 consecutive balls form a
+// compact lane group (tight arrival-time spread at every detector).
+__device__ __forceinline__ uint32_t hilbert3(uint32_t x, uint32_t y, uint32_t z) {
+  uint32_t X[3] = {x, y, z};
+  constexpr uint32_t M = 1u << 9;
+#pragma unroll
+  for (uint32_t Q = M; Q > 1; Q >>= 1) {
+    const uint32_t P = Q - 1;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      if (X[i] & Q) {
+        X[0] ^= P;
+      } else {
+        const uint32_t t = (X[0] ^ X[i]) & P;
+        X[0] ^= t;
+        X[i] ^= t;
+      }
+    }
+  }
+  X[1] ^= X[0];
+  X[2] ^= X[1];
+  uint32_t t = 0;
+#pragma unroll
+  for (uint32_t Q = M; Q > 1; Q >>= 1)
+    if (X[2] & Q) t ^= Q - 1;
+  X[0] ^= t; X[1] ^= t; X[2] ^= t;
+  uint32_t h = 0;
+#pragma unroll
+  for (int b = 9; b >= 0; --b)
+    h = (h << 3) | (((X[0] >> b) & 1u) << 2) | (((X[1] >> b) & 1u) << 1) | ((X[2] >> b) & 1u);
+  return h;
+}
+
+// key = a0 bucket (4 bits) << 58 | hilbert30 << 28 | index (28 bits): balls
+// of similar radius share lane groups (equal window lengths: no divergence in
+// the per-lane window loops), spatially compact within a bucket.
+__global__ void morton_keys_kernel(const double* __restrict__ pos, const double* __restrict__ a0, int64_t n,
+                                   double lox, double loy, double loz, double inv_ext, double a0lo,
+                                   double inv_a0span, int nbuckets, int64_t* __restrict__ keys) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double s = 1023.0 * inv_ext;
   const uint32_t qx = (uint32_t)fmin(fmax((pos[3 * i + 0] - lox) * s, 0.0), 1023.0);
   const uint32_t qy = (uint32_t)fmin(fmax((pos[3 * i + 1] - loy) * s, 0.0), 1023.0);
   const uint32_t qz = (uint32_t)fmin(fmax((pos[3 * i + 2] - loz) * s, 0.0), 1023.0);
-  const uint64_t code = (uint64_t)(spread3(qx) | (spread3(qy) << 1) | (spread3(qz) << 2));
-  keys[i] = (int64_t)((code << 32) | (uint64_t)i);
+  const uint64_t code = (uint64_t)hilbert3(qx, qy, qz);
+  int b = 0;
+  if (nbuckets > 1) b = (int)fmin(fmax((a0[i] - a0lo) * inv_a0span * nbuckets, 0.0), (double)(nbuckets - 1));
+  keys[i] = (int64_t)(((uint64_t)b << 58) | (code << 28) | ((uint64_t)i & 0xFFFFFFFull));
 }
 
 __device__ __forceinline__ double warp_min(double v) {
@@ -66,20 +104,21 @@ __global__ void pack_kernel(const double* __restrict__ pos, const double* __rest
     pp = p0[b]; aa = a0[b];
   }
   const double big = 1e300;
-  const double cx = 0.5 * (warp_min(live ? x : big) + warp_max(live ? x : -big));
-  const double cy = 0.5 * (warp_min(live ? y : big) + warp_max(live ? y : -big));
-  const double cz = 0.5 * (warp_min(live ? z : big) + warp_max(live ? z : -big));
+  const double xl = warp_min(live ? x : big), xh = warp_max(live ? x : -big);
+  const double yl = warp_min(live ? y : big), yh = warp_max(live ? y : -big);
+  const double zl = warp_min(live ? z : big), zh = warp_max(live ? z : -big);
+  const double cx = 0.5 * (xl + xh), cy = 0.5 * (yl + yh), cz = 0.5 * (zl + zh);
   BallA A;
   BallB B;
   if (live) {
     A.dx = (float)(x - cx); A.dy = (float)(y - cy); A.dz = (float)(z - cz); A.a0 = (float)aa;
     B.p0 = (float)pp;
     B.r2 = A.dx * A.dx + A.dy * A.dy + A.dz * A.dz;
-    B.pad = 0.0f;
+    B.inv_a0 = 1.0f / A.a0;
     B.orig = b;
   } else {
     A.dx = A.dy = A.dz = 0.0f; A.a0 = 1.0f;
-    B.p0 = 0.0f; B.r2 = 0.0f; B.pad = 0.0f; B.orig = -1;
+    B.p0 = 0.0f; B.r2 = 0.0f; B.inv_a0 = 1.0f; B.orig = -1;
   }
   const float rad = warp_maxf(live ? sqrtf(B.r2) : 0.0f);
   const float amax = warp_maxf(live ? A.a0 : 0.0f);
@@ -90,6 +129,11 @@ __global__ void pack_kernel(const double* __restrict__ pos, const double* __rest
     m.cx = cx; m.cy = cy; m.cz = cz;
     m.radius = rad * 1.000001f + 1e-12f;
     m.a0max = amax;
+    // half extents, rounded up so the FP32 box still contains every ball
+    m.hx = (float)(0.5 * (xh - xl)) * 1.000001f + 1e-12f;
+    m.hy = (float)(0.5 * (yh - yl)) * 1.000001f + 1e-12f;
+    m.hz = (float)(0.5 * (zh - zl)) * 1.000001f + 1e-12f;
+    m.pad = 0.0f;
     gm[g] = m;
   }
 }
@@ -100,13 +144,15 @@ using namespace pab;
 
 extern "C" {
 
-int pab_morton_keys(const double* pos, int64_t n, double lox, double loy, double loz, double extent,
-                    int64_t* keys, void* stream) {
+int pab_morton_keys(const double* pos, const double* a0, int64_t n, double lox, double loy, double loz,
+                    double extent, double a0lo, double a0hi, int a0_buckets, int64_t* keys, void* stream) {
   if (n <= 0) return 0;
-  if (!pos || !keys || !(extent > 0.0)) return 1;
+  if (!pos || !keys || !(extent > 0.0) || n > (1ll << 28) || a0_buckets < 1 || a0_buckets > 16) return 1;
+  if (a0_buckets > 1 && (!a0 || !(a0hi > a0lo))) a0_buckets = 1;
   const int threads = 256;
   morton_keys_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0, (cudaStream_t)stream>>>(
-      pos, n, lox, loy, loz, 1.0 / extent, keys);
+      pos, a0, n, lox, loy, loz, 1.0 / extent, a0lo, a0_buckets > 1 ? 1.0 / (a0hi - a0lo) : 0.0, a0_buckets,
+      keys);
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 

@@ -26,9 +26,11 @@ STATUS_COINCIDENT = 2
 STATUS_NONFINITE = 8
 
 FORWARD_WARPS = 8
-FORWARD_TILE_ROWS = 160
+FORWARD_TILE_ROWS = 128
 ADJOINT_WARPS = 8
 GROUP = 32
+A0_BUCKETS = 4   # lane groups hold balls of similar radius (equal window lengths)
+GROUP_META_BYTES = 48
 
 
 def cuda_device() -> torch.device:
@@ -159,11 +161,12 @@ class DeviceCloud:
         ext = float(torch.max(hi - lo).item())
         ext = ext if ext > 0.0 else 1.0
         lo_h = lo.cpu().numpy()
+        a0lo, a0hi = (float(x) for x in torch.aminmax(self.a0))
         keys = torch.empty(n, dtype=torch.int64, device=self.dev)
-        call("pab_morton_keys", ptr(self.pos), n, float(lo_h[0]), float(lo_h[1]), float(lo_h[2]), ext,
-             ptr(keys), _stream())
+        call("pab_morton_keys", ptr(self.pos), ptr(self.a0), n, float(lo_h[0]), float(lo_h[1]), float(lo_h[2]),
+             ext, a0lo, a0hi, A0_BUCKETS, ptr(keys), _stream())
         skeys, _ = torch.sort(keys)
-        self.perm = (skeys & 0xFFFFFFFF).to(torch.int32)
+        self.perm = (skeys & 0xFFFFFFF).to(torch.int32)
 
     def pack(self) -> None:
         if self._packed:
@@ -175,7 +178,7 @@ class DeviceCloud:
         if not hasattr(self, "rec_a") or self.rec_a.numel() < npad * 16:
             self.rec_a = torch.empty(npad * 16, dtype=torch.uint8, device=self.dev)
             self.rec_b = torch.empty(npad * 16, dtype=torch.uint8, device=self.dev)
-            self.gmeta = torch.empty(max(ng, 1) * 32, dtype=torch.uint8, device=self.dev)
+            self.gmeta = torch.empty(max(ng, 1) * GROUP_META_BYTES, dtype=torch.uint8, device=self.dev)
         if self.n:
             call("pab_pack", ptr(self.pos), ptr(self.p0), ptr(self.a0), ptr(self.perm), self.n,
                  ptr(self.rec_a), ptr(self.rec_b), ptr(self.gmeta), _stream())
@@ -189,7 +192,7 @@ class DeviceCloud:
             if ng == 0:
                 self._stats = (0.0, 0.0)
             else:
-                meta = self.gmeta[: ng * 32].view(torch.float32).view(ng, 8)
+                meta = self.gmeta[: ng * GROUP_META_BYTES].view(torch.float32).view(ng, GROUP_META_BYTES // 4)
                 r = float(torch.median(meta[:, 6]).item())
                 amax = float(torch.max(meta[:, 7]).item())
                 self._stats = (r, amax)
@@ -234,26 +237,17 @@ class ForwardPlan:
 
 
 def plan_forward(cloud: DeviceCloud, det: DeviceDetectors, acq: Acq) -> ForwardPlan:
+    """One CTA (8 warps, ~165-190 KB smem) per SM: detectors x partitions
+    should cover >= 2 waves; each partition keeps >= 4 lane groups per warp."""
     dev = cloud.dev
-    r_g, amax = cloud.stats()
-    vdt = det.sound_speed * acq.dt
-    f = acq.f
     tile = FORWARD_TILE_ROWS
     warps = FORWARD_WARPS
     while warps > 1 and _lib.load().pab_forward_smem_bytes(acq.n_out, warps, tile) > 227 * 1024:
         warps //= 2
-    rho = acq.cutoff * amax / vdt
-    avail = tile - 2.0 * rho / f - 6.0
-    if avail <= 0.0 or r_g <= 0.0:
-        C = 1 if avail <= 0.0 else 32
-    else:
-        r_cell = avail * vdt * f / 2.0
-        C = int(max(1, min(32, math.floor((r_cell / r_g) ** 3 * 0.7))))
-    n_cells = max(1, -(-cloud.n_groups // C))
     target_ctas = 2 * sm_count(dev)
     parts = max(1, -(-target_ctas // max(det.n_local, 1)))
-    parts = int(max(1, min(parts, n_cells // (2 * warps) if n_cells >= 2 * warps else 1)))
-    return ForwardPlan(C, parts, warps, tile)
+    parts = int(max(1, min(parts, cloud.n_groups // (4 * warps))))
+    return ForwardPlan(0, parts, warps, tile)
 
 
 def plan_adjoint(cloud: DeviceCloud, det: DeviceDetectors) -> int:

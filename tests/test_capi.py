@@ -47,7 +47,7 @@ def test_binding_matches_header(lib_path):
     assert lib.pab_version() == 100
     a, b, g = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
     lib.pab_record_sizes(ctypes.byref(a), ctypes.byref(b), ctypes.byref(g))
-    assert (a.value, b.value, g.value) == (16, 16, 32)
+    assert (a.value, b.value, g.value) == (16, 16, 48)
 
 
 def test_library_is_sm100a(lib_path):
