@@ -99,7 +99,8 @@ int pab_adam(double* param, const double* grad, double* m, double* v, int64_t co
              double bc2, double floor_value, int use_floor, void* stream);
 
 /* Stable compaction: idx_out <- ascending indices i with key[i] < 0 (mode 0),
- * <= 0 (mode 1) or != 0 (mode 2); *count_dev <- their number.
+ * <= 0 (mode 1), != 0 (mode 2), > 0 (mode 3) or == 0 (mode 4); *count_dev <-
+ * their number.
  * Replaces: the boolean subset in optimizer.py:255-256 / model.py:239-244. */
 size_t pab_compact_workspace_bytes(int64_t n);
 int pab_compact(const double* key, int64_t n, int mode, int32_t* idx_out, int* count_dev, void* workspace,
@@ -112,6 +113,33 @@ int pab_sumsq_diff_f64(const double* a, const double* b, int64_t n, double* out,
 
 /* dst[r][c] = src[idx[r]][c] for r < m, c < width (FP64). */
 int pab_gather_f64(const double* src, int width, const int32_t* idx, int64_t m, double* dst, void* stream);
+
+/* ---- Adaptive density control (optimizer.py:314-406) ----
+ * Exact k-th smallest (0-based) of x by 8-pass radix selection (workspace:
+ * pab_select_workspace_bytes); the median is the mean of the two middle order
+ * statistics for even n, as numpy's. */
+size_t pab_select_workspace_bytes(void);
+int pab_select_kth_f64(const double* x, int64_t n, int64_t k, double* out, void* workspace, void* stream);
+/* key[i] = -1 keep / +1 destroy: p0 < frac * median or a0 outside [a0_min, a0_max]
+ * (median_hi nullable: odd n).  Replaces optimizer.py:330-334. */
+int pab_density_keep_key(const double* p0, const double* a0, int64_t n, const double* median_lo,
+                         const double* median_hi, double frac, double a0_min, double a0_max, double* key,
+                         void* stream);
+/* key[i] = -1 split (a0 > split_a0) / +1 parent.  Replaces optimizer.py:349-350. */
+int pab_density_split_key(const double* a0, int64_t n, double split_a0, double* key, void* stream);
+/* out[r] = |v[idx[r]]| (idx nullable), numpy's sqrt((x*x + y*y) + z*z).  Replaces optimizer.py:345. */
+int pab_row_norms(const double* v, const int32_t* idx, int64_t m, double* out, void* stream);
+/* Duplicate selection (optimizer.py:378-384): key = -1 for gn > t, 0 for gn == t,
+ * +1 below; then the first k_dup - n_above ties (ascending) are set to -1. */
+int pab_density_dup_key(const double* gn, int64_t m, const double* t, double* key, void* stream);
+int pab_density_take_ties(const int32_t* ties, const int* n_ties, const int* n_above, int k_dup, int64_t m,
+                          double* key, void* stream);
+/* Split children (optimizer.py:352-357): +child rows [0, m), -child rows [m, 2m). */
+int pab_split_children(const double* pos, const double* p0, const double* a0, const double* unit, int64_t m,
+                       double* out_pos, double* out_p0, double* out_a0, void* stream);
+/* Duplicates (optimizer.py:385-389): pos + (a0 / 4) unit, p0 and a0 copied. */
+int pab_duplicate(const double* pos, const double* p0, const double* a0, const double* unit, int64_t m,
+                  double* out_pos, double* out_p0, double* out_a0, void* stream);
 
 #ifdef __cplusplus
 }

@@ -34,6 +34,15 @@ _SIGS = {
     "pab_gather_f64": ([_vp, _i, _vp, _i64, _vp, _vp], _i),
     "pab_sumsq_workspace_bytes": ([_i64], C.c_size_t),
     "pab_sumsq_diff_f64": ([_vp, _vp, _i64, _vp, _vp, _vp], _i),
+    "pab_select_workspace_bytes": ([], C.c_size_t),
+    "pab_select_kth_f64": ([_vp, _i64, _i64, _vp, _vp, _vp], _i),
+    "pab_density_keep_key": ([_vp, _vp, _i64, _vp, _vp, _d, _d, _d, _vp, _vp], _i),
+    "pab_density_split_key": ([_vp, _i64, _d, _vp, _vp], _i),
+    "pab_row_norms": ([_vp, _vp, _i64, _vp, _vp], _i),
+    "pab_density_dup_key": ([_vp, _i64, _vp, _vp, _vp], _i),
+    "pab_density_take_ties": ([_vp, _vp, _vp, _i, _i64, _vp, _vp], _i),
+    "pab_split_children": ([_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp], _i),
+    "pab_duplicate": ([_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp], _i),
 }
 EXPORTED = tuple(_SIGS)
 

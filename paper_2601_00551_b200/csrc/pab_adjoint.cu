@@ -192,18 +192,21 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       my_ops += (unsigned long long)(max(jhi - jlo + 1, 0) + max(nhi - nlo + 1, 0));
 
       Moments M = {0.f, 0.f, 0.f, 0.f};
-      const bool staged = hi - lo + 1 <= kSeg;
-      const float* seg = staged ? seg_all[warp][buf] : res + (size_t)(jb + jj) * n_out;
-      const int sbase = staged ? lo : 0;
-      moments_run<STAGE>(seg, jlo - sbase, jhi - jlo + 1, (float)(jlo * f - pg.kc), fs, sc, pg.phi * sc, M);
-      if (nlo <= nhi) {   // u+ = -kappa y: odd moments flip sign
-        Moments N = {0.f, 0.f, 0.f, 0.f};
-        moments_run<STAGE>(seg, nlo - sbase, nhi - nlo + 1, (float)(nlo * f - nkc), fs, sc, nphi * sc, N);
-        M.T0 += N.T0;
-        M.T1 -= N.T1;
-        M.T2 += N.T2;
-        M.T3 -= N.T3;
-      }
+      // separate call sites for the shared (staged) and global (wide) sources
+      // so the compiler emits LDS, not generic loads, on the hot path
+      auto walk = [&](const float* seg, int sbase) {
+        moments_run<STAGE>(seg, jlo - sbase, jhi - jlo + 1, (float)(jlo * f - pg.kc), fs, sc, pg.phi * sc, M);
+        if (nlo <= nhi) {   // u+ = -kappa y: odd moments flip sign
+          Moments N = {0.f, 0.f, 0.f, 0.f};
+          moments_run<STAGE>(seg, nlo - sbase, nhi - nlo + 1, (float)(nlo * f - nkc), fs, sc, nphi * sc, N);
+          M.T0 += N.T0;
+          M.T1 -= N.T1;
+          M.T2 += N.T2;
+          M.T3 -= N.T3;
+        }
+      };
+      if (hi - lo + 1 <= kSeg) walk(seg_all[warp][buf], lo);
+      else walk(res + (size_t)(jb + jj) * n_out, 0);
       __syncwarp();
 
       // per-pair gradient terms (reference radiator.py:275-286 in y units)

@@ -33,9 +33,16 @@ __global__ void adam_kernel(double* __restrict__ param, const double* __restrict
   param[i] = out;
 }
 
-// flags: keep = (x < 0) if strict else (x <= 0)  [mode 0/1], or x != 0 [mode 2]
+// flags: keep = (x < 0) if strict else (x <= 0)  [mode 0/1], x != 0 [mode 2],
+// x > 0 [mode 3], x == 0 [mode 4]
 __device__ __forceinline__ bool keep_pred(double x, int mode) {
-  return mode == 0 ? (x < 0.0) : (mode == 1 ? (x <= 0.0) : (x != 0.0));
+  switch (mode) {
+    case 0: return x < 0.0;
+    case 1: return x <= 0.0;
+    case 2: return x != 0.0;
+    case 3: return x > 0.0;
+    default: return x == 0.0;
+  }
 }
 
 constexpr int kCompactBlock = 1024;
@@ -164,7 +171,7 @@ size_t pab_compact_workspace_bytes(int64_t n) {
 int pab_compact(const double* key, int64_t n, int mode, int32_t* idx_out, int* count_dev, void* workspace,
                 void* stream) {
   if (n <= 0) return 0;
-  if (!key || !idx_out || !count_dev || !workspace || mode < 0 || mode > 2) return 1;
+  if (!key || !idx_out || !count_dev || !workspace || mode < 0 || mode > 4) return 1;
   const int nb = (int)((n + kCompactBlock - 1) / kCompactBlock);
   int* counts = (int*)workspace;
   const cudaStream_t s = (cudaStream_t)stream;

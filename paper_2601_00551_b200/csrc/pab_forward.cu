@@ -39,38 +39,47 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 }
 
 // acc[slot] += Ak * y G over n consecutive samples starting at column pointer
-// t (row stride 32 floats, no wrap inside), m-offset mf, step fs.
+// t (row stride 32 floats, no wrap inside), m-offset mf, step fs.  Eight
+// samples per iteration ride four packed FP32x2 registers (FFMA2/FMUL2); all
+// eight shared-memory reads are issued before the arithmetic (ILP).
+__device__ __forceinline__ float2 contrib2(float2 y, float2 Ak2) {
+  const float2 q = __fmul2_rn(y, y);
+  return __fmul2_rn(Ak2, __fmul2_rn(y, make_float2(ex2(-q.x), ex2(-q.y))));
+}
+
 __device__ __forceinline__ void rmw_run(float* t, int n, float mf, float fs, float sc, float ps, float Ak) {
-  // samples (i, i+1) and (i+2, i+3) ride packed FP32x2 registers (FFMA2/FMUL2)
-  int i = 0;
   const float2 nsc2 = make_float2(-sc, -sc);
-  const float2 ps2 = make_float2(ps, ps);
   const float2 Ak2 = make_float2(Ak, Ak);
-  float2 ma = make_float2(mf, mf + fs), mb = make_float2(mf + 2.0f * fs, mf + 3.0f * fs);
-  const float2 step4 = make_float2(4.0f * fs, 4.0f * fs);
+  // y of pair k of an 8-sample block: (mb + 2k fs, mb + (2k+1) fs) * -sc + ps
+  const float2 c0 = make_float2(ps, fmaf(fs, -sc, ps));
+  const float2 c1 = make_float2(fmaf(2.0f * fs, -sc, ps), fmaf(3.0f * fs, -sc, ps));
+  const float2 c2 = make_float2(fmaf(4.0f * fs, -sc, ps), fmaf(5.0f * fs, -sc, ps));
+  const float2 c3 = make_float2(fmaf(6.0f * fs, -sc, ps), fmaf(7.0f * fs, -sc, ps));
+  int i = 0;
 #pragma unroll 1
-  for (; i + 4 <= n; i += 4, t += 4 * kWarp) {
-    const float2 ya = __ffma2_rn(ma, nsc2, ps2);
-    const float2 yb = __ffma2_rn(mb, nsc2, ps2);
-    const float2 oa = make_float2(t[0], t[kWarp]);
-    const float2 ob = make_float2(t[2 * kWarp], t[3 * kWarp]);
-    const float2 qa = __fmul2_rn(ya, ya), qb = __fmul2_rn(yb, yb);
-    const float2 Ga = make_float2(ex2(-qa.x), ex2(-qa.y));
-    const float2 Gb = make_float2(ex2(-qb.x), ex2(-qb.y));
-    const float2 na = __ffma2_rn(Ak2, __fmul2_rn(ya, Ga), oa);
-    const float2 nb = __ffma2_rn(Ak2, __fmul2_rn(yb, Gb), ob);
-    t[0] = na.x;
-    t[kWarp] = na.y;
-    t[2 * kWarp] = nb.x;
-    t[3 * kWarp] = nb.y;
-    ma = __fadd2_rn(ma, step4);
-    mb = __fadd2_rn(mb, step4);
+  for (; i + 8 <= n; i += 8, mf += 8.0f * fs, t += 8 * kWarp) {
+    const float2 m2 = make_float2(mf, mf);
+    const float2 o0 = make_float2(t[0], t[kWarp]);
+    const float2 o1 = make_float2(t[2 * kWarp], t[3 * kWarp]);
+    const float2 o2 = make_float2(t[4 * kWarp], t[5 * kWarp]);
+    const float2 o3 = make_float2(t[6 * kWarp], t[7 * kWarp]);
+    const float2 n0 = __fadd2_rn(o0, contrib2(__ffma2_rn(m2, nsc2, c0), Ak2));
+    const float2 n1 = __fadd2_rn(o1, contrib2(__ffma2_rn(m2, nsc2, c1), Ak2));
+    const float2 n2 = __fadd2_rn(o2, contrib2(__ffma2_rn(m2, nsc2, c2), Ak2));
+    const float2 n3 = __fadd2_rn(o3, contrib2(__ffma2_rn(m2, nsc2, c3), Ak2));
+    t[0] = n0.x; t[kWarp] = n0.y; t[2 * kWarp] = n1.x; t[3 * kWarp] = n1.y;
+    t[4 * kWarp] = n2.x; t[5 * kWarp] = n2.y; t[6 * kWarp] = n3.x; t[7 * kWarp] = n3.y;
   }
-  mf = ma.x;
 #pragma unroll 1
-  for (; i < n; ++i, mf += fs, t += kWarp) {
+  for (; i + 2 <= n; i += 2, mf += 2.0f * fs, t += 2 * kWarp) {
+    const float2 o = make_float2(t[0], t[kWarp]);
+    const float2 nv = __fadd2_rn(o, contrib2(__ffma2_rn(make_float2(mf, mf), nsc2, c0), Ak2));
+    t[0] = nv.x;
+    t[kWarp] = nv.y;
+  }
+  if (i < n) {
     const float y = fmaf(mf, -sc, ps);
-    *t = fmaf(Ak, y * ex2(-y * y), *t);
+    *t += Ak * (y * ex2(-y * y));
   }
 }
 
@@ -140,7 +149,7 @@ __device__ __forceinline__ void evaluate_pair(float* tile, int lane, const Acq& 
 }
 
 template <int DIR>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(128, 2)
 forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
                const GroupMeta* __restrict__ gmeta, int64_t n_groups,
                const double* __restrict__ det_pos, const double* __restrict__ det_aux, int n_det,
@@ -258,12 +267,13 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
         else my_stage[r - zone_end] = v;
       };
       int fp = zs[warp];
+      int touched = fp - 1;   // highest row any window of this sweep may have written
       for (int i0 = s_begin; i0 < s_end; i0 += kWarp) {
         const int nb = min(kWarp, s_end - i0);
         // lane l prepares the geometry of the l-th group of this batch
         GroupDet gd_l = empty_gd();
         int64_t g_l = 0;
-        int bin_l = 0, near_l = 0;
+        int bin_l = 0, near_l = 0, hi_l = -1;
         if (lane < nb) {
           const int gl = sorted[i0 + lane];
           g_l = cg0 + gl;
@@ -271,6 +281,8 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
           const GroupMeta gm = gmeta[g_l];
           gd_l = group_det(gm, det.px, det.py, det.pz, acq);
           near_l = group_near(acq, gd_l, gm) ? 1 : 0;
+          int glo;
+          group_range(acq, gd_l, gm, &glo, &hi_l);
         }
         // software pipeline: records of the next group are loaded while the
         // current one is evaluated
@@ -289,17 +301,19 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
           }
           const int blo = __shfl_sync(0xffffffffu, bin_l, k) << kBinShift;
           const int near = __shfl_sync(0xffffffffu, near_l, k);
-          if (blo > fp) {
-            flush_rows(tile, lane, fp, min(blo, fp + kTile), sink);
+          const int ghi = __shfl_sync(0xffffffffu, hi_l, k);
+          if (blo > fp) {   // rows past the last touched one are still zero: skip them
+            flush_rows(tile, lane, fp, min(min(blo, fp + kTile), touched + 1), sink);
             fp = blo;
           }
+          touched = max(touched, ghi);
           GroupMeta gm;
           if (gd.slow) gm = gmeta[g];
           evaluate_pair<DIR>(tile, lane, acq, gd, gm, det, dd, A, B, near, my_ops, coinc, INT_MIN, INT_MAX);
           __syncwarp();
         }
       }
-      if (s_begin < s_end) flush_rows(tile, lane, fp, min(fp + kTile, n_out), sink);
+      if (s_begin < s_end) flush_rows(tile, lane, fp, min(min(fp + kTile, n_out), touched + 1), sink);
     }
     __syncthreads();
 
@@ -415,7 +429,7 @@ int pab_forward(const void* rec_a, const void* rec_b, const void* group_meta, in
   (void)groups_per_cell;
   (void)tile_rows;
   if (n_det <= 0 || n_out <= 0) return 0;
-  if (f < 1 || partitions < 1 || warps < 1 || warps > 8) return 1;
+  if (f < 1 || partitions < 1 || warps < 1 || warps > 4) return 1;
   if (!rec_a || !rec_b || !group_meta || !det_pos || !det_aux || !partial_rows || !ops_total || !status)
     return 1;
   if ((int64_t)n_out * f > (1 << 24)) return 1;

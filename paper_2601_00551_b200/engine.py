@@ -25,7 +25,7 @@ from .parallel import Shard, allreduce_scalar, allreduce_sum_, current_shard, ga
 STATUS_COINCIDENT = 2
 STATUS_NONFINITE = 8
 
-FORWARD_WARPS = 8
+FORWARD_WARPS = 4   # 2 CTAs per SM: one CTA sorts while the other sweeps
 FORWARD_TILE_ROWS = 128
 ADJOINT_WARPS = 8
 GROUP = 32
@@ -237,14 +237,15 @@ class ForwardPlan:
 
 
 def plan_forward(cloud: DeviceCloud, det: DeviceDetectors, acq: Acq) -> ForwardPlan:
-    """One CTA (8 warps, ~165-190 KB smem) per SM: detectors x partitions
-    should cover >= 2 waves; each partition keeps >= 4 lane groups per warp."""
+    """Two CTAs (4 warps, ~100-110 KB smem each) per SM: detectors x
+    partitions should cover >= 6 waves (tail < 3%); each partition keeps >= 4
+    lane groups per warp."""
     dev = cloud.dev
     tile = FORWARD_TILE_ROWS
     warps = FORWARD_WARPS
     while warps > 1 and _lib.load().pab_forward_smem_bytes(acq.n_out, warps, tile) > 227 * 1024:
         warps //= 2
-    target_ctas = 2 * sm_count(dev)
+    target_ctas = 12 * sm_count(dev)   # >= 6 waves of 2 resident CTAs per SM
     parts = max(1, -(-target_ctas // max(det.n_local, 1)))
     parts = int(max(1, min(parts, cloud.n_groups // (4 * warps))))
     return ForwardPlan(0, parts, warps, tile)

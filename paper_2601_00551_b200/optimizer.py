@@ -196,7 +196,7 @@ class OptimState:
     # -- cloud ------------------------------------------------------------
     def _set_cloud(self, cloud: PointCloud) -> None:
         self._dc = E.DeviceCloud.from_host(cloud.positions, cloud.p0, cloud.a0, self._dev)
-        self._a0_free = np.asarray(cloud.a0_free, dtype=np.float64).copy()
+        self._free = torch.from_numpy(np.ascontiguousarray(cloud.a0_free, dtype=np.float64)).to(self._dev)
         self._generation = int(cloud.generation)
         self._host_cache = None
 
@@ -205,7 +205,7 @@ class OptimState:
         if self._host_cache is None:
             dc = self._dc
             self._host_cache = PointCloud(dc.pos.cpu().numpy(), dc.p0.cpu().numpy(), dc.a0.cpu().numpy(),
-                                          self._a0_free.copy(), self._generation)
+                                          self._free.cpu().numpy(), self._generation)
         return self._host_cache
 
     @cloud.setter
@@ -264,9 +264,12 @@ class FilterReport:
 
 
 def _compact_indices(key: torch.Tensor, mode: int) -> torch.Tensor:
-    """Ascending indices i with key[i] < 0 (mode 0) / <= 0 (mode 1) / != 0 (mode 2)."""
+    """Ascending indices i with key[i] < 0 (mode 0) / <= 0 (1) / != 0 (2) /
+    > 0 (3) / == 0 (4)."""
     n = key.numel()
     dev = key.device
+    if n == 0:
+        return torch.empty(0, dtype=torch.int32, device=dev)
     ws = E.workspace(dev)
     idx = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
     count = ws.get("compact_count", 1, torch.int32)
@@ -373,63 +376,114 @@ def step(state: OptimState, ctx, real_k, f: int, stage: str):
 # ---------------------------------------------------------------------------
 
 
+def _select(x: torch.Tensor, k: int, out: torch.Tensor) -> None:
+    """out[0] = k-th smallest (0-based) of x (exact radix selection on device)."""
+    ws = E.workspace(x.device)
+    st = ws.get("select_state", int(_lib.load().pab_select_workspace_bytes()) // 8, torch.int64)
+    call("pab_select_kth_f64", ptr(x), x.numel(), int(k), ptr(out), ptr(st), E._stream())
+
+
 def density_control(state: OptimState, thresholds: DensityThresholds, stage: str) -> OptimState:
     """Destroy weak / out-of-range balls, split oversized ones, duplicate the
-    top decile by position-gradient norm (fine).  Runs every 100-200
-    iterations on the host copies (O(n)); SplitMix64 streams are bit-exact
-    with the reference (CounterRng.spawn(generation))."""
+    top decile by position-gradient norm (fine); optimizer.py:314-406.
+
+    Runs on the GPU (``pab_select_kth_f64``, ``pab_density_*``,
+    ``pab_compact``, gathers); the isotropic unit vectors are drawn from the
+    reference's SplitMix64 stream (``CounterRng(seed).spawn(generation)``) on
+    the host in the reference's order (split children first, then
+    duplicates) and uploaded.  Outputs are bit-identical to the reference."""
     n = state.n
     if n == 0:
         state._generation += 1
         state._host_cache = None
         return state
+    dev = state._dev
     dc = state._dc
-    pos_all, p0_all, a0_all = dc.pos.cpu().numpy(), dc.p0.cpu().numpy(), dc.a0.cpu().numpy()
-    m_h = {k: t.cpu().numpy() for k, t in state._m.items()}
-    v_h = {k: t.cpu().numpy() for k, t in state._v.items()}
     rng = CounterRng(state.seed).spawn(state._generation)
-    median_p0 = float(np.median(p0_all))
-    weak = p0_all < thresholds.destroy_p0_frac * median_p0
-    bad = (a0_all < thresholds.a0_min) | (a0_all > thresholds.a0_max)
-    surv = np.flatnonzero(~(weak | bad))
-    pos, p0, a0, free = pos_all[surv], p0_all[surv], a0_all[surv], state._a0_free[surv]
-    m = {k: x[surv] for k, x in m_h.items()}
-    v = {k: x[surv] for k, x in v_h.items()}
+    f64 = lambda m: torch.empty(m, dtype=torch.float64, device=dev)
+    up = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)
+
+    # destroy: p0 below frac * median, a0 outside [a0_min, a0_max]
+    med = f64(2)
+    _select(dc.p0, (n - 1) // 2, med[0:1])
+    if n % 2 == 0:
+        _select(dc.p0, n // 2, med[1:2])
+    key = f64(n)
+    call("pab_density_keep_key", ptr(dc.p0), ptr(dc.a0), n, ptr(med[0:1]), ptr(med[1:2]) if n % 2 == 0 else None,
+         float(thresholds.destroy_p0_frac), float(thresholds.a0_min), float(thresholds.a0_max), ptr(key),
+         E._stream())
+    surv = _compact_indices(key, 0)
+    ns = surv.numel()
+    pos, p0, a0 = _gather(dc.pos, 3, surv).view(ns, 3), _gather(dc.p0, 1, surv), _gather(dc.a0, 1, surv)
+    free = _gather(state._free, 1, surv)
+    m = {"p0": _gather(state._m["p0"], 1, surv), "a0": _gather(state._m["a0"], 1, surv),
+         "position": _gather(state._m["position"], 3, surv).view(ns, 3)}
+    v = {"p0": _gather(state._v["p0"], 1, surv), "a0": _gather(state._v["a0"], 1, surv),
+         "position": _gather(state._v["position"], 3, surv).view(ns, 3)}
     gnorm = None
-    if state._last is not None:
-        gnorm = np.linalg.norm(state._last.d_pos_t.cpu().numpy(), axis=1)[surv]
-    split = a0 > thresholds.split_a0
-    sidx = np.flatnonzero(split)
-    parts = [[pos[~split]], [p0[~split]], [a0[~split]], [free[~split]]]
-    if sidx.size:
-        off = 0.5 * a0[sidx, None] * rng.unit_vectors(sidx.size)
-        parts[0].append(np.concatenate([pos[sidx] + off, pos[sidx] - off]))
-        parts[1].append(np.concatenate([0.5 * p0[sidx]] * 2))
-        parts[2].append(np.concatenate([a0[sidx] / math.sqrt(2.0)] * 2))
-        parts[3].append(np.concatenate([free[sidx]] * 2))
-    m = {k: x[~split] for k, x in m.items()}
-    v = {k: x[~split] for k, x in v.items()}
-    if stage == "fine" and gnorm is not None and gnorm[~split].size:
-        gn = gnorm[~split]
-        k_dup = min(math.ceil((1.0 - thresholds.duplicate_grad_quantile) * gn.size), gn.size)
+    if state._last is not None and ns:
+        gnorm = f64(ns)
+        call("pab_row_norms", ptr(state._last.d_pos_t), ptr(surv), ns, ptr(gnorm), E._stream())
+
+    # split: a0 > split_a0 -> two children
+    skey = f64(max(ns, 1))[:ns]
+    if ns:
+        call("pab_density_split_key", ptr(a0), ns, float(thresholds.split_a0), ptr(skey), E._stream())
+    S = _compact_indices(skey, 0)
+    K = _compact_indices(skey, 3)
+    nS, nK = S.numel(), K.numel()
+    par_pos, par_p0, par_a0 = _gather(pos, 3, K).view(nK, 3), _gather(p0, 1, K), _gather(a0, 1, K)
+    par_free = _gather(free, 1, K)
+    parts_pos, parts_p0, parts_a0, parts_free = [par_pos], [par_p0], [par_a0], [par_free]
+    if nS:
+        unit = up(rng.unit_vectors(nS))
+        cpos, cp0, ca0 = f64(2 * nS * 3), f64(2 * nS), f64(2 * nS)
+        call("pab_split_children", ptr(_gather(pos, 3, S)), ptr(_gather(p0, 1, S)), ptr(_gather(a0, 1, S)),
+             ptr(unit), nS, ptr(cpos), ptr(cp0), ptr(ca0), E._stream())
+        sfree = _gather(free, 1, S)
+        parts_pos.append(cpos.view(2 * nS, 3))
+        parts_p0.append(cp0)
+        parts_a0.append(ca0)
+        parts_free.append(torch.cat([sfree, sfree]))
+
+    # duplicate (fine): top ceil((1 - q) n_live) by |grad pos|, ties by index
+    if stage == "fine" and gnorm is not None and nK:
+        gn = _gather(gnorm, 1, K)
+        k_dup = min(math.ceil((1.0 - thresholds.duplicate_grad_quantile) * nK), nK)
         if k_dup > 0:
-            order = np.sort(np.argsort(-gn, kind="stable")[:k_dup])
-            kp = (parts[0][0], parts[1][0], parts[2][0], parts[3][0])
-            jitter = (kp[2][order, None] / 4.0) * rng.unit_vectors(order.size)
-            parts[0].append(kp[0][order] + jitter)
-            parts[1].append(kp[1][order])
-            parts[2].append(kp[2][order])
-            parts[3].append(kp[3][order])
-    n_kept = parts[0][0].shape[0]
-    new = PointCloud(np.concatenate(parts[0]), np.concatenate(parts[1]), np.concatenate(parts[2]),
-                     np.concatenate(parts[3]), generation=state._generation + 1)
-    n_new = len(new)
-    state._set_cloud(new)
-    for key in _KEYS:
-        fresh = (n_new - n_kept,) + m[key].shape[1:]
-        up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(state._dev)
-        state._m[key] = up(np.concatenate([m[key], np.zeros(fresh)]))
-        state._v[key] = up(np.concatenate([v[key], np.zeros(fresh)]))
+            t = f64(1)
+            _select(gn, nK - k_dup, t)
+            dkey = f64(nK)
+            call("pab_density_dup_key", ptr(gn), nK, ptr(t), ptr(dkey), E._stream())
+            above = _compact_indices(dkey, 0)
+            ties = _compact_indices(dkey, 4)
+            cnt = torch.tensor([ties.numel(), above.numel()], dtype=torch.int32, device=dev)
+            call("pab_density_take_ties", ptr(ties), ptr(cnt[0:1]), ptr(cnt[1:2]), int(k_dup), nK, ptr(dkey),
+                 E._stream())
+            order = _compact_indices(dkey, 0)
+            unit = up(rng.unit_vectors(order.numel()))
+            k = order.numel()
+            dpos, dp0, da0 = f64(3 * k), f64(k), f64(k)
+            call("pab_duplicate", ptr(_gather(par_pos, 3, order)), ptr(_gather(par_p0, 1, order)),
+                 ptr(_gather(par_a0, 1, order)), ptr(unit), k, ptr(dpos), ptr(dp0), ptr(da0), E._stream())
+            parts_pos.append(dpos.view(k, 3))
+            parts_p0.append(dp0)
+            parts_a0.append(da0)
+            parts_free.append(_gather(par_free, 1, order))
+
+    new_pos = torch.cat(parts_pos).contiguous()
+    n_new = new_pos.shape[0]
+    state._dc = E.DeviceCloud(new_pos, torch.cat(parts_p0), torch.cat(parts_a0))
+    state._free = torch.cat(parts_free)
+    for src, dst in ((m, state._m), (v, state._v)):
+        for key_ in _KEYS:
+            kept = _gather(src[key_], 3 if key_ == "position" else 1, K)
+            shape = (n_new, 3) if key_ == "position" else (n_new,)
+            z = torch.zeros(shape, dtype=torch.float64, device=dev)
+            z[:nK] = kept.view(nK, 3) if key_ == "position" else kept
+            dst[key_] = z
+    state._generation += 1
+    state._host_cache = None
     state._last = None
     return state
 
@@ -496,8 +550,7 @@ def _filter_state_(state: OptimState, det, acq, real_local, strict: bool = True)
         d["p0"] = ws_gather(d["p0"], 1)
         d["a0"] = ws_gather(d["a0"], 1)
         d["position"] = ws_gather(d["position"], 3).view(m, 3)
-    keep = idx.cpu().numpy()
-    state._a0_free = state._a0_free[keep]
+    state._free = ws_gather(state._free, 1)
     state._host_cache = None
     state._last = None
 

@@ -150,6 +150,127 @@ def toy_config(directivity=("none",)) -> Scene:
     return Scene("toy", array, grid, truth, init, tuple(directivity))
 
 
+def branching_tubes(n_balls: int, n_tubes: int, radius_range, box_lo, box_hi, p0_range=(0.5, 1.0),
+                    a0: float = 0.1 * MM, seed: int = SEED_TRUTH, segment: float = 1.0 * MM,
+                    steps: int = 12) -> PointCloud:
+    """Random vessel trees: a few roots inside the box, each tube a smooth
+    random walk of `steps` segments; later tubes branch off random points of
+    earlier ones.  Balls are spread over tubes by length, uniform in the tube
+    cross-section (radius drawn per tube from `radius_range`)."""
+    rng = CounterRng(seed)
+    lo, hi = np.asarray(box_lo, dtype=float), np.asarray(box_hi, dtype=float)
+    n_roots = max(1, n_tubes // 5)
+    tubes = []
+    for t in range(n_tubes):
+        if t < n_roots or not tubes:
+            start = lo + (hi - lo) * rng.uniform(0.2, 0.8, 3)
+        else:
+            parent = tubes[int(rng.uniform(0.0, len(tubes), 1)[0]) % len(tubes)]
+            start = parent[int(rng.uniform(0.0, len(parent), 1)[0]) % len(parent)]
+        d = rng.unit_vectors(1)[0]
+        pts = [start]
+        for _ in range(steps):
+            d = d + 0.5 * rng.unit_vectors(1)[0]
+            d /= np.linalg.norm(d)
+            nxt = np.clip(pts[-1] + segment * d, lo, hi)
+            pts.append(nxt)
+        tubes.append(np.array(pts))
+    radii = rng.uniform(radius_range[0], radius_range[1], n_tubes)
+    seg_len = [np.linalg.norm(np.diff(tb, axis=0), axis=1) for tb in tubes]
+    total = np.array([s.sum() for s in seg_len])
+    counts = np.floor(n_balls * total / total.sum()).astype(np.int64)
+    counts[: n_balls - counts.sum()] += 1
+    out = []
+    for tb, sl, cnt, rad in zip(tubes, seg_len, counts, radii):
+        if cnt == 0:
+            continue
+        cum = np.concatenate([[0.0], np.cumsum(sl)])
+        s = rng.uniform(0.0, max(cum[-1], 1e-12), int(cnt))
+        k = np.clip(np.searchsorted(cum, s, side="right") - 1, 0, len(sl) - 1)
+        frac = (s - cum[k]) / np.maximum(sl[k], 1e-12)
+        centre = tb[k] + frac[:, None] * (tb[k + 1] - tb[k])
+        off = rng.unit_vectors(int(cnt)) * (rad * np.cbrt(rng.uniform(0.0, 1.0, int(cnt))))[:, None]
+        out.append(centre + off)
+    pos = np.concatenate(out)[:n_balls]
+    p0 = rng.uniform(p0_range[0], p0_range[1], pos.shape[0])
+    return PointCloud(pos, p0, np.full(pos.shape[0], a0))
+
+
+def schedule_config(directivity=("none",), grid_n: int = 96) -> Scene:
+    """BASELINE config 3: 512 detectors = seeded random subset of a
+    2,048-point Fibonacci hemisphere (r = 40 mm); 50k truth balls on 40
+    branching tubes; 96^3 init grid over the interior box [-14, 14]^2 x
+    [-30, -2] mm (p0 = 0.1, a0 = 0.15 mm); 40 MHz x 4096 samples."""
+    full = fibonacci_hemisphere(2048, 40 * MM)
+    pick = np.sort(np.argsort(CounterRng(SEED_GEOMETRY).uniform(0.0, 1.0, 2048))[:512])
+    array = SensorArray(full.positions[pick], 1500.0, normals=full.normals[pick])
+    grid = TimeGrid(0.0, 1.0 / 40e6, 4096)
+    lo, hi = np.array([-14, -14, -30]) * MM, np.array([14, 14, -2]) * MM
+    truth = branching_tubes(50_000, 40, (0.1 * MM, 0.3 * MM), lo + 2 * MM, hi - 2 * MM)
+    step = (hi - lo) / grid_n
+    axes = [lo[a] + (np.arange(grid_n) + 0.5) * step[a] for a in range(3)]
+    gx, gy, gz = np.meshgrid(*axes, indexing="ij")
+    pos = np.column_stack([gx.ravel(), gy.ravel(), gz.ravel()])
+    init = PointCloud(pos, np.full(pos.shape[0], 0.1), np.full(pos.shape[0], 0.15 * MM))
+    return Scene("schedule", array, grid, truth, init, tuple(directivity))
+
+
+def planar_config(n_balls: int = 4_000_000, directivity=("element", 0.5 * MM)) -> Scene:
+    """BASELINE config 4: 32 x 32 planar detectors at 1.5 mm pitch on z = 0,
+    each outward normal (+z) tilted by theta <= 30 deg (cos theta uniform)
+    about a random azimuth; 4M balls in a 30 x 30 x 15 mm slab at
+    z in [-20, -5] mm, p0 = exp(N(-1, 0.5)), a0 ~ U[0.05, 0.2] mm;
+    40 MHz x 6144 samples; 0.5 mm square element directivity."""
+    rng = CounterRng(SEED_GEOMETRY)
+    ax = (np.arange(32) - 15.5) * 1.5 * MM
+    gx, gy = np.meshgrid(ax, ax, indexing="ij")
+    pos = np.column_stack([gx.ravel(), gy.ravel(), np.zeros(1024)])
+    cth = rng.uniform(math.cos(math.radians(30.0)), 1.0, 1024)
+    az = rng.uniform(0.0, 2.0 * math.pi, 1024)
+    sth = np.sqrt(1.0 - cth * cth)
+    normals = np.column_stack([sth * np.cos(az), sth * np.sin(az), cth])
+    array = SensorArray(pos, 1500.0, normals=normals)
+    grid = TimeGrid(0.0, 1.0 / 40e6, 6144)
+    r = CounterRng(SEED_TRUTH)
+    bp = np.column_stack([r.uniform(-15 * MM, 15 * MM, n_balls), r.uniform(-15 * MM, 15 * MM, n_balls),
+                          r.uniform(-20 * MM, -5 * MM, n_balls)])
+    p0 = np.exp(-1.0 + 0.5 * r.normal(n_balls))
+    a0 = r.uniform(0.05 * MM, 0.2 * MM, n_balls)
+    cloud = PointCloud(bp, p0, a0)
+    p0_true = np.exp(-1.0 + 0.5 * CounterRng(SEED_RESAMPLE).normal(n_balls))
+    return Scene("planar", array, grid, PointCloud(bp, p0_true, a0), cloud, tuple(directivity))
+
+
+def mouse_config(grid_n: int = 256, n_truth: int = 300_000, n_det: int = 2048,
+                 directivity=("cos_power", 2.0)) -> Scene:
+    """BASELINE config 5: 256^3 grid cropped to the ellipsoid with full axes
+    25 x 20 x 40 mm (about 8.8M balls survive; BASELINE's '16M' is the
+    uncropped 256^3 = 16.8M); 300k truth balls on 500 tubes of radius
+    0.05-0.4 mm; 2048 detectors on a seeded ring cylinder (radius 30 mm,
+    z in [-25, 25] mm) with normals tilted randomly by <= 30 deg from the
+    inward radial direction; 40 MHz x 8192 samples."""
+    semi = np.array([12.5, 10.0, 20.0]) * MM
+    ax = [(-1.0 + (np.arange(grid_n) + 0.5) * 2.0 / grid_n) * semi[a] for a in range(3)]
+    gx, gy, gz = np.meshgrid(*ax, indexing="ij")
+    inside = (gx / semi[0]) ** 2 + (gy / semi[1]) ** 2 + (gz / semi[2]) ** 2 <= 1.0
+    pos = np.column_stack([gx[inside], gy[inside], gz[inside]])
+    init = PointCloud(pos, np.full(pos.shape[0], 0.1), np.full(pos.shape[0], 0.1 * MM))
+    truth = branching_tubes(n_truth, 500, (0.05 * MM, 0.4 * MM), -0.7 * semi, 0.7 * semi,
+                            a0=0.1 * MM, steps=16)
+    rng = CounterRng(SEED_GEOMETRY)
+    phi = rng.uniform(0.0, 2.0 * math.pi, n_det)
+    z = rng.uniform(-25 * MM, 25 * MM, n_det)
+    R = 30 * MM
+    dpos = np.column_stack([R * np.cos(phi), R * np.sin(phi), z])
+    radial = np.column_stack([np.cos(phi), np.sin(phi), np.zeros(n_det)])   # outward
+    tilt = rng.unit_vectors(n_det) * np.tan(math.radians(30.0)) * np.cbrt(rng.uniform(0, 1, n_det))[:, None]
+    nrm = radial + tilt - np.sum(tilt * radial, axis=1, keepdims=True) * radial
+    nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    array = SensorArray(dpos, 1500.0, normals=nrm)
+    grid = TimeGrid(0.0, 1.0 / 40e6, 8192)
+    return Scene("mouse", array, grid, truth, init, tuple(directivity))
+
+
 def microbench_config(n_balls: int = 1_000_000, n_det: int = 1024, n_samples: int = 4096,
                       directivity=("cos_power", 2.0)) -> Scene:
     """BASELINE config 2: uniform balls in a 20 mm cube, p0 ~ U[0, 1],
