@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-balls", type=int, default=20000, help="oracle sample: balls x 64 detectors")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--recon", action="store_true",
+                    help="also time the full config-3 reconstruction (filter + 300 iterations)")
     return ap.parse_args()
 
 
@@ -158,6 +160,34 @@ def run_reference(args, rank, world):
 # ---------------------------------------------------------------------------
 # Our arm
 # ---------------------------------------------------------------------------
+
+def run_recon():
+    """BASELINE config 3 end to end through the public API: zero-gradient
+    filter of the 96^3 grid at f = 4, then the (4,100,coarse), (2,100,fine),
+    (1,100,fine) schedule with the filter re-applied every 10 iterations and
+    the reference density-control cadence; host wall clock."""
+    import torch
+
+    import paper_2601_00551_b200 as P
+    from paper_2601_00551_b200 import scenes
+    sc = scenes.schedule_config()
+    ctx = P.ForwardContext(sc.array, sc.grid)
+    real = P.simulate_signals(sc.truth, ctx)
+    spacing = 28e-3 / 96
+    th = P.DensityThresholds.from_spacing(spacing)
+    lr = P.LearningRates.from_spacing(spacing)
+    sched = P.Schedule((P.Level(4, 100, "coarse"), P.Level(2, 100, "fine"), P.Level(1, 100, "fine")),
+                       duplication_period=100)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    kept, rep = P.zero_gradient_filter(sc.init, ctx, real, f=4)
+    final, trace = P.run_hierarchical(kept, ctx, real, sched, th, lr=lr, seed=103, filter_every=10, plateau=False)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    return {"workload": "config3: 512 det, 96^3 init, 50k-ball truth, 40 MHz x 4096, schedule 4/2/1 x 100",
+            "wall_s": wall, "iterations": len(trace.records), "n_init": len(sc.init), "n_after_filter": len(kept),
+            "n_final": len(final), "loss_first": trace.records[0].loss, "loss_last": trace.records[-1].loss}
+
 
 def main():
     args = parse()
@@ -312,7 +342,11 @@ def main():
             "data": "synthetic (seeded CounterRng, BASELINE config 2)", "config": config_dict(args, world),
             "in_window_samples_per_step": samples, "samples_per_pair": samples / pairs,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": sampler.summary(),
-            "gpu_launches": 4 * args.steps}
+            "gpu_launches": 4 * args.steps,
+            "kernel_ms_min_median": {"forward+residual": [min(fwd_ms), statistics.median(fwd_ms)],
+                                     "adjoint+finalize": [min(adj_ms), statistics.median(adj_ms)]}}
+    if args.recon:
+        line["recon"] = run_recon()
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

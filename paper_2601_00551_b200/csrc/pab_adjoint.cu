@@ -23,10 +23,15 @@
 namespace pab {
 
 constexpr int kSeg = 256;   // staged residual samples per warp and buffer
+constexpr int kPad = 96;    // zero padding after the staged samples (uniform-walk overrun)
 
 __device__ __forceinline__ void cp_async4(float* smem_dst, const float* gsrc) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async16(float* smem_dst, const float* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gsrc));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
@@ -104,6 +109,50 @@ __device__ __forceinline__ void moments_run(const float* seg, int off, int n, fl
   M.T3 += A3.x + A3.y;
 }
 
+// Warp-uniform masked walk over the staged segment: every lane runs `nblk`
+// 8-sample blocks from its own 8-aligned start J0 (16-byte aligned LDS.128);
+// samples outside the lane's support (q > qmax) get G = 0 and contribute an
+// exact 0 (the staged residual is finite and zero-padded).
+template <int STAGE>
+__device__ __forceinline__ void moment_pair_masked(float2 res, float2 y, float qmax, float2& A0, float2& A1,
+                                                   float2& A2, float2& A3) {
+  const float2 q = __fmul2_rn(y, y);
+  const float2 G = make_float2(q.x <= qmax ? ex2(-q.x) : 0.0f, q.y <= qmax ? ex2(-q.y) : 0.0f);
+  const float2 r = __fmul2_rn(res, G);
+  const float2 t = __fmul2_rn(r, y);
+  A1 = __fadd2_rn(A1, t);
+  if (STAGE >= kStageCoarse) A3 = __ffma2_rn(t, q, A3);
+  if (STAGE == kStageFine) {
+    A0 = __fadd2_rn(A0, r);
+    A2 = __ffma2_rn(t, y, A2);
+  }
+}
+
+template <int STAGE>
+__device__ __forceinline__ void moments_uniform(const float* seg, int off, int nblk, float mf, float fs, float sc,
+                                                float ps, float qmax, Moments& M) {
+  const float4* s4 = reinterpret_cast<const float4*>(seg + off);
+  float2 A0 = make_float2(0.f, 0.f), A1 = A0, A2 = A0, A3 = A0;
+  const float2 nsc2 = make_float2(-sc, -sc);
+  const float2 c0 = make_float2(ps, fmaf(fs, -sc, ps));
+  const float2 c1 = make_float2(fmaf(2.0f * fs, -sc, ps), fmaf(3.0f * fs, -sc, ps));
+  const float2 c2 = make_float2(fmaf(4.0f * fs, -sc, ps), fmaf(5.0f * fs, -sc, ps));
+  const float2 c3 = make_float2(fmaf(6.0f * fs, -sc, ps), fmaf(7.0f * fs, -sc, ps));
+#pragma unroll 1
+  for (int b = 0; b < nblk; ++b, s4 += 2, mf += 8.0f * fs) {
+    const float4 ra = s4[0], rb = s4[1];
+    const float2 m2 = make_float2(mf, mf);
+    moment_pair_masked<STAGE>(make_float2(ra.x, ra.y), __ffma2_rn(m2, nsc2, c0), qmax, A0, A1, A2, A3);
+    moment_pair_masked<STAGE>(make_float2(ra.z, ra.w), __ffma2_rn(m2, nsc2, c1), qmax, A0, A1, A2, A3);
+    moment_pair_masked<STAGE>(make_float2(rb.x, rb.y), __ffma2_rn(m2, nsc2, c2), qmax, A0, A1, A2, A3);
+    moment_pair_masked<STAGE>(make_float2(rb.z, rb.w), __ffma2_rn(m2, nsc2, c3), qmax, A0, A1, A2, A3);
+  }
+  M.T0 += A0.x + A0.y;
+  M.T1 += A1.x + A1.y;
+  M.T2 += A2.x + A2.y;
+  M.T3 += A3.x + A3.y;
+}
+
 template <int STAGE, int DIR>
 __global__ void __launch_bounds__(256)
 adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
@@ -112,7 +161,8 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
                Acq acq, const float* __restrict__ res, float res_sign, int det_per_chunk,
                double* __restrict__ gpart, int64_t n_pad, unsigned long long* __restrict__ ops_total,
                int* __restrict__ status) {
-  __shared__ __align__(16) float seg_all[8][2][kSeg];
+  __shared__ __align__(16) float seg_all[8][2][kSeg + kPad + 4];
+  const bool vec16 = (acq.n_out & 3) == 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
   if (g >= n_groups) return;
@@ -151,13 +201,25 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       nearl = group_near(acq, gdl, gm) ? 1 : 0;
       if (DIR != kDirNone) ddl = load_detdir(det_aux, jl);
     }
+    // stage res[j][lo8 .. hi] (lo8 = lo rounded down to 8) + kPad zeros
     auto stage_seg = [&](int jj, int buf) {
-      const int lo = __shfl_sync(0xffffffffu, rlo, jj) & ~1;
+      const int lo = __shfl_sync(0xffffffffu, rlo, jj) & ~7;
       const int hi = __shfl_sync(0xffffffffu, rhi, jj);
       if (lo <= hi && hi - lo + 1 <= kSeg) {
         const float* src = res + (size_t)(jb + jj) * n_out + lo;
         float* dst = seg_all[warp][buf];
-        for (int k = lane; k <= hi - lo; k += kWarp) cp_async4(dst + k, src + k);
+        const int len = hi - lo + 1;
+        const int len4 = (len + 3) >> 2;
+        if (vec16 && lo + 4 * len4 <= n_out) {   // 16-byte copies: 16B-aligned rows, lo a multiple of 8
+          for (int k = lane; k < len4; k += kWarp) cp_async16(dst + 4 * k, src + 4 * k);
+          // zero padding from the next 16-byte boundary (the partial vector
+          // above copied up to 3 extra finite residual samples: harmless)
+          float4* z = reinterpret_cast<float4*>(dst + 4 * len4);
+          if (lane < kPad / 4) z[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+          for (int k = lane; k < len; k += kWarp) cp_async4(dst + k, src + k);
+          for (int k = lane; k < kPad; k += kWarp) dst[len + k] = 0.0f;
+        }
       }
       cp_async_commit();
     };
@@ -165,7 +227,7 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
     stage_seg(0, 0);
     for (int jj = 0; jj < nd; ++jj) {
       const int buf = jj & 1;
-      const int lo = __shfl_sync(0xffffffffu, rlo, jj) & ~1;   // even staging base
+      const int lo = __shfl_sync(0xffffffffu, rlo, jj) & ~7;   // 8-aligned staging base
       const int hi = __shfl_sync(0xffffffffu, rhi, jj);
       const int near = __shfl_sync(0xffffffffu, nearl, jj);
       const GroupDet gd = shfl_gd(gdl, jj);
@@ -192,21 +254,31 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       my_ops += (unsigned long long)(max(jhi - jlo + 1, 0) + max(nhi - nlo + 1, 0));
 
       Moments M = {0.f, 0.f, 0.f, 0.f};
-      // separate call sites for the shared (staged) and global (wide) sources
-      // so the compiler emits LDS, not generic loads, on the hot path
-      auto walk = [&](const float* seg, int sbase) {
-        moments_run<STAGE>(seg, jlo - sbase, jhi - jlo + 1, (float)(jlo * f - pg.kc), fs, sc, pg.phi * sc, M);
+      // uniform masked walk over the staged segment when the warp's blocks fit
+      // in staged + padding; otherwise (wide/near-field cases) a per-lane walk
+      // over the global residual row
+      const bool empty = jlo > jhi;
+      const int J0 = empty ? lo : (jlo & ~7);
+      const int nb = empty ? 0 : ((jhi - J0) >> 3) + 1;
+      const int nblk = __reduce_max_sync(0xffffffffu, nb);
+      const int reach = __reduce_max_sync(0xffffffffu, J0 - lo + 8 * nblk);
+      const bool any_near = __any_sync(0xffffffffu, nlo <= nhi);
+      if (!any_near && hi - lo + 1 <= kSeg && reach <= hi - lo + 1 + kPad) {
+        const float rs = rho * sc;
+        moments_uniform<STAGE>(seg_all[warp][buf], J0 - lo, nblk, (float)(J0 * f - pg.kc), fs, sc, pg.phi * sc,
+                               empty ? -1.0f : rs * rs, M);
+      } else {
+        const float* row = res + (size_t)(jb + jj) * n_out;
+        moments_run<STAGE>(row, jlo, jhi - jlo + 1, (float)(jlo * f - pg.kc), fs, sc, pg.phi * sc, M);
         if (nlo <= nhi) {   // u+ = -kappa y: odd moments flip sign
           Moments N = {0.f, 0.f, 0.f, 0.f};
-          moments_run<STAGE>(seg, nlo - sbase, nhi - nlo + 1, (float)(nlo * f - nkc), fs, sc, nphi * sc, N);
+          moments_run<STAGE>(row, nlo, nhi - nlo + 1, (float)(nlo * f - nkc), fs, sc, nphi * sc, N);
           M.T0 += N.T0;
           M.T1 -= N.T1;
           M.T2 += N.T2;
           M.T3 -= N.T3;
         }
-      };
-      if (hi - lo + 1 <= kSeg) walk(seg_all[warp][buf], lo);
-      else walk(res + (size_t)(jb + jj) * n_out, 0);
+      }
       __syncwarp();
 
       // per-pair gradient terms (reference radiator.py:275-286 in y units)

@@ -119,6 +119,98 @@ __device__ __forceinline__ void flush_rows(float* tile, int lane, int a, int b, 
   __syncwarp();
 }
 
+// Warp-uniform masked window walk.  Every lane walks the same number `nblk`
+// of 8-sample blocks from its own 8-aligned start J0 (tile slots J0 % kTile:
+// kTile is a multiple of 8, so a block never straddles the circular wrap).
+// Samples outside the lane's support (q = y^2 > qmax) get G = 0 and add an
+// exact +-0 to whatever row their slot holds, so the extension past the
+// window is harmless; in exchange there is no divergence and no tail code.
+__device__ __forceinline__ float2 masked_g2(float2 q, float qmax) {
+  return make_float2(q.x <= qmax ? ex2(-q.x) : 0.0f, q.y <= qmax ? ex2(-q.y) : 0.0f);
+}
+
+__device__ __forceinline__ void rmw_uniform(float* tile, int lane, int J0, int nblk, float mf, float fs, float sc,
+                                            float ps, float Ak, float qmax) {
+  const float2 nsc2 = make_float2(-sc, -sc);
+  const float2 Ak2 = make_float2(Ak, Ak);
+  const float2 c0 = make_float2(ps, fmaf(fs, -sc, ps));
+  const float2 c1 = make_float2(fmaf(2.0f * fs, -sc, ps), fmaf(3.0f * fs, -sc, ps));
+  const float2 c2 = make_float2(fmaf(4.0f * fs, -sc, ps), fmaf(5.0f * fs, -sc, ps));
+  const float2 c3 = make_float2(fmaf(6.0f * fs, -sc, ps), fmaf(7.0f * fs, -sc, ps));
+  int s = J0 % kTile;
+#pragma unroll 1
+  for (int b = 0; b < nblk; ++b) {
+    float* t = tile + s * kWarp + lane;
+    const float2 m2 = make_float2(mf, mf);
+    const float2 o0 = make_float2(t[0], t[kWarp]);
+    const float2 o1 = make_float2(t[2 * kWarp], t[3 * kWarp]);
+    const float2 o2 = make_float2(t[4 * kWarp], t[5 * kWarp]);
+    const float2 o3 = make_float2(t[6 * kWarp], t[7 * kWarp]);
+    const float2 y0 = __ffma2_rn(m2, nsc2, c0), y1 = __ffma2_rn(m2, nsc2, c1);
+    const float2 y2 = __ffma2_rn(m2, nsc2, c2), y3 = __ffma2_rn(m2, nsc2, c3);
+    const float2 g0 = masked_g2(__fmul2_rn(y0, y0), qmax), g1 = masked_g2(__fmul2_rn(y1, y1), qmax);
+    const float2 g2 = masked_g2(__fmul2_rn(y2, y2), qmax), g3 = masked_g2(__fmul2_rn(y3, y3), qmax);
+    const float2 n0 = __ffma2_rn(Ak2, __fmul2_rn(y0, g0), o0);
+    const float2 n1 = __ffma2_rn(Ak2, __fmul2_rn(y1, g1), o1);
+    const float2 n2 = __ffma2_rn(Ak2, __fmul2_rn(y2, g2), o2);
+    const float2 n3 = __ffma2_rn(Ak2, __fmul2_rn(y3, g3), o3);
+    t[0] = n0.x; t[kWarp] = n0.y; t[2 * kWarp] = n1.x; t[3 * kWarp] = n1.y;
+    t[4 * kWarp] = n2.x; t[5 * kWarp] = n2.y; t[6 * kWarp] = n3.x; t[7 * kWarp] = n3.y;
+    mf += 8.0f * fs;
+    s += 8;
+    if (s == kTile) s = 0;
+  }
+}
+
+// One ball (lane) of one group against the CTA's detector in the time sweep:
+// setup, then the warp-uniform masked walk of the u- window (and, if any lane
+// has one, of the u+ near-field window).  `fp` is a live tile row used as the
+// start of empty windows.
+template <int DIR>
+__device__ __forceinline__ void evaluate_pair_uniform(float* tile, int lane, const Acq& acq, const GroupDet& gd,
+                                                      const GroupMeta& gm, const Detector& det, const DetDir& dd,
+                                                      const BallA& A, const BallB& B, int near,
+                                                      unsigned long long& ops, int& coinc, int fp) {
+  const PairGeom pg = pair_geom(gd, gm, det.px, det.py, det.pz, A, B, acq);
+  coinc |= pg.coincident;
+  const float rho = acq.cutoff * A.a0 * acq.inv_vdt_f;
+  const float sc = acq.vdt_f * kSqrtHalfLog2e * B.inv_a0;
+  const float rs = rho * sc;
+  const float qmax = rs * rs;
+  int jlo, jhi;
+  pair_window(pg.kc, pg.phi, rho, acq, &jlo, &jhi);
+  const bool live = B.orig >= 0;
+  if (!live) { jlo = 1; jhi = 0; }
+  int nlo = 1, nhi = 0, nkc = 0;
+  float nphi = 0.0f;
+  if (near && live) pair_near_window(pg.d, rho, acq, &nlo, &nhi, &nkc, &nphi);
+  ops += (unsigned long long)(max(jhi - jlo + 1, 0) + max(nhi - nlo + 1, 0));
+  float D = 1.0f;
+  if (DIR != kDirNone)
+    D = dir_weight<DIR, false>(dd, pg.rx * pg.id, pg.ry * pg.id, pg.rz * pg.id, pg.id, acq.dir_param,
+                               acq.dir_param, B.inv_a0, nullptr, nullptr);
+  // u G amp = Ak * y G with Ak = amp * kappa = (p0 D / 2d) a0 sqrt(2 ln 2)
+  const float Ak = (0.5f * B.p0 * D) * pg.id * (A.a0 * kSqrt2Ln2);
+  const float fs = (float)acq.f;
+  {
+    const bool empty = jlo > jhi;
+    const int J0 = (empty ? fp : jlo) & ~7;
+    const int nb = empty ? 0 : ((jhi - J0) >> 3) + 1;
+    const int nblk = __reduce_max_sync(0xffffffffu, nb);
+    if (nblk > 0)
+      rmw_uniform(tile, lane, J0, nblk, (float)(J0 * acq.f - pg.kc), fs, sc, pg.phi * sc, empty ? 0.0f : Ak,
+                  empty ? -1.0f : qmax);
+  }
+  if (__any_sync(0xffffffffu, nlo <= nhi)) {   // u+ = -kappa y: walk with -sc
+    const bool empty = nlo > nhi;
+    const int J0 = (empty ? fp : nlo) & ~7;
+    const int nb = empty ? 0 : ((nhi - J0) >> 3) + 1;
+    const int nblk = __reduce_max_sync(0xffffffffu, nb);
+    rmw_uniform(tile, lane, J0, nblk, (float)(J0 * acq.f - nkc), fs, -sc, nphi * -sc, empty ? 0.0f : Ak,
+                empty ? -1.0f : qmax);
+  }
+}
+
 // One ball (lane) of one group against the CTA's detector: setup, then the
 // u- (and, near field, u+) window clipped to [clip_lo, clip_hi] into the tile.
 template <int DIR>
@@ -309,7 +401,7 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
           touched = max(touched, ghi);
           GroupMeta gm;
           if (gd.slow) gm = gmeta[g];
-          evaluate_pair<DIR>(tile, lane, acq, gd, gm, det, dd, A, B, near, my_ops, coinc, INT_MIN, INT_MAX);
+          evaluate_pair_uniform<DIR>(tile, lane, acq, gd, gm, det, dd, A, B, near, my_ops, coinc, fp);
           __syncwarp();
         }
       }

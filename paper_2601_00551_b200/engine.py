@@ -29,7 +29,7 @@ FORWARD_WARPS = 4   # 2 CTAs per SM: one CTA sorts while the other sweeps
 FORWARD_TILE_ROWS = 128
 ADJOINT_WARPS = 8
 GROUP = 32
-A0_BUCKETS = 4   # lane groups hold balls of similar radius (equal window lengths)
+A0_BUCKETS = 8   # lane groups hold balls of similar radius (equal window lengths)
 GROUP_META_BYTES = 48
 
 

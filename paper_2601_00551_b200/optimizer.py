@@ -438,8 +438,11 @@ def density_control(state: OptimState, thresholds: DensityThresholds, stage: str
     if nS:
         unit = up(rng.unit_vectors(nS))
         cpos, cp0, ca0 = f64(2 * nS * 3), f64(2 * nS), f64(2 * nS)
-        call("pab_split_children", ptr(_gather(pos, 3, S)), ptr(_gather(p0, 1, S)), ptr(_gather(a0, 1, S)),
-             ptr(unit), nS, ptr(cpos), ptr(cp0), ptr(ca0), E._stream())
+        # bind gathered operands to names: a temporary freed right after ptr()
+        # would be recycled by the caching allocator before the kernel runs
+        s_pos, s_p0, s_a0 = _gather(pos, 3, S), _gather(p0, 1, S), _gather(a0, 1, S)
+        call("pab_split_children", ptr(s_pos), ptr(s_p0), ptr(s_a0), ptr(unit), nS, ptr(cpos), ptr(cp0),
+             ptr(ca0), E._stream())
         sfree = _gather(free, 1, S)
         parts_pos.append(cpos.view(2 * nS, 3))
         parts_p0.append(cp0)
@@ -464,8 +467,9 @@ def density_control(state: OptimState, thresholds: DensityThresholds, stage: str
             unit = up(rng.unit_vectors(order.numel()))
             k = order.numel()
             dpos, dp0, da0 = f64(3 * k), f64(k), f64(k)
-            call("pab_duplicate", ptr(_gather(par_pos, 3, order)), ptr(_gather(par_p0, 1, order)),
-                 ptr(_gather(par_a0, 1, order)), ptr(unit), k, ptr(dpos), ptr(dp0), ptr(da0), E._stream())
+            o_pos, o_p0, o_a0 = _gather(par_pos, 3, order), _gather(par_p0, 1, order), _gather(par_a0, 1, order)
+            call("pab_duplicate", ptr(o_pos), ptr(o_p0), ptr(o_a0), ptr(unit), k, ptr(dpos), ptr(dp0), ptr(da0),
+                 E._stream())
             parts_pos.append(dpos.view(k, 3))
             parts_p0.append(dp0)
             parts_a0.append(da0)
