@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpaball_b200.so")
+# PAB_LIBRARY selects another build of the same library (tuning experiments)
+LIB_PATH = os.environ.get("PAB_LIBRARY") or os.path.join(_HERE, "libpaball_b200.so")
 
 _vp, _i, _i64, _d, _f = C.c_void_p, C.c_int, C.c_int64, C.c_double, C.c_float
 _SIGS = {

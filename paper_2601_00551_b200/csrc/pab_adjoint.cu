@@ -109,15 +109,21 @@ __device__ __forceinline__ void moments_run(const float* seg, int off, int n, fl
   M.T3 += A3.x + A3.y;
 }
 
-// Warp-uniform masked walk over the staged segment: every lane runs `nblk`
-// 8-sample blocks from its own 8-aligned start J0 (16-byte aligned LDS.128);
-// samples outside the lane's support (q > qmax) get G = 0 and contribute an
-// exact 0 (the staged residual is finite and zero-padded).
-template <int STAGE>
+// Warp-uniform walk over the staged segment: every lane runs the same number
+// of samples L (a multiple of 4) from its own 4-aligned start J0 (16-byte
+// aligned LDS.128); the staged residual is finite and zero-padded.
+//   MASK   samples outside the lane's support (q > qmax) get G = 0: exact
+//          truncation at cutoff sigmas;
+//   !MASK  samples walked past a window's ends lie beyond cutoff sigmas
+//          (G <= exp(-cutoff^2/2) < 2^-24 for cutoff >= kUnmaskedCutoff):
+//          their terms are below FP32 resolution; lanes with an empty window
+//          discard their moments.
+template <int STAGE, bool MASK>
 __device__ __forceinline__ void moment_pair_masked(float2 res, float2 y, float qmax, float2& A0, float2& A1,
                                                    float2& A2, float2& A3) {
   const float2 q = __fmul2_rn(y, y);
-  const float2 G = make_float2(q.x <= qmax ? ex2(-q.x) : 0.0f, q.y <= qmax ? ex2(-q.y) : 0.0f);
+  const float2 G = MASK ? make_float2(q.x <= qmax ? ex2(-q.x) : 0.0f, q.y <= qmax ? ex2(-q.y) : 0.0f)
+                        : make_float2(ex2(-q.x), ex2(-q.y));
   const float2 r = __fmul2_rn(res, G);
   const float2 t = __fmul2_rn(r, y);
   A1 = __fadd2_rn(A1, t);
@@ -128,33 +134,64 @@ __device__ __forceinline__ void moment_pair_masked(float2 res, float2 y, float q
   }
 }
 
-template <int STAGE>
-__device__ __forceinline__ void moments_uniform(const float* seg, int off, int nblk, float mf, float fs, float sc,
-                                                float ps, float qmax, Moments& M) {
-  const float4* s4 = reinterpret_cast<const float4*>(seg + off);
-  float2 A0 = make_float2(0.f, 0.f), A1 = A0, A2 = A0, A3 = A0;
-  const float2 nsc2 = make_float2(-sc, -sc);
-  const float2 c0 = make_float2(ps, fmaf(fs, -sc, ps));
-  const float2 c1 = make_float2(fmaf(2.0f * fs, -sc, ps), fmaf(3.0f * fs, -sc, ps));
-  const float2 c2 = make_float2(fmaf(4.0f * fs, -sc, ps), fmaf(5.0f * fs, -sc, ps));
-  const float2 c3 = make_float2(fmaf(6.0f * fs, -sc, ps), fmaf(7.0f * fs, -sc, ps));
-#pragma unroll 1
-  for (int b = 0; b < nblk; ++b, s4 += 2, mf += 8.0f * fs) {
-    const float4 ra = s4[0], rb = s4[1];
-    const float2 m2 = make_float2(mf, mf);
-    moment_pair_masked<STAGE>(make_float2(ra.x, ra.y), __ffma2_rn(m2, nsc2, c0), qmax, A0, A1, A2, A3);
-    moment_pair_masked<STAGE>(make_float2(ra.z, ra.w), __ffma2_rn(m2, nsc2, c1), qmax, A0, A1, A2, A3);
-    moment_pair_masked<STAGE>(make_float2(rb.x, rb.y), __ffma2_rn(m2, nsc2, c2), qmax, A0, A1, A2, A3);
-    moment_pair_masked<STAGE>(make_float2(rb.z, rb.w), __ffma2_rn(m2, nsc2, c3), qmax, A0, A1, A2, A3);
-  }
-  M.T0 += A0.x + A0.y;
-  M.T1 += A1.x + A1.y;
-  M.T2 += A2.x + A2.y;
-  M.T3 += A3.x + A3.y;
+// Per-ball walk constants: y of sample pair k of an 8-sample block starting at
+// m-offset m is  m * (-sc) + ps + kk_k,  kk_k = (2k, 2k+1) * f * (-sc).
+struct WalkConst {
+  float2 nsc2, k0, k1, k2, k3;
+  float step8;   // 8 f (m advance per block)
+};
+
+__device__ __forceinline__ WalkConst walk_const(float sc, int f) {
+  WalkConst w;
+  const float nsc = -sc, fs = (float)f;
+  w.nsc2 = make_float2(nsc, nsc);
+  w.k0 = make_float2(0.0f, fs * nsc);
+  w.k1 = make_float2(2.0f * fs * nsc, 3.0f * fs * nsc);
+  w.k2 = make_float2(4.0f * fs * nsc, 5.0f * fs * nsc);
+  w.k3 = make_float2(6.0f * fs * nsc, 7.0f * fs * nsc);
+  w.step8 = 8.0f * fs;
+  return w;
 }
 
-template <int STAGE, int DIR>
-__global__ void __launch_bounds__(256)
+template <int STAGE, bool MASK>
+__device__ __forceinline__ void moments_uniform(const float* seg, int L, float mf, const WalkConst& W, float ps,
+                                                float qmax, Moments& M) {
+  const float4* s4 = reinterpret_cast<const float4*>(seg);
+  float2 A0 = make_float2(0.f, 0.f), A1 = A0, A2 = A0, A3 = A0;
+  const float2 p2 = make_float2(ps, ps);
+  const float2 c0 = __fadd2_rn(W.k0, p2), c1 = __fadd2_rn(W.k1, p2);
+  const float2 c2 = __fadd2_rn(W.k2, p2), c3 = __fadd2_rn(W.k3, p2);
+#pragma unroll 1
+  for (int nb = L >> 3; nb > 0; --nb, s4 += 2, mf += W.step8) {
+    const float4 ra = s4[0], rb = s4[1];
+    const float2 m2 = make_float2(mf, mf);
+    moment_pair_masked<STAGE, MASK>(make_float2(ra.x, ra.y), __ffma2_rn(m2, W.nsc2, c0), qmax, A0, A1, A2, A3);
+    moment_pair_masked<STAGE, MASK>(make_float2(ra.z, ra.w), __ffma2_rn(m2, W.nsc2, c1), qmax, A0, A1, A2, A3);
+    moment_pair_masked<STAGE, MASK>(make_float2(rb.x, rb.y), __ffma2_rn(m2, W.nsc2, c2), qmax, A0, A1, A2, A3);
+    moment_pair_masked<STAGE, MASK>(make_float2(rb.z, rb.w), __ffma2_rn(m2, W.nsc2, c3), qmax, A0, A1, A2, A3);
+  }
+  if (L & 4) {   // 4-sample tail block
+    const float4 ra = s4[0];
+    const float2 m2 = make_float2(mf, mf);
+    moment_pair_masked<STAGE, MASK>(make_float2(ra.x, ra.y), __ffma2_rn(m2, W.nsc2, c0), qmax, A0, A1, A2, A3);
+    moment_pair_masked<STAGE, MASK>(make_float2(ra.z, ra.w), __ffma2_rn(m2, W.nsc2, c1), qmax, A0, A1, A2, A3);
+  }
+  M.T0 = A0.x + A0.y;
+  M.T1 = A1.x + A1.y;
+  M.T2 = A2.x + A2.y;
+  M.T3 = A3.x + A3.y;
+}
+
+// flags of a (lane group, detector) pair, computed by the batch lane
+constexpr int kFlagUniform = 1;   // staged uniform walk (far field, fits the segment)
+constexpr int kFlagNear = 2;      // a u+ window may exist
+constexpr int kFlagSlow = 4;      // detector within two group radii: FP64 per-pair geometry
+
+#ifndef PAB_ADJ_MINB
+#define PAB_ADJ_MINB 2
+#endif
+template <int STAGE, int DIR, bool MASK>
+__global__ void __launch_bounds__(256, PAB_ADJ_MINB)
 adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
                const GroupMeta* __restrict__ gmeta, int64_t n_groups,
                const double* __restrict__ det_pos, const double* __restrict__ det_aux, int n_det,
@@ -180,9 +217,14 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   // per-ball constants (detector independent)
   const float sc = acq.vdt_f * kSqrtHalfLog2e * B.inv_a0;
   const float rho = acq.cutoff * A.a0 * acq.inv_vdt_f;
-  const float kap = A.a0 * kSqrt2Ln2;
-  const float p0h = 0.5f * B.p0;
   const bool live = B.orig >= 0;
+  const float qmax = live ? (rho * sc) * (rho * sc) : -1.0f;
+  const WalkConst W = walk_const(sc, f);
+  const float kap_rs = A.a0 * kSqrt2Ln2 * res_sign;   // kappa * sign
+  const float p0h = 0.5f * B.p0;
+  // the uniform walk must stay inside the staged samples + zero padding
+  // (cover window <= 2 rho / f + 3 samples, + 3 alignment + 3 rounding)
+  const bool fits = 2.0f * (acq.cutoff * gm.a0max * acq.inv_vdt_f) * acq.inv_f + 12.0f <= (float)kPad;
   double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
   unsigned long long my_ops = 0;
   int coinc = 0;
@@ -191,26 +233,30 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
     const int nd = min(kWarp, j1 - jb);
     GroupDet gdl = empty_gd();
     DetDir ddl{};
-    int rlo = 0, rhi = -1, nearl = 0;
+    int rlo = 0, rhi = -1, rfl = 0;
     double pxl = 0.0, pyl = 0.0, pzl = 0.0;
     if (lane < nd) {
       const int jl = jb + lane;
       pxl = det_pos[3 * jl]; pyl = det_pos[3 * jl + 1]; pzl = det_pos[3 * jl + 2];
       gdl = group_det(gm, pxl, pyl, pzl, acq);
       group_range(acq, gdl, gm, &rlo, &rhi);
-      nearl = group_near(acq, gdl, gm) ? 1 : 0;
+      rlo &= ~3;   // 16-byte aligned staging base
+      const bool nr = group_near(acq, gdl, gm);
+      rfl = (nr ? kFlagNear : 0) | (gdl.slow ? kFlagSlow : 0) |
+            (!nr && fits && rlo <= rhi && rhi - rlo + 1 <= kSeg ? kFlagUniform : 0);
       if (DIR != kDirNone) ddl = load_detdir(det_aux, jl);
     }
-    // stage res[j][lo8 .. hi] (lo8 = lo rounded down to 8) + kPad zeros
+    // stage res[j][lo .. hi] (lo a multiple of 4) + kPad zeros
     auto stage_seg = [&](int jj, int buf) {
-      const int lo = __shfl_sync(0xffffffffu, rlo, jj) & ~7;
+      const int lo = __shfl_sync(0xffffffffu, rlo, jj);
       const int hi = __shfl_sync(0xffffffffu, rhi, jj);
-      if (lo <= hi && hi - lo + 1 <= kSeg) {
+      const int fl = __shfl_sync(0xffffffffu, rfl, jj);
+      if (fl & kFlagUniform) {
         const float* src = res + (size_t)(jb + jj) * n_out + lo;
         float* dst = seg_all[warp][buf];
         const int len = hi - lo + 1;
         const int len4 = (len + 3) >> 2;
-        if (vec16 && lo + 4 * len4 <= n_out) {   // 16-byte copies: 16B-aligned rows, lo a multiple of 8
+        if (vec16 && lo + 4 * len4 <= n_out) {   // 16-byte copies (16B-aligned rows and base)
           for (int k = lane; k < len4; k += kWarp) cp_async16(dst + 4 * k, src + 4 * k);
           // zero padding from the next 16-byte boundary (the partial vector
           // above copied up to 3 extra finite residual samples: harmless)
@@ -227,47 +273,53 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
     stage_seg(0, 0);
     for (int jj = 0; jj < nd; ++jj) {
       const int buf = jj & 1;
-      const int lo = __shfl_sync(0xffffffffu, rlo, jj) & ~7;   // 8-aligned staging base
+      const int lo = __shfl_sync(0xffffffffu, rlo, jj);
       const int hi = __shfl_sync(0xffffffffu, rhi, jj);
-      const int near = __shfl_sync(0xffffffffu, nearl, jj);
-      const GroupDet gd = shfl_gd(gdl, jj);
+      const int fl = __shfl_sync(0xffffffffu, rfl, jj);
+      GroupDet gd = shfl_gd_fast(gdl, jj);
       const DetDir dd = shfl_detdir<DIR>(ddl, jj);
-      double px = 0.0, py = 0.0, pz = 0.0;
-      if (gd.slow) {
-        px = __shfl_sync(0xffffffffu, pxl, jj);
-        py = __shfl_sync(0xffffffffu, pyl, jj);
-        pz = __shfl_sync(0xffffffffu, pzl, jj);
-      }
       cp_async_wait_all();
       __syncwarp();
       if (jj + 1 < nd) stage_seg(jj + 1, buf ^ 1);
       if (lo > hi) continue;
 
-      const PairGeom pg = pair_geom(gd, gm, px, py, pz, A, B, acq);
-      coinc |= pg.coincident;
-      int jlo, jhi;
-      pair_window(pg.kc, pg.phi, rho, acq, &jlo, &jhi);
-      if (!live) { jlo = 1; jhi = 0; }
-      int nlo = 1, nhi = 0, nkc = 0;
-      float nphi = 0.0f;
-      if (near && live) pair_near_window(pg.d, rho, acq, &nlo, &nhi, &nkc, &nphi);
-      my_ops += (unsigned long long)(max(jhi - jlo + 1, 0) + max(nhi - nlo + 1, 0));
-
-      Moments M = {0.f, 0.f, 0.f, 0.f};
-      // uniform masked walk over the staged segment when the warp's blocks fit
-      // in staged + padding; otherwise (wide/near-field cases) a per-lane walk
-      // over the global residual row
-      const bool empty = jlo > jhi;
-      const int J0 = empty ? lo : (jlo & ~7);
-      const int nb = empty ? 0 : ((jhi - J0) >> 3) + 1;
-      const int nblk = __reduce_max_sync(0xffffffffu, nb);
-      const int reach = __reduce_max_sync(0xffffffffu, J0 - lo + 8 * nblk);
-      const bool any_near = __any_sync(0xffffffffu, nlo <= nhi);
-      if (!any_near && hi - lo + 1 <= kSeg && reach <= hi - lo + 1 + kPad) {
-        const float rs = rho * sc;
-        moments_uniform<STAGE>(seg_all[warp][buf], J0 - lo, nblk, (float)(J0 * f - pg.kc), fs, sc, pg.phi * sc,
-                               empty ? -1.0f : rs * rs, M);
+      Moments M;
+      PairGeom pg;
+      if (fl & kFlagUniform) {
+        pg = pair_geom_fast(gd, A, B, acq);
+        int jlo, jhi;
+        pair_window_cover(pg.kc, pg.phi, rho, acq, &jlo, &jhi);
+        const bool empty = !live || jlo > jhi;
+        const int J0 = empty ? lo : max(jlo & ~3, lo);
+        const int Lmax = __reduce_max_sync(0xffffffffu, empty ? 0 : jhi - J0 + 1);
+        if (ops_total && live) {   // exact sample count for the op counter
+          int elo, ehi;
+          pair_window(pg.kc, pg.phi, rho, acq, &elo, &ehi);
+          my_ops += (unsigned long long)max(ehi - elo + 1, 0);
+        }
+        moments_uniform<STAGE, MASK>(seg_all[warp][buf] + (J0 - lo), (Lmax + 3) & ~3, (float)(J0 * f - pg.kc),
+                                     W, pg.phi * sc, empty ? -1.0f : qmax, M);
+        if (!MASK && empty) M = {0.f, 0.f, 0.f, 0.f};
       } else {
+        // near field / detector close to the group / wide windows: per-lane
+        // walks over the global residual row, FP64 geometry when slow
+        gd.slow = (fl & kFlagSlow) ? 1 : 0;
+        double px = 0.0, py = 0.0, pz = 0.0;
+        if (gd.slow) {
+          px = __shfl_sync(0xffffffffu, pxl, jj);
+          py = __shfl_sync(0xffffffffu, pyl, jj);
+          pz = __shfl_sync(0xffffffffu, pzl, jj);
+        }
+        pg = pair_geom(gd, gm, px, py, pz, A, B, acq);
+        coinc |= pg.coincident;
+        int jlo, jhi;
+        pair_window(pg.kc, pg.phi, rho, acq, &jlo, &jhi);
+        if (!live) { jlo = 1; jhi = 0; }
+        int nlo = 1, nhi = 0, nkc = 0;
+        float nphi = 0.0f;
+        if ((fl & kFlagNear) && live) pair_near_window(pg.d, rho, acq, &nlo, &nhi, &nkc, &nphi);
+        my_ops += (unsigned long long)(max(jhi - jlo + 1, 0) + max(nhi - nlo + 1, 0));
+        M = {0.f, 0.f, 0.f, 0.f};
         const float* row = res + (size_t)(jb + jj) * n_out;
         moments_run<STAGE>(row, jlo, jhi - jlo + 1, (float)(jlo * f - pg.kc), fs, sc, pg.phi * sc, M);
         if (nlo <= nhi) {   // u+ = -kappa y: odd moments flip sign
@@ -283,21 +335,19 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
 
       // per-pair gradient terms (reference radiator.py:275-286 in y units)
       float dDdr[3] = {0.f, 0.f, 0.f}, dDda0 = 0.f;
-      const float hx = pg.rx * pg.id, hy = pg.ry * pg.id, hz = pg.rz * pg.id;
+      const float id = pg.id;
       const float D = dir_weight<DIR, STAGE == kStageFine || DIR == kDirElement>(
-          dd, hx, hy, hz, pg.id, acq.dir_param, acq.dir_param, B.inv_a0, dDdr, &dDda0);
-      const float base = p0h * pg.id;   // p0 / 2d
-      const float amp = base * D;
-      const float s_uG = kap * (res_sign * M.T1);
-      gb[0] = fmaf(D * s_uG, 0.5f * pg.id, gb[0]);
+          dd, pg.rx * id, pg.ry * id, pg.rz * id, id, acq.dir_param, acq.dir_param, B.inv_a0, dDdr, &dDda0);
+      const float base = p0h * id;   // p0 / 2d
+      const float s_uG = kap_rs * M.T1;
+      gb[0] = fmaf(D * s_uG, 0.5f * id, gb[0]);
       if (STAGE >= kStageCoarse) {
-        float ga = amp * kSqrt2Ln2Cubed * (res_sign * M.T3);
+        float ga = (base * D) * (kSqrt2Ln2Cubed * res_sign) * M.T3;
         if (DIR == kDirElement) ga = fmaf(base * dDda0, s_uG, ga);
         gb[1] += ga;
       }
       if (STAGE == kStageFine) {
-        const float gdist = amp * res_sign * (M.T0 - kTwoLn2 * M.T2) - (amp * pg.id) * s_uG;
-        const float w = gdist * pg.id;
+        const float w = (base * D) * fmaf(res_sign, fmaf(-kTwoLn2, M.T2, M.T0), -id * s_uG) * id;
         float gx = w * pg.rx, gy = w * pg.ry, gz = w * pg.rz;
         if (DIR != kDirNone) {
           const float bs = base * s_uG;
@@ -361,8 +411,13 @@ static void launch_adjoint(dim3 grid, int threads, cudaStream_t s, const BallA* 
                            const GroupMeta* G, int64_t n_groups, const double* det_pos, const double* det_aux,
                            int n_det, const Acq& a, const float* res, float res_sign, int per_chunk, double* gpart,
                            int64_t n_pad, unsigned long long* ops, int* status) {
-  adjoint_kernel<STAGE, DIR><<<grid, threads, 0, s>>>(A, B, G, n_groups, det_pos, det_aux, n_det, a, res, res_sign,
-                                                       per_chunk, gpart, n_pad, ops, status);
+  // per-sample truncation test only where the walk's overrun could matter
+  if (a.cutoff < kUnmaskedCutoff)
+    adjoint_kernel<STAGE, DIR, true><<<grid, threads, 0, s>>>(A, B, G, n_groups, det_pos, det_aux, n_det, a, res,
+                                                               res_sign, per_chunk, gpart, n_pad, ops, status);
+  else
+    adjoint_kernel<STAGE, DIR, false><<<grid, threads, 0, s>>>(A, B, G, n_groups, det_pos, det_aux, n_det, a, res,
+                                                                res_sign, per_chunk, gpart, n_pad, ops, status);
 }
 
 template <int STAGE>

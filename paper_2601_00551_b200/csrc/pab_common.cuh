@@ -24,6 +24,11 @@ constexpr float kSqrt2Ln2 = 1.17741002251547469f;        // sqrt(2 ln 2) = kappa
 constexpr float kTwoLn2 = 1.38629436111989061f;          // kappa^2 / a0^2
 constexpr float kSqrt2Ln2Cubed = 1.63221961130884960f;   // (kappa / a0)^3
 
+// Cutoffs (in sigmas) at or above which the window walks skip the per-sample
+// truncation test: the few samples walked past a window's ends then carry
+// G <= exp(-cutoff^2 / 2) < 2^-24, below FP32 resolution (see the walks).
+constexpr float kUnmaskedCutoff = 5.8f;
+
 // status bits written by kernels (host raises the reference error classes)
 constexpr int kStatusCoincident = 2;   // SimulationError (radiator.py:190-193)
 constexpr int kStatusNonFinite = 8;    // OptimizationError (optimizer.py:284-294)
@@ -118,6 +123,20 @@ __device__ __forceinline__ GroupDet shfl_gd(const GroupDet& g, int src) {
   return r;
 }
 
+// Broadcast without the slow flag (callers carry it in their own flag word).
+__device__ __forceinline__ GroupDet shfl_gd_fast(const GroupDet& g, int src) {
+  GroupDet r;
+  r.Sx = __shfl_sync(0xffffffffu, g.Sx, src);
+  r.Sy = __shfl_sync(0xffffffffu, g.Sy, src);
+  r.Sz = __shfl_sync(0xffffffffu, g.Sz, src);
+  r.Sn = __shfl_sync(0xffffffffu, g.Sn, src);
+  r.isn = __shfl_sync(0xffffffffu, g.isn, src);
+  r.phg = __shfl_sync(0xffffffffu, g.phg, src);
+  r.kg = __shfl_sync(0xffffffffu, g.kg, src);
+  r.slow = 0;
+  return r;
+}
+
 __device__ __forceinline__ int floor_div(int a, int b) {
   int q = a / b;
   return (a % b != 0 && ((a < 0) != (b < 0))) ? q - 1 : q;
@@ -138,6 +157,19 @@ __device__ __forceinline__ int ceil_div_f(int a, int f, float inv_f) { return -f
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// MUFU reciprocal / reciprocal square root without the denormal-range
+// rescaling rsqrtf/__fdividef emit (operands here are normal numbers; the
+// results are identical to theirs for normal inputs)
+__device__ __forceinline__ float rcp_ftz(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 
@@ -390,6 +422,34 @@ __device__ __forceinline__ PairGeom pair_geom(const GroupDet& gd, const GroupMet
   g.phi = tr - kr;
   g.id = __fdividef(1.0f, g.d);
   return g;
+}
+
+// Fast path only (caller knows the detector is far from the group).
+__device__ __forceinline__ PairGeom pair_geom_fast(const GroupDet& gd, const BallA& A, const BallB& B,
+                                                   const Acq& a) {
+  PairGeom g;
+  g.coincident = 0;
+  const float sd = gd.Sx * A.dx + gd.Sy * A.dy + gd.Sz * A.dz;
+  const float num = B.r2 - 2.0f * sd;
+  const float e1 = fmaf(num * gd.isn, gd.isn, 1.0f);
+  const float dd = (num * gd.isn) * rcp_ftz(1.0f + e1 * rsqrt_ftz(e1));
+  g.d = gd.Sn + dd;
+  const float tr = fmaf(dd, a.inv_vdt_f, gd.phg);
+  g.rx = A.dx - gd.Sx; g.ry = A.dy - gd.Sy; g.rz = A.dz - gd.Sz;
+  const float kr = rintf(tr);
+  g.kc = gd.kg + (int)kr;
+  g.phi = tr - kr;
+  g.id = rcp_ftz(g.d);
+  return g;
+}
+
+// Cover of the u- window for masked walks: jlo' <= jlo and jhi' >= jhi, each
+// off by at most one (float quotient, no exact integer correction); the
+// caller's per-sample mask |x| <= rho selects the exact support.
+__device__ __forceinline__ void pair_window_cover(int kc, float phi, float rho, const Acq& a, int* jlo, int* jhi) {
+  const float kf = (float)kc;
+  *jlo = max(__float2int_rd((kf + (phi - rho)) * a.inv_f), 0);
+  *jhi = min(__float2int_ru((kf + (phi + rho)) * a.inv_f), a.n_out - 1);
 }
 
 // u- window on the decimated grid, clipped to [0, n_out).

@@ -4,7 +4,8 @@
 // scatter) and :263-264 (residual, loss part).
 //
 // Decomposition.  One CTA owns one detector row (all samples of the
-// decimated grid, in shared memory) and a partition of the lane groups (32
+// decimated grid; its partial row in global memory, L2-resident) and a
+// partition of the lane groups (32
 // balls of similar radius, spatially compact).  Groups are processed in
 // chunks; per chunk the CTA
 //   A  computes every group's sample range for this detector (FP64 geometry),
@@ -13,7 +14,7 @@
 //   C  gives each warp a contiguous slice of the sorted list.  A warp walks
 //      its slice in time order; lane l evaluates ball l of each group over
 //      its own arrival window and read-modify-writes its private column of a
-//      circular per-warp tile [UT rows x 32 lanes] (lane l -> bank l: no
+//      circular per-warp tile [kTile rows x 32 lanes] (lane l -> bank l: no
 //      conflicts, no atomics).  Rows the sweep has passed are reduced across
 //      lanes (rotated, conflict-free) and added to the CTA row: each sample is
 //      reduced once per warp instead of once per group,
@@ -27,10 +28,21 @@
 
 namespace pab {
 
-constexpr int kBinShift = 2;           // 4 decimated samples per sort bin
-constexpr int kChunk = 2048;           // lane groups per sort chunk
+constexpr int kBinShift = 3;           // 8 decimated samples per sort bin (bin starts 8-aligned)
+#ifndef PAB_FWD_CHUNK
+#define PAB_FWD_CHUNK 1536
+#endif
+#ifndef PAB_FWD_TILE
+#define PAB_FWD_TILE 160
+#endif
+#ifndef PAB_FWD_MAXWARPS
+#define PAB_FWD_MAXWARPS 4
+#endif
+constexpr int kChunk = PAB_FWD_CHUNK;  // lane groups per sort chunk
 constexpr unsigned short kEmptyBin = 0xFFFF;
-constexpr int kTile = 160;             // tile rows per warp (circular, slot = J % kTile)
+constexpr int kTile = PAB_FWD_TILE;    // tile rows per warp (circular, slot = J % kTile, multiple of 8)
+constexpr int kMaxWarps = PAB_FWD_MAXWARPS;
+constexpr int kTileAlloc = kTile + 8;  // + one 8-row dump block per warp
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
@@ -119,60 +131,118 @@ __device__ __forceinline__ void flush_rows(float* tile, int lane, int a, int b, 
   __syncwarp();
 }
 
-// Warp-uniform masked window walk.  Every lane walks the same number `nblk`
-// of 8-sample blocks from its own 8-aligned start J0 (tile slots J0 % kTile:
-// kTile is a multiple of 8, so a block never straddles the circular wrap).
-// Samples outside the lane's support (q = y^2 > qmax) get G = 0 and add an
-// exact +-0 to whatever row their slot holds, so the extension past the
-// window is harmless; in exchange there is no divergence and no tail code.
-__device__ __forceinline__ float2 masked_g2(float2 q, float qmax) {
-  return make_float2(q.x <= qmax ? ex2(-q.x) : 0.0f, q.y <= qmax ? ex2(-q.y) : 0.0f);
+// Warp-uniform window walk.  Every lane walks the same number L (a multiple
+// of 4) of samples from its own 8-aligned start J0 (tile slots J0 % kTile:
+// kTile is a multiple of 8, so an 8-sample block never straddles the circular
+// wrap).  Blocks that start past the lane's last sample `lim` are redirected
+// to a per-warp dump block, so a lane writes at most 7 rows beyond its window
+// (the bin criterion keeps those rows inside the live tile).  Inside the
+// walked range:
+//   MASK   samples with q = y^2 > qmax get G = 0 (exact truncation at
+//          cutoff sigmas, any cutoff);
+//   !MASK  no per-sample test: the <= 7 samples walked past either end of a
+//          window lie beyond cutoff sigmas, where G <= exp(-cutoff^2/2) <=
+//          2^-24 (cutoff >= 5.77, host-checked), below the FP32 resolution
+//          of the ball's own contribution.
+// Two blocks per iteration (16 independent read-modify-writes in flight).
+template <bool MASK>
+__device__ __forceinline__ float2 gauss2(float2 q, float qmax) {
+  if (MASK) return make_float2(q.x <= qmax ? ex2(-q.x) : 0.0f, q.y <= qmax ? ex2(-q.y) : 0.0f);
+  return make_float2(ex2(-q.x), ex2(-q.y));
 }
 
-__device__ __forceinline__ void rmw_uniform(float* tile, int lane, int J0, int nblk, float mf, float fs, float sc,
-                                            float ps, float Ak, float qmax) {
-  const float2 nsc2 = make_float2(-sc, -sc);
-  const float2 Ak2 = make_float2(Ak, Ak);
-  const float2 c0 = make_float2(ps, fmaf(fs, -sc, ps));
-  const float2 c1 = make_float2(fmaf(2.0f * fs, -sc, ps), fmaf(3.0f * fs, -sc, ps));
-  const float2 c2 = make_float2(fmaf(4.0f * fs, -sc, ps), fmaf(5.0f * fs, -sc, ps));
-  const float2 c3 = make_float2(fmaf(6.0f * fs, -sc, ps), fmaf(7.0f * fs, -sc, ps));
+struct Walk {
+  float2 nsc2, c0, c1, c2, c3, Ak2;
+  float qmax;
+};
+
+template <bool MASK>
+__device__ __forceinline__ float2 rmw_pair(float2 o, float2 m2, float2 c, const Walk& w) {
+  const float2 y = __ffma2_rn(m2, w.nsc2, c);
+  const float2 g = gauss2<MASK>(__fmul2_rn(y, y), w.qmax);
+  return __ffma2_rn(w.Ak2, __fmul2_rn(y, g), o);
+}
+
+template <bool MASK>
+__device__ __forceinline__ void rmw_block8(float* t, float mf, const Walk& w) {
+  const float2 m2 = make_float2(mf, mf);
+  const float2 o0 = make_float2(t[0], t[kWarp]);
+  const float2 o1 = make_float2(t[2 * kWarp], t[3 * kWarp]);
+  const float2 o2 = make_float2(t[4 * kWarp], t[5 * kWarp]);
+  const float2 o3 = make_float2(t[6 * kWarp], t[7 * kWarp]);
+  const float2 n0 = rmw_pair<MASK>(o0, m2, w.c0, w), n1 = rmw_pair<MASK>(o1, m2, w.c1, w);
+  const float2 n2 = rmw_pair<MASK>(o2, m2, w.c2, w), n3 = rmw_pair<MASK>(o3, m2, w.c3, w);
+  t[0] = n0.x; t[kWarp] = n0.y; t[2 * kWarp] = n1.x; t[3 * kWarp] = n1.y;
+  t[4 * kWarp] = n2.x; t[5 * kWarp] = n2.y; t[6 * kWarp] = n3.x; t[7 * kWarp] = n3.y;
+}
+
+template <bool MASK>
+__device__ __forceinline__ void rmw_uniform(float* tile, int lane, int J0, int L, int lim, float mf, float fs,
+                                            float sc, float ps, float Ak, float qmax) {
+  Walk w;
+  w.nsc2 = make_float2(-sc, -sc);
+  w.Ak2 = make_float2(Ak, Ak);
+  w.c0 = make_float2(ps, fmaf(fs, -sc, ps));
+  w.c1 = make_float2(fmaf(2.0f * fs, -sc, ps), fmaf(3.0f * fs, -sc, ps));
+  w.c2 = make_float2(fmaf(4.0f * fs, -sc, ps), fmaf(5.0f * fs, -sc, ps));
+  w.c3 = make_float2(fmaf(6.0f * fs, -sc, ps), fmaf(7.0f * fs, -sc, ps));
+  w.qmax = qmax;
+  float* const dump = tile + kTile * kWarp + lane;
+  const float step = 8.0f * fs;
   int s = J0 % kTile;
+  int Jb = J0;   // row of the current block's first sample
+  int nb = L >> 3;
 #pragma unroll 1
-  for (int b = 0; b < nblk; ++b) {
-    float* t = tile + s * kWarp + lane;
-    const float2 m2 = make_float2(mf, mf);
-    const float2 o0 = make_float2(t[0], t[kWarp]);
-    const float2 o1 = make_float2(t[2 * kWarp], t[3 * kWarp]);
-    const float2 o2 = make_float2(t[4 * kWarp], t[5 * kWarp]);
-    const float2 o3 = make_float2(t[6 * kWarp], t[7 * kWarp]);
-    const float2 y0 = __ffma2_rn(m2, nsc2, c0), y1 = __ffma2_rn(m2, nsc2, c1);
-    const float2 y2 = __ffma2_rn(m2, nsc2, c2), y3 = __ffma2_rn(m2, nsc2, c3);
-    const float2 g0 = masked_g2(__fmul2_rn(y0, y0), qmax), g1 = masked_g2(__fmul2_rn(y1, y1), qmax);
-    const float2 g2 = masked_g2(__fmul2_rn(y2, y2), qmax), g3 = masked_g2(__fmul2_rn(y3, y3), qmax);
-    const float2 n0 = __ffma2_rn(Ak2, __fmul2_rn(y0, g0), o0);
-    const float2 n1 = __ffma2_rn(Ak2, __fmul2_rn(y1, g1), o1);
-    const float2 n2 = __ffma2_rn(Ak2, __fmul2_rn(y2, g2), o2);
-    const float2 n3 = __ffma2_rn(Ak2, __fmul2_rn(y3, g3), o3);
-    t[0] = n0.x; t[kWarp] = n0.y; t[2 * kWarp] = n1.x; t[3 * kWarp] = n1.y;
-    t[4 * kWarp] = n2.x; t[5 * kWarp] = n2.y; t[6 * kWarp] = n3.x; t[7 * kWarp] = n3.y;
-    mf += 8.0f * fs;
+  for (; nb >= 2; nb -= 2) {
+    float* ta = Jb <= lim ? tile + s * kWarp + lane : dump;
     s += 8;
     if (s == kTile) s = 0;
+    float* tb = Jb + 8 <= lim ? tile + s * kWarp + lane : dump;
+    s += 8;
+    if (s == kTile) s = 0;
+    Jb += 16;
+    // both blocks' reads before either block's writes
+    const float2 ma = make_float2(mf, mf), mb = make_float2(mf + step, mf + step);
+    const float2 a0 = make_float2(ta[0], ta[kWarp]), a1 = make_float2(ta[2 * kWarp], ta[3 * kWarp]);
+    const float2 a2 = make_float2(ta[4 * kWarp], ta[5 * kWarp]), a3 = make_float2(ta[6 * kWarp], ta[7 * kWarp]);
+    const float2 b0 = make_float2(tb[0], tb[kWarp]), b1 = make_float2(tb[2 * kWarp], tb[3 * kWarp]);
+    const float2 b2 = make_float2(tb[4 * kWarp], tb[5 * kWarp]), b3 = make_float2(tb[6 * kWarp], tb[7 * kWarp]);
+    const float2 na0 = rmw_pair<MASK>(a0, ma, w.c0, w), nb0 = rmw_pair<MASK>(b0, mb, w.c0, w);
+    const float2 na1 = rmw_pair<MASK>(a1, ma, w.c1, w), nb1 = rmw_pair<MASK>(b1, mb, w.c1, w);
+    const float2 na2 = rmw_pair<MASK>(a2, ma, w.c2, w), nb2 = rmw_pair<MASK>(b2, mb, w.c2, w);
+    const float2 na3 = rmw_pair<MASK>(a3, ma, w.c3, w), nb3 = rmw_pair<MASK>(b3, mb, w.c3, w);
+    ta[0] = na0.x; ta[kWarp] = na0.y; ta[2 * kWarp] = na1.x; ta[3 * kWarp] = na1.y;
+    ta[4 * kWarp] = na2.x; ta[5 * kWarp] = na2.y; ta[6 * kWarp] = na3.x; ta[7 * kWarp] = na3.y;
+    tb[0] = nb0.x; tb[kWarp] = nb0.y; tb[2 * kWarp] = nb1.x; tb[3 * kWarp] = nb1.y;
+    tb[4 * kWarp] = nb2.x; tb[5 * kWarp] = nb2.y; tb[6 * kWarp] = nb3.x; tb[7 * kWarp] = nb3.y;
+    mf += 2.0f * step;
+  }
+  if (nb) {
+    rmw_block8<MASK>(Jb <= lim ? tile + s * kWarp + lane : dump, mf, w);
+    mf += step;
+    s += 8;
+    if (s == kTile) s = 0;
+    Jb += 8;
+  }
+  if (L & 4) {   // 4-sample tail (8-aligned start: no wrap inside)
+    float* t = Jb <= lim ? tile + s * kWarp + lane : dump;
+    const float2 m2 = make_float2(mf, mf);
+    const float2 o0 = make_float2(t[0], t[kWarp]), o1 = make_float2(t[2 * kWarp], t[3 * kWarp]);
+    const float2 n0 = rmw_pair<MASK>(o0, m2, w.c0, w), n1 = rmw_pair<MASK>(o1, m2, w.c1, w);
+    t[0] = n0.x; t[kWarp] = n0.y; t[2 * kWarp] = n1.x; t[3 * kWarp] = n1.y;
   }
 }
 
 // One ball (lane) of one group against the CTA's detector in the time sweep:
-// setup, then the warp-uniform masked walk of the u- window (and, if any lane
-// has one, of the u+ near-field window).  `fp` is a live tile row used as the
-// start of empty windows.
-template <int DIR>
+// setup, then the warp-uniform walk of the u- window (and, if any lane has
+// one, of the u+ near-field window).  `fp` is the first live tile row (the
+// start of empty windows, which are redirected to the dump block).  Groups
+// whose detector is close (slow geometry) take the linear-pass path instead.
+template <int DIR, bool MASK>
 __device__ __forceinline__ void evaluate_pair_uniform(float* tile, int lane, const Acq& acq, const GroupDet& gd,
-                                                      const GroupMeta& gm, const Detector& det, const DetDir& dd,
-                                                      const BallA& A, const BallB& B, int near,
-                                                      unsigned long long& ops, int& coinc, int fp) {
-  const PairGeom pg = pair_geom(gd, gm, det.px, det.py, det.pz, A, B, acq);
-  coinc |= pg.coincident;
+                                                      const DetDir& dd, const BallA& A, const BallB& B, int near,
+                                                      unsigned long long& ops, int fp) {
+  const PairGeom pg = pair_geom_fast(gd, A, B, acq);
   const float rho = acq.cutoff * A.a0 * acq.inv_vdt_f;
   const float sc = acq.vdt_f * kSqrtHalfLog2e * B.inv_a0;
   const float rs = rho * sc;
@@ -181,10 +251,7 @@ __device__ __forceinline__ void evaluate_pair_uniform(float* tile, int lane, con
   pair_window(pg.kc, pg.phi, rho, acq, &jlo, &jhi);
   const bool live = B.orig >= 0;
   if (!live) { jlo = 1; jhi = 0; }
-  int nlo = 1, nhi = 0, nkc = 0;
-  float nphi = 0.0f;
-  if (near && live) pair_near_window(pg.d, rho, acq, &nlo, &nhi, &nkc, &nphi);
-  ops += (unsigned long long)(max(jhi - jlo + 1, 0) + max(nhi - nlo + 1, 0));
+  ops += (unsigned long long)max(jhi - jlo + 1, 0);
   float D = 1.0f;
   if (DIR != kDirNone)
     D = dir_weight<DIR, false>(dd, pg.rx * pg.id, pg.ry * pg.id, pg.rz * pg.id, pg.id, acq.dir_param,
@@ -195,19 +262,23 @@ __device__ __forceinline__ void evaluate_pair_uniform(float* tile, int lane, con
   {
     const bool empty = jlo > jhi;
     const int J0 = (empty ? fp : jlo) & ~7;
-    const int nb = empty ? 0 : ((jhi - J0) >> 3) + 1;
-    const int nblk = __reduce_max_sync(0xffffffffu, nb);
-    if (nblk > 0)
-      rmw_uniform(tile, lane, J0, nblk, (float)(J0 * acq.f - pg.kc), fs, sc, pg.phi * sc, empty ? 0.0f : Ak,
-                  empty ? -1.0f : qmax);
+    const int L = __reduce_max_sync(0xffffffffu, empty ? 0 : jhi - J0 + 1);
+    if (L > 0)
+      rmw_uniform<MASK>(tile, lane, J0, (L + 3) & ~3, empty ? -1 : jhi, (float)(J0 * acq.f - pg.kc), fs, sc,
+                        pg.phi * sc, empty ? 0.0f : Ak, qmax);
   }
-  if (__any_sync(0xffffffffu, nlo <= nhi)) {   // u+ = -kappa y: walk with -sc
-    const bool empty = nlo > nhi;
-    const int J0 = (empty ? fp : nlo) & ~7;
-    const int nb = empty ? 0 : ((nhi - J0) >> 3) + 1;
-    const int nblk = __reduce_max_sync(0xffffffffu, nb);
-    rmw_uniform(tile, lane, J0, nblk, (float)(J0 * acq.f - nkc), fs, -sc, nphi * -sc, empty ? 0.0f : Ak,
-                empty ? -1.0f : qmax);
+  if (near) {
+    int nlo = 1, nhi = 0, nkc = 0;
+    float nphi = 0.0f;
+    if (live) pair_near_window(pg.d, rho, acq, &nlo, &nhi, &nkc, &nphi);
+    ops += (unsigned long long)max(nhi - nlo + 1, 0);
+    if (__any_sync(0xffffffffu, nlo <= nhi)) {   // u+ = -kappa y: walk with -sc
+      const bool empty = nlo > nhi;
+      const int J0 = (empty ? fp : nlo) & ~7;
+      const int L = __reduce_max_sync(0xffffffffu, empty ? 0 : nhi - J0 + 1);
+      rmw_uniform<MASK>(tile, lane, J0, (L + 3) & ~3, empty ? -1 : nhi, (float)(J0 * acq.f - nkc), fs, -sc,
+                        nphi * -sc, empty ? 0.0f : Ak, qmax);
+    }
   }
 }
 
@@ -240,8 +311,8 @@ __device__ __forceinline__ void evaluate_pair(float* tile, int lane, const Acq& 
     rmw_window(tile, lane, max(nlo, clip_lo), min(nhi, clip_hi), nkc, acq.f, -sc, nphi, Ak);
 }
 
-template <int DIR>
-__global__ void __launch_bounds__(128, 2)
+template <int DIR, bool MASK>
+__global__ void __launch_bounds__(kMaxWarps * 32, 2)
 forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
                const GroupMeta* __restrict__ gmeta, int64_t n_groups,
                const double* __restrict__ det_pos, const double* __restrict__ det_aux, int n_det,
@@ -250,11 +321,14 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int W = blockDim.x >> 5;
   const int n_out = acq.n_out;
-  const int row_pad = (n_out + 3) & ~3;
   const int n_bins = (n_out + (1 << kBinShift) - 1) >> kBinShift;
+#ifdef PAB_FWD_GLOBAL_ROW
+  float* tiles = reinterpret_cast<float*>(smem_raw);
+#else
   float* row = reinterpret_cast<float*>(smem_raw);
-  float* tiles = row + row_pad;
-  float* stage = tiles + (size_t)W * kTile * kWarp;
+  float* tiles = row + ((n_out + 3) & ~3);
+#endif
+  float* stage = tiles + (size_t)W * kTileAlloc * kWarp;
   int* hist = reinterpret_cast<int*>(stage + W * kTile);        // [n_bins + 1]
   int* zs = hist + (n_bins + 1);                                // [W + 1]
   int* misc = zs + W + 1;                                       // [4]
@@ -265,16 +339,20 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   const int part = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tid = threadIdx.x, nthr = blockDim.x;
-  const int f = acq.f;
 
-  for (int i = tid; i < row_pad; i += nthr) row[i] = 0.0f;
-  for (int i = tid; i < W * kTile * kWarp; i += nthr) tiles[i] = 0.0f;
+  // the CTA's output row lives in global memory (L2): written only by this
+  // CTA, each sample by one warp at a time, in a fixed order
+#ifdef PAB_FWD_GLOBAL_ROW
+  float* row = partial_rows + ((size_t)part * n_det + j) * (size_t)n_out;
+#endif
+  for (int i = tid; i < n_out; i += nthr) row[i] = 0.0f;
+  for (int i = tid; i < W * kTileAlloc * kWarp; i += nthr) tiles[i] = 0.0f;
   for (int i = tid; i < W * kTile; i += nthr) stage[i] = 0.0f;
 
   const Detector det = load_detector(det_pos, det_aux, j);
   DetDir dd{};
   if (DIR != kDirNone) dd = load_detdir(det_aux, j);
-  float* tile = tiles + (size_t)warp * kTile * kWarp;
+  float* tile = tiles + (size_t)warp * kTileAlloc * kWarp;
   const int64_t g_begin = (int64_t)part * groups_per_part;
   const int64_t g_end = min(n_groups, g_begin + groups_per_part);
   unsigned long long my_ops = 0;
@@ -294,7 +372,11 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       unsigned short bin = kEmptyBin;
       if (lo <= hi) {
         const int blo = lo & ~((1 << kBinShift) - 1);
-        bin = (hi - blo + 1 > kTile) ? (unsigned short)n_bins : (unsigned short)(lo >> kBinShift);
+        // a lane writes rows [blo, hi + 7] (8-aligned starts, last block may
+        // run 7 rows past the window): the span must fit the live tile
+        // wide groups and groups close to the detector (FP64 per-pair
+        // geometry) take the linear-pass path (phase F)
+        bin = (hi + 7 - blo + 1 > kTile || gd.slow) ? (unsigned short)n_bins : (unsigned short)(lo >> kBinShift);
         atomicAdd(&hist[bin], 1);   // counts only: order-independent
       }
       gbin[gl] = bin;
@@ -382,8 +464,7 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
         BallA An = ra[g_next * kWarp + lane];
         BallB Bn = rb[g_next * kWarp + lane];
         for (int k = 0; k < nb; ++k) {
-          const GroupDet gd = shfl_gd(gd_l, k);
-          const int64_t g = g_next;
+          const GroupDet gd = shfl_gd_fast(gd_l, k);
           const BallA A = An;
           const BallB B = Bn;
           if (k + 1 < nb) {
@@ -398,14 +479,16 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
             flush_rows(tile, lane, fp, min(min(blo, fp + kTile), touched + 1), sink);
             fp = blo;
           }
-          touched = max(touched, ghi);
-          GroupMeta gm;
-          if (gd.slow) gm = gmeta[g];
-          evaluate_pair_uniform<DIR>(tile, lane, acq, gd, gm, det, dd, A, B, near, my_ops, coinc, fp);
+          touched = max(touched, ghi + 7);
+          evaluate_pair_uniform<DIR, MASK>(tile, lane, acq, gd, dd, A, B, near, my_ops, fp);
           __syncwarp();
         }
       }
       if (s_begin < s_end) flush_rows(tile, lane, fp, min(min(fp + kTile, n_out), touched + 1), sink);
+      // rows past the signal end (clipped windows' overrun) are never
+      // flushed: clear the tile for the next chunk / the linear passes
+      for (int r = 0; r < kTile; ++r) tile[r * kWarp + lane] = 0.0f;
+      __syncwarp();
     }
     __syncthreads();
 
@@ -443,9 +526,10 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
     __syncthreads();
   }
 
+#ifndef PAB_FWD_GLOBAL_ROW
   float* out = partial_rows + ((size_t)part * n_det + j) * (size_t)n_out;
   for (int i = tid; i < n_out; i += nthr) out[i] = row[i];
-
+#endif
   for (int o = 16; o > 0; o >>= 1) {
     my_ops += __shfl_xor_sync(0xffffffffu, my_ops, o);
     coinc |= __shfl_xor_sync(0xffffffffu, coinc, o);
@@ -496,10 +580,14 @@ __global__ void decimate_kernel(const float* __restrict__ src, int n_rows, int n
 }
 
 size_t forward_smem(int n_out, int warps) {
-  const size_t row_pad = (size_t)((n_out + 3) & ~3);
   const size_t n_bins = (size_t)((n_out + (1 << kBinShift) - 1) >> kBinShift);
-  return row_pad * 4 + (size_t)warps * kTile * kWarp * 4 + (size_t)warps * kTile * 4 +
-         (n_bins + 1) * 4 + (size_t)(warps + 1) * 4 + 16 + 2 * kChunk * 2 + 16;
+#ifdef PAB_FWD_GLOBAL_ROW
+  const size_t row_bytes = 0;
+#else
+  const size_t row_bytes = (size_t)((n_out + 3) & ~3) * 4;
+#endif
+  return row_bytes + (size_t)warps * kTileAlloc * kWarp * 4 + (size_t)warps * kTile * 4 + (n_bins + 1) * 4 +
+         (size_t)(warps + 1) * 4 + 16 + 2 * kChunk * 2 + 16;
 }
 
 }  // namespace pab
@@ -521,7 +609,7 @@ int pab_forward(const void* rec_a, const void* rec_b, const void* group_meta, in
   (void)groups_per_cell;
   (void)tile_rows;
   if (n_det <= 0 || n_out <= 0) return 0;
-  if (f < 1 || partitions < 1 || warps < 1 || warps > 4) return 1;
+  if (f < 1 || partitions < 1 || warps < 1 || warps > kMaxWarps) return 1;
   if (!rec_a || !rec_b || !group_meta || !det_pos || !det_aux || !partial_rows || !ops_total || !status)
     return 1;
   if ((int64_t)n_out * f > (1 << 24)) return 1;
@@ -537,9 +625,12 @@ int pab_forward(const void* rec_a, const void* rec_b, const void* group_meta, in
         (const BallA*)rec_a, (const BallB*)rec_b, (const GroupMeta*)group_meta, n_groups, det_pos, det_aux,
         n_det, acq, per_part, partial_rows, ops_total, status);
   };
-  if (dir_kind == kDirNone) launch(forward_kernel<kDirNone>);
-  else if (dir_kind == kDirCosPower) launch(forward_kernel<kDirCosPower>);
-  else launch(forward_kernel<kDirElement>);
+  // per-sample truncation test only where the walk's overrun could matter
+  const bool mask = cutoff < kUnmaskedCutoff;
+  if (dir_kind == kDirNone) mask ? launch(forward_kernel<kDirNone, true>) : launch(forward_kernel<kDirNone, false>);
+  else if (dir_kind == kDirCosPower)
+    mask ? launch(forward_kernel<kDirCosPower, true>) : launch(forward_kernel<kDirCosPower, false>);
+  else mask ? launch(forward_kernel<kDirElement, true>) : launch(forward_kernel<kDirElement, false>);
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 

@@ -11,6 +11,8 @@ iteration are the scalar loss and the per-ball gradient all-reduce (NCCL).
 
 from __future__ import annotations
 
+import os
+
 import math
 from dataclasses import dataclass
 
@@ -25,7 +27,7 @@ from .parallel import Shard, allreduce_scalar, allreduce_sum_, current_shard, ga
 STATUS_COINCIDENT = 2
 STATUS_NONFINITE = 8
 
-FORWARD_WARPS = 4   # 2 CTAs per SM: one CTA sorts while the other sweeps
+FORWARD_WARPS = int(os.environ.get("PAB_FWD_WARPS", "4"))   # 2 CTAs per SM: one sorts while the other sweeps
 FORWARD_TILE_ROWS = 128
 ADJOINT_WARPS = 8
 GROUP = 32
@@ -244,7 +246,7 @@ def plan_forward(cloud: DeviceCloud, det: DeviceDetectors, acq: Acq) -> ForwardP
     tile = FORWARD_TILE_ROWS
     warps = FORWARD_WARPS
     while warps > 1 and _lib.load().pab_forward_smem_bytes(acq.n_out, warps, tile) > 227 * 1024:
-        warps //= 2
+        warps -= 1
     target_ctas = 12 * sm_count(dev)   # >= 6 waves of 2 resident CTAs per SM
     parts = max(1, -(-target_ctas // max(det.n_local, 1)))
     parts = int(max(1, min(parts, cloud.n_groups // (4 * warps))))

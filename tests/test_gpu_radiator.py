@@ -397,3 +397,62 @@ def test_microbench_slice_matches_oracle(P):
     assert rel_l2(gr.d_p0, gp0) < GRAD_TOL
     assert rel_l2(gr.d_a0, ga0) < GRAD_TOL
     assert rel_l2(gr.d_position, gpos) < GRAD_TOL
+
+
+# ----------------------------------------------------------- walk edge cases
+
+@pytest.mark.parametrize("cutoff", [4.0, 5.0, 5.79, 5.8, 7.5])
+def test_cutoff_paths_match_oracle(P, cutoff):
+    """Cutoffs below kUnmaskedCutoff (5.8) run the per-sample truncation
+    test, the rest the unmasked walk: both match the oracle's truncation."""
+    ctx, cloud, truth, _, _ = seeded_instance(P)
+    cctx = P.ForwardContext(ctx.array, ctx.grid, cutoff_sigma=cutoff)
+    rows, _, _, ops = OR.run_model(truth.positions, truth.p0, truth.a0, ctx.array.positions, None,
+                                   1500.0, 0.0, 5e-8, 256, 1, cutoff=cutoff)
+    P.reset_op_count()
+    assert rel_l2(P.simulate_signals(truth, cctx).data, rows) < SIG_TOL
+    assert abs(P.op_count() - ops) <= 2
+    _, L, (gp0, ga0, gpos), _ = OR.run_model(cloud.positions, cloud.p0, cloud.a0, ctx.array.positions, None,
+                                             1500.0, 0.0, 5e-8, 256, 1, cutoff=cutoff, real=rows, stage="fine")
+    Lg, gr = P.backward(cloud, cctx, P.SignalSet(ctx.grid, rows), stage="fine")
+    assert abs(Lg - L) <= 1e-4 * L
+    assert rel_l2(gr.d_p0, gp0) < GRAD_TOL
+    assert rel_l2(gr.d_a0, ga0) < GRAD_TOL
+    assert rel_l2(gr.d_position, gpos) < GRAD_TOL
+
+
+@pytest.mark.parametrize("f", [1, 3])
+def test_windows_clipped_at_both_recording_ends(P, f):
+    """A dense cloud whose arrivals straddle the first and the last sample
+    (t0 > 0, short record): clipped windows, groups wider than the live
+    tile near the end, every sample of the record written by many groups."""
+    rng = np.random.default_rng(11)
+    n = 6000
+    sens = np.array([[0.0, 0.0, 0.0], [0.002, 0.0, 0.001], [-0.001, 0.002, 0.0]])
+    # distances 10..16 mm: arrival samples ~ 6.7..10.7 us at 1500 m/s
+    r = rng.uniform(0.010, 0.016, n)
+    u = rng.normal(size=(n, 3))
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    u[:, 2] = np.abs(u[:, 2])
+    pos = u * r[:, None]
+    p0 = rng.uniform(0.2, 1.0, n)
+    a0 = rng.uniform(0.05e-3, 0.2e-3, n)
+    grid = P.TimeGrid(8.0e-6, 2.5e-8, 96)   # records 8.0 .. 10.4 us only
+    ctx = P.ForwardContext(P.SensorArray(sens, 1500.0), grid)
+    cloud = P.PointCloud(pos, p0, a0)
+    rows, _, _, ops = OR.run_model(pos, p0, a0, sens, None, 1500.0, grid.t0, grid.dt, grid.n_samples, f)
+    P.reset_op_count()
+    got = P.simulate_at_rate(cloud, ctx, f).data
+    assert got.shape == rows.shape
+    assert rel_l2(got, rows) < SIG_TOL
+    assert abs(P.op_count() - ops) <= 2
+    real = rows * 0.9 + 0.01 * np.abs(rows).max()
+    cand = P.PointCloud(pos + rng.normal(scale=2e-5, size=pos.shape), p0 * 1.1, a0 * 0.97)
+    _, L, (gp0, ga0, gpos), _ = OR.run_model(cand.positions, cand.p0, cand.a0, sens, None, 1500.0, grid.t0,
+                                             grid.dt, grid.n_samples, f, real=real, stage="fine")
+    sup = P.SignalSet(grid.decimated(f), real)
+    Lg, gr = P.backward(cand, ctx, sup, stage="fine")
+    assert abs(Lg - L) <= 1e-4 * L
+    assert rel_l2(gr.d_p0, gp0) < GRAD_TOL
+    assert rel_l2(gr.d_a0, ga0) < GRAD_TOL
+    assert rel_l2(gr.d_position, gpos) < GRAD_TOL
