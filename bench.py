@@ -230,8 +230,10 @@ def main():
 
     def one_step(ev=None):
         c = E.PassCounters(dev)
+        cloud.invalidate()   # parameters change every iteration: repack (the optimizer's per-step cost)
         if ev:
             ev[0].record(stream)
+        cloud.pack()
         res, loss_rows = E.forward_rows(cloud, det, acq, c, real_local=real_local, out=res_buf)
         if ev:
             ev[1].record(stream)
@@ -245,7 +247,7 @@ def main():
     torch.cuda.synchronize()
     ops_per_step = c.read()
 
-    # kernel-level events: forward+residual, adjoint+finalize(+allreduce)
+    # kernel-level events: pack+forward+residual, adjoint+finalize(+allreduce)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     sampler = ClockSampler(local)
     if world > 1:

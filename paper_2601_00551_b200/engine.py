@@ -289,9 +289,12 @@ class PassCounters:
 
 
 def forward_rows(cloud: DeviceCloud, det: DeviceDetectors, acq: Acq, counters: PassCounters,
-                 real_local: torch.Tensor | None = None, out: torch.Tensor | None = None):
+                 real_local: torch.Tensor | None = None, out: torch.Tensor | None = None,
+                 real_ready: torch.cuda.Event | None = None):
     """Simulate this rank's rows.  With ``real_local`` the result is the
-    residual sim - real and the per-row FP64 sum of squares is returned.
+    residual sim - real and the per-row FP64 sum of squares is returned
+    (``real_ready``: event the supervision upload records; only the residual
+    epilogue waits for it, the forward kernel overlaps the copy).
     Returns (out [J_local, n_out] f32, loss_rows [J_local] f64 or None)."""
     ws = workspace(cloud.dev)
     n_out = acq.n_out
@@ -311,20 +314,31 @@ def forward_rows(cloud: DeviceCloud, det: DeviceDetectors, acq: Acq, counters: P
              plan.tile_rows, ptr(partial), ptr(counters.ops), ptr(counters.status), _stream())
     else:
         partial.zero_()
+    if real_ready is not None:
+        torch.cuda.current_stream(cloud.dev).wait_event(real_ready)
     call("pab_residual", ptr(partial), plan.partitions, J, n_out, ptr(real_local), ptr(out),
          ptr(loss_rows), _stream())
     return out, loss_rows
 
 
 def adjoint_grads(cloud: DeviceCloud, det: DeviceDetectors, acq: Acq, res: torch.Tensor, res_sign: float,
-                  stage: int, scale: float, counters: PassCounters, count_ops: bool = False):
+                  stage: int, scale: float, counters: PassCounters, count_ops: bool = False,
+                  flat: torch.Tensor | None = None):
     """Per-ball loss gradients in caller order (FP64), reduced over ranks.
-    stage: 0 filter (d_p0 only), 1 coarse, 2 fine."""
+    stage: 0 filter (d_p0 only), 1 coarse, 2 fine.  The three fields are
+    views of one contiguous buffer ``flat`` ([n] for stage 0, [5n] otherwise;
+    allocated when not given): one all-reduce, one host copy."""
     dev = cloud.dev
     n = cloud.n
-    d_p0 = torch.zeros(n, dtype=torch.float64, device=dev)
-    d_a0 = torch.zeros(n, dtype=torch.float64, device=dev) if stage >= 1 else None
-    d_pos = torch.zeros((n, 3), dtype=torch.float64, device=dev) if stage >= 1 else None
+    width = 1 if stage == 0 else 5
+    if flat is None:
+        flat = torch.zeros(width * n, dtype=torch.float64, device=dev)
+    else:
+        flat = flat[: width * n]
+        flat.zero_()
+    d_p0 = flat[:n]
+    d_a0 = flat[n:2 * n] if stage >= 1 else None
+    d_pos = flat[2 * n:].view(n, 3) if stage >= 1 else None
     if n > 0 and det.n_local > 0:
         cloud.pack()
         chunks = plan_adjoint(cloud, det)
@@ -339,10 +353,7 @@ def adjoint_grads(cloud: DeviceCloud, det: DeviceDetectors, acq: Acq, res: torch
         call("pab_grad_finalize", ptr(gpart), chunks, cloud.n_groups, ptr(cloud.rec_b), float(scale), int(stage),
              ptr(d_p0), ptr(d_a0), ptr(d_pos), ptr(counters.status), _stream())
     if det.shard.world > 1:
-        allreduce_sum_(d_p0)
-        if d_a0 is not None:
-            allreduce_sum_(d_a0)
-            allreduce_sum_(d_pos)
+        allreduce_sum_(flat)
     return d_p0, d_a0, d_pos
 
 

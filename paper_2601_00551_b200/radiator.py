@@ -204,17 +204,43 @@ def _fingerprint(a: np.ndarray) -> tuple:
     return (a.ctypes.data, a.shape, a.strides, flat[::step].tobytes())
 
 
-def device_supervision(data: np.ndarray, det: E.DeviceDetectors) -> torch.Tensor:
-    """This rank's supervision rows as FP32 on device (cached per array)."""
+_side_streams: dict = {}
+
+
+def _side_stream(dev) -> torch.cuda.Stream:
+    s = _side_streams.get(dev.index)
+    if s is None:
+        s = _side_streams[dev.index] = torch.cuda.Stream(dev)
+    return s
+
+
+def device_supervision(data: np.ndarray, det: E.DeviceDetectors, defer: bool = False):
+    """This rank's supervision rows as FP32 on device (cached per array).
+
+    The rows travel in their host dtype (no host-side conversion pass) on a
+    side stream and are narrowed on the device.  ``defer=True`` returns
+    (tensor, event or None) without making the current stream wait, so the
+    copy overlaps whatever is enqueued before the caller waits on the event."""
     key = (_fingerprint(data), det.lo, det.hi)
     for k, t in _sup_cache:
         if k == key:
-            return t
-    rows = np.ascontiguousarray(data[det.lo:det.hi], dtype=np.float32)
-    t = torch.from_numpy(rows).to(det.pos.device)
+            return (t, None) if defer else t
+    dev = det.pos.device
+    host = torch.from_numpy(np.ascontiguousarray(data[det.lo:det.hi]))
+    main = torch.cuda.current_stream(dev)
+    side = _side_stream(dev)
+    side.wait_stream(main)
+    with torch.cuda.stream(side):
+        t = host.to(dev, non_blocking=True).to(torch.float32)
+        ev = torch.cuda.Event()
+        ev.record(side)
+    t.record_stream(main)
     _sup_cache.append((key, t))
     if len(_sup_cache) > 4:
         _sup_cache.pop(0)
+    if defer:
+        return t, ev
+    main.wait_event(ev)
     return t
 
 
@@ -248,6 +274,8 @@ def _run_model(cloud, ctx, f, real=None, stage="fine"):
     det = device_detectors(ctx)
     dev = det.pos.device
     acq = _acq(ctx, f)
+    if need_grad:   # supervision upload first: it overlaps the cloud upload, packing and forward kernel
+        real_local, real_ready = device_supervision(real.data, det, defer=True)
     dc = E.DeviceCloud.from_host(cloud.positions, cloud.p0, a0, dev)
     counters = E.PassCounters(dev)
     if not need_grad:
@@ -256,16 +284,22 @@ def _run_model(cloud, ctx, f, real=None, stage="fine"):
         ops = counters.read()
         _add_ops(ops)
         return rows, None, None, ops
-    real_local = device_supervision(real.data, det)
-    res, loss_rows = E.forward_rows(dc, det, acq, counters, real_local=real_local)
+    res, loss_rows = E.forward_rows(dc, det, acq, counters, real_local=real_local, real_ready=real_ready)
     stage_code = 2 if stage == "fine" else 1
     n_total = det.n_total * n_out
-    d_p0, d_a0, d_pos = E.adjoint_grads(dc, det, acq, res, 1.0, stage_code, 2.0 / n_total, counters)
+    flat = torch.empty(5 * n, dtype=torch.float64, device=dev)
+    E.adjoint_grads(dc, det, acq, res, 1.0, stage_code, 2.0 / n_total, counters, flat=flat)
+    # one copy into page-locked host memory; the returned arrays are views
+    # that keep it alive
+    host = torch.empty(5 * n, dtype=torch.float64, pin_memory=True)
+    host.copy_(flat, non_blocking=True)
     loss_sum = E.allreduce_scalar(float(loss_rows.sum().item()), dev) if det.shard.world > 1 \
         else float(loss_rows.sum().item())
     ops = counters.read()
     _add_ops(ops)
-    grads = ParamGradients(d_p0.cpu().numpy(), d_a0.cpu().numpy(), d_pos.cpu().numpy())
+    torch.cuda.current_stream(dev).synchronize()
+    h = host.numpy()
+    grads = ParamGradients(h[:n], h[n:2 * n], h[2 * n:].reshape(n, 3))
     return None, loss_sum / n_total, grads, ops
 
 
