@@ -134,23 +134,36 @@ __device__ __forceinline__ void moment_pair_masked(float2 res, float2 y, float q
   }
 }
 
-// Per-ball walk constants: y of sample pair k of an 8-sample block starting at
-// m-offset m is  m * (-sc) + ps + kk_k,  kk_k = (2k, 2k+1) * f * (-sc).
+// Per-ball walk constants.  Sample s of an 8-sample block starting at
+// m-offset m has y = m * (-sc) + ps + s * dl, dl = f * (-sc); the block's
+// four sample-pair offsets c_k = ps + (2k, 2k+1) dl are built per pair from
+// ps with one FADD and three FADD2 (no per-ball vector constants held).
 struct WalkConst {
-  float2 nsc2, k0, k1, k2, k3;
-  float step8;   // 8 f (m advance per block)
+  float2 nsc2;
+  float dl, dl2;   // f * (-sc), 2 f * (-sc)
+  float step8;     // 8 f (m advance per block)
 };
 
 __device__ __forceinline__ WalkConst walk_const(float sc, int f) {
   WalkConst w;
   const float nsc = -sc, fs = (float)f;
   w.nsc2 = make_float2(nsc, nsc);
-  w.k0 = make_float2(0.0f, fs * nsc);
-  w.k1 = make_float2(2.0f * fs * nsc, 3.0f * fs * nsc);
-  w.k2 = make_float2(4.0f * fs * nsc, 5.0f * fs * nsc);
-  w.k3 = make_float2(6.0f * fs * nsc, 7.0f * fs * nsc);
+  w.dl = fs * nsc;
+  w.dl2 = 2.0f * fs * nsc;
   w.step8 = 8.0f * fs;
   return w;
+}
+
+template <int STAGE, bool MASK>
+__device__ __forceinline__ void moment_block8(const float4* s4, float mf, const WalkConst& W, float2 c0, float2 c1,
+                                              float2 c2, float2 c3, float qmax, float2& A0, float2& A1, float2& A2,
+                                              float2& A3) {
+  const float4 ra = s4[0], rb = s4[1];
+  const float2 m2 = make_float2(mf, mf);
+  moment_pair_masked<STAGE, MASK>(make_float2(ra.x, ra.y), __ffma2_rn(m2, W.nsc2, c0), qmax, A0, A1, A2, A3);
+  moment_pair_masked<STAGE, MASK>(make_float2(ra.z, ra.w), __ffma2_rn(m2, W.nsc2, c1), qmax, A0, A1, A2, A3);
+  moment_pair_masked<STAGE, MASK>(make_float2(rb.x, rb.y), __ffma2_rn(m2, W.nsc2, c2), qmax, A0, A1, A2, A3);
+  moment_pair_masked<STAGE, MASK>(make_float2(rb.z, rb.w), __ffma2_rn(m2, W.nsc2, c3), qmax, A0, A1, A2, A3);
 }
 
 template <int STAGE, bool MASK>
@@ -158,17 +171,20 @@ __device__ __forceinline__ void moments_uniform(const float* seg, int L, float m
                                                 float qmax, Moments& M) {
   const float4* s4 = reinterpret_cast<const float4*>(seg);
   float2 A0 = make_float2(0.f, 0.f), A1 = A0, A2 = A0, A3 = A0;
-  const float2 p2 = make_float2(ps, ps);
-  const float2 c0 = __fadd2_rn(W.k0, p2), c1 = __fadd2_rn(W.k1, p2);
-  const float2 c2 = __fadd2_rn(W.k2, p2), c3 = __fadd2_rn(W.k3, p2);
+  const float2 c0 = make_float2(ps, ps + W.dl);
+  const float2 c1 = __fadd2_rn(c0, make_float2(W.dl2, W.dl2));
+  const float2 c2 = __fadd2_rn(c1, make_float2(W.dl2, W.dl2));
+  const float2 c3 = __fadd2_rn(c2, make_float2(W.dl2, W.dl2));
+  int nb = L >> 3;
 #pragma unroll 1
-  for (int nb = L >> 3; nb > 0; --nb, s4 += 2, mf += W.step8) {
-    const float4 ra = s4[0], rb = s4[1];
-    const float2 m2 = make_float2(mf, mf);
-    moment_pair_masked<STAGE, MASK>(make_float2(ra.x, ra.y), __ffma2_rn(m2, W.nsc2, c0), qmax, A0, A1, A2, A3);
-    moment_pair_masked<STAGE, MASK>(make_float2(ra.z, ra.w), __ffma2_rn(m2, W.nsc2, c1), qmax, A0, A1, A2, A3);
-    moment_pair_masked<STAGE, MASK>(make_float2(rb.x, rb.y), __ffma2_rn(m2, W.nsc2, c2), qmax, A0, A1, A2, A3);
-    moment_pair_masked<STAGE, MASK>(make_float2(rb.z, rb.w), __ffma2_rn(m2, W.nsc2, c3), qmax, A0, A1, A2, A3);
+  for (; nb >= 2; nb -= 2, s4 += 4, mf += 2.0f * W.step8) {   // two blocks per trip
+    moment_block8<STAGE, MASK>(s4, mf, W, c0, c1, c2, c3, qmax, A0, A1, A2, A3);
+    moment_block8<STAGE, MASK>(s4 + 2, mf + W.step8, W, c0, c1, c2, c3, qmax, A0, A1, A2, A3);
+  }
+  if (nb) {
+    moment_block8<STAGE, MASK>(s4, mf, W, c0, c1, c2, c3, qmax, A0, A1, A2, A3);
+    s4 += 2;
+    mf += W.step8;
   }
   if (L & 4) {   // 4-sample tail block
     const float4 ra = s4[0];
@@ -234,11 +250,9 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
     GroupDet gdl = empty_gd();
     DetDir ddl{};
     int rlo = 0, rhi = -1, rfl = 0;
-    double pxl = 0.0, pyl = 0.0, pzl = 0.0;
     if (lane < nd) {
       const int jl = jb + lane;
-      pxl = det_pos[3 * jl]; pyl = det_pos[3 * jl + 1]; pzl = det_pos[3 * jl + 2];
-      gdl = group_det(gm, pxl, pyl, pzl, acq);
+      gdl = group_det(gm, det_pos[3 * jl], det_pos[3 * jl + 1], det_pos[3 * jl + 2], acq);
       group_range(acq, gdl, gm, &rlo, &rhi);
       rlo &= ~3;   // 16-byte aligned staging base
       const bool nr = group_near(acq, gdl, gm);
@@ -306,9 +320,9 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
         gd.slow = (fl & kFlagSlow) ? 1 : 0;
         double px = 0.0, py = 0.0, pz = 0.0;
         if (gd.slow) {
-          px = __shfl_sync(0xffffffffu, pxl, jj);
-          py = __shfl_sync(0xffffffffu, pyl, jj);
-          pz = __shfl_sync(0xffffffffu, pzl, jj);
+          px = det_pos[3 * (jb + jj)];
+          py = det_pos[3 * (jb + jj) + 1];
+          pz = det_pos[3 * (jb + jj) + 2];
         }
         pg = pair_geom(gd, gm, px, py, pz, A, B, acq);
         coinc |= pg.coincident;

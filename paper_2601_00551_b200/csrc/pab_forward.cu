@@ -182,10 +182,11 @@ __device__ __forceinline__ void rmw_uniform(float* tile, int lane, int J0, int L
   Walk w;
   w.nsc2 = make_float2(-sc, -sc);
   w.Ak2 = make_float2(Ak, Ak);
-  w.c0 = make_float2(ps, fmaf(fs, -sc, ps));
-  w.c1 = make_float2(fmaf(2.0f * fs, -sc, ps), fmaf(3.0f * fs, -sc, ps));
-  w.c2 = make_float2(fmaf(4.0f * fs, -sc, ps), fmaf(5.0f * fs, -sc, ps));
-  w.c3 = make_float2(fmaf(6.0f * fs, -sc, ps), fmaf(7.0f * fs, -sc, ps));
+  const float dl = fs * -sc, dl2 = 2.0f * dl;   // y step per sample / per sample pair
+  w.c0 = make_float2(ps, ps + dl);
+  w.c1 = __fadd2_rn(w.c0, make_float2(dl2, dl2));
+  w.c2 = __fadd2_rn(w.c1, make_float2(dl2, dl2));
+  w.c3 = __fadd2_rn(w.c2, make_float2(dl2, dl2));
   w.qmax = qmax;
   float* const dump = tile + kTile * kWarp + lane;
   const float step = 8.0f * fs;
