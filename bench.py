@@ -304,33 +304,44 @@ def main():
             dist.destroy_process_group()
         return
 
-    # roofline of the dominant kernel (FP32 CUDA-core bound)
+    # roofline of the dominant kernel.  Per
+    # in-window sample the forward does 1 ex2 + 1 shared-memory
+    # read-modify-write of its private tile column (8 B) + 7 FP32 flops; the
+    # binding ceiling is the smem RMW rate, measured live by tools/probe
+    # (same access pattern), with the ex2 and FP32 ceilings reported beside.
     probe = os.path.join(ROOT, "tools", "probe", "libfp32_peak.so")
-    peak_flops, peak_ex2, peak_kind = None, None, "measured (tools/probe FFMA2 chains, this GPU)"
+    peak_flops = peak_ex2 = peak_rmw = None
+    peak_kind = "measured live (tools/probe: FFMA2 chains, ex2 chains, private-column smem RMW; this GPU)"
     try:
         lib = ctypes.CDLL(probe)
-        fl, ex = ctypes.c_double(), ctypes.c_double()
+        fl, ex, rm = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
         if lib.probe_fp32_peak(3, ctypes.byref(fl), ctypes.byref(ex)) == 0:
             peak_flops, peak_ex2 = fl.value, ex.value
-    except OSError:
+        if lib.probe_smem_rmw(3, ctypes.byref(rm)) == 0:
+            peak_rmw = rm.value
+    except (OSError, AttributeError):
         pass
-    if peak_flops is None:
-        sms = torch.cuda.get_device_properties(dev).multi_processor_count
-        peak_flops, peak_ex2, peak_kind = sms * 256 * 1.965e9, sms * 16 * 1.965e9, "nominal at 1965 MHz"
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    if peak_flops is None or peak_rmw is None:
+        peak_flops, peak_ex2, peak_rmw = sms * 256 * 1.965e9, sms * 16 * 1.965e9, sms * 14.4 * 1.965e9
+        peak_kind = "nominal at 1965 MHz (FFMA2 256 flop/clk/SM, ex2 16/clk/SM, smem RMW 14.4/clk/SM)"
     fwd_mean = sum(fwd_ms) / len(fwd_ms)
     adj_mean = sum(adj_ms) / len(adj_ms)
     samples = ops_per_step   # in-window samples evaluated by the forward (== adjoint)
-    kern = {"forward": (fwd_mean, FLOPS_FWD * samples), "adjoint_fine": (adj_mean, FLOPS_ADJ_FINE * samples)}
-    dom = max(kern, key=lambda k: kern[k][0])
-    ach = kern[dom][1] / (kern[dom][0] * 1e-3)
-    path_flops = (FLOPS_FWD + FLOPS_ADJ_FINE) * samples / (ms_max * 1e-3)
-    roofline = {"bound": "fp32", "achieved": ach / 1e12, "peak": peak_flops / 1e12, "unit": "TFLOP/s",
-                "frac": ach / peak_flops, "traffic": None, "kernel": dom, "peak_source": peak_kind,
-                "algorithmic": f"{FLOPS_FWD if dom == 'forward' else FLOPS_ADJ_FINE} FP32 flops x "
-                               f"{samples} in-window samples per launch",
-                "path_fwd_adj": {"achieved": path_flops / 1e12, "frac": path_flops / peak_flops,
-                                 "ex2_per_s": 2 * samples / (ms_max * 1e-3), "ex2_peak": peak_ex2,
-                                 "ex2_frac": 2 * samples / (ms_max * 1e-3) / peak_ex2},
+    fwd_s, adj_s = fwd_mean * 1e-3, adj_mean * 1e-3
+    ach = 8.0 * samples / fwd_s
+    roofline = {"bound": "smem", "achieved": ach / 1e9, "peak": 8.0 * peak_rmw / 1e9, "unit": "GB/s",
+                "frac": ach / (8.0 * peak_rmw), "traffic": None, "kernel": "forward_kernel",
+                "peak_source": peak_kind,
+                "algorithmic": f"8 B shared-memory read-modify-write x {samples} in-window samples per launch "
+                               "(forward+residual events; pack and residual are < 0.3% of it)",
+                "other_bounds": {
+                    "forward_ex2": {"frac": samples / fwd_s / peak_ex2, "peak_per_s": peak_ex2},
+                    "forward_fp32": {"frac": FLOPS_FWD * samples / fwd_s / peak_flops,
+                                     "peak_tflops": peak_flops / 1e12},
+                    "adjoint_ex2 (its binding ceiling)": {"frac": samples / adj_s / peak_ex2},
+                    "adjoint_fp32": {"frac": FLOPS_ADJ_FINE * samples / adj_s / peak_flops},
+                    "path_ex2 (fwd+adj, 2 ex2 per sample)": {"frac": 2 * samples / (ms_max * 1e-3) / peak_ex2}},
                 "kernel_ms": {"forward+residual": fwd_mean, "adjoint+finalize": adj_mean}}
 
     cpu = None

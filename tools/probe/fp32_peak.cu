@@ -36,9 +36,61 @@ __global__ void ex2_chains(float* out, float a) {
   for (int i = 0; i < 8; ++i) s += x[i];
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
+// Private-column shared-memory read-modify-write, the forward tile's access
+// pattern (lane l owns bank l of a [rows][32] float tile; LDS + FADD + STS).
+__global__ void smem_rmw(float* out, float a) {
+  constexpr int kRows = 64;
+  __shared__ float tile[4][kRows * 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* t = tile[warp] + lane;
+  for (int r = 0; r < kRows; ++r) t[r * 32] = 0.0f;
+  __syncwarp();
+  for (int it = 0; it < kIters / 64; ++it) {
+#pragma unroll 1
+    for (int r0 = 0; r0 < kRows; r0 += 16) {
+      float v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = t[(r0 + i) * 32];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) t[(r0 + i) * 32] = v[i] + a;
+    }
+  }
+  float s = 0.f;
+  for (int r = 0; r < kRows; ++r) s += t[r * 32];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
 }  // namespace
 
 extern "C" {
+// Returns 0 and fills *rmw (lane read-modify-writes per second).
+int probe_smem_rmw(int reps, double* rmw) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int blocks = sms * 6, threads = 128;
+  float* out = nullptr;
+  if (cudaMalloc(&out, sizeof(float) * blocks * threads) != cudaSuccess) return 4;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  double best = 0.0;
+  for (int r = 0; r < reps; ++r) {
+    float ms = 0.f;
+    cudaEventRecord(e0);
+    smem_rmw<<<blocks, threads>>>(out, 1e-3f);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double v = (double)(kIters / 64) * 64.0 * (double)blocks * threads / (ms * 1e-3);
+    best = v > best ? v : best;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  *rmw = best;
+  return cudaGetLastError() == cudaSuccess ? 0 : 4;
+}
+
 // Returns 0 and fills *flops (FP32 FLOP/s, FMA = 2) and *ex2 (ex2/s).
 int probe_fp32_peak(int reps, double* flops, double* ex2) {
   int dev = 0, sms = 0;
