@@ -18,7 +18,8 @@
  *      2  ball coincident with a detector   -> SimulationError (radiator.py:190-193)
  *      8  non-finite gradient               -> OptimizationError (optimizer.py:284-294)
  *  - Ball clouds are packed once per change by pab_pack into processing order
- *    (lane groups of 32 Morton-ordered balls).  Record sizes: pab_record_sizes.
+ *    (lane groups of 32 balls ordered by a0 bucket, then 3-D Hilbert index).
+ *    Record sizes: pab_record_sizes.
  *  - Detector auxiliary data `det_aux` is [n_det][9] doubles: receive
  *    direction (unit, = -outward normal), element axes e1, e2.
  *  - Directivity: dir_kind 0 none (reference semantics), 1 cos^p (dir_param =
@@ -41,8 +42,10 @@ int pab_device_info(int device, int* sm_count, int* cc_major, int* cc_minor, int
 const char* pab_last_cuda_error(void);
 int pab_record_sizes(int* ball_a, int* ball_b, int* group_meta);
 
-/* Processing-order sort keys: key[i] = a0_bucket << 58 | morton30(pos[i]) << 28 | i
- * (a0 buckets: a0_buckets equal bins of [a0lo, a0hi]; n < 2^28).
+/* Processing-order sort keys: key[i] = a0_bucket << 58 | hilbert30(pos[i]) << 28 | i
+ * (hilbert30: 10-bit-per-axis 3-D Hilbert index of the position in the cube
+ * [lo, lo + extent)^3; a0 buckets: a0_buckets equal bins of [a0lo, a0hi]; n < 2^28).
+ * (The entry point keeps its first-version name; the key is a Hilbert key.)
  * Replaces: nothing (the reference visits balls in input order, radiator.py:185). */
 int pab_morton_keys(const double* pos /*[n][3]*/, const double* a0, int64_t n, double lox, double loy,
                     double loz, double extent, double a0lo, double a0hi, int a0_buckets, int64_t* keys,
