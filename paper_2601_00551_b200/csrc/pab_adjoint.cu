@@ -22,6 +22,9 @@
 
 namespace pab {
 
+#ifndef PAB_ADJ_TMA
+#define PAB_ADJ_TMA 0   // residual staging by TMA bulk copy (1) or 16-B cp.async (0)
+#endif
 constexpr int kSeg = 256;   // staged residual samples per warp and buffer
 constexpr int kPad = 96;    // zero padding after the staged samples (uniform-walk overrun)
 
@@ -34,6 +37,13 @@ __device__ __forceinline__ void cp_async16(float* smem_dst, const float* gsrc) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gsrc));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+__device__ __forceinline__ void mbar_wait(unsigned addr, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+          addr),
+      "r"(parity)
+      : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 struct Moments {
@@ -118,12 +128,18 @@ __device__ __forceinline__ void moments_run(const float* seg, int off, int n, fl
 //          (G <= exp(-cutoff^2/2) < 2^-24 for cutoff >= kUnmaskedCutoff):
 //          their terms are below FP32 resolution; lanes with an empty window
 //          discard their moments.
-template <int STAGE, bool MASK>
+template <int STAGE, bool MASK, bool POLY = false>
 __device__ __forceinline__ void moment_pair_masked(float2 res, float2 y, float qmax, float2& A0, float2& A1,
                                                    float2& A2, float2& A3) {
   const float2 q = __fmul2_rn(y, y);
-  const float2 G = MASK ? make_float2(q.x <= qmax ? ex2(-q.x) : 0.0f, q.y <= qmax ? ex2(-q.y) : 0.0f)
-                        : make_float2(ex2(-q.x), ex2(-q.y));
+  float2 G;
+  if (POLY) {
+    G = exp2_neg_poly2(q);
+    if (MASK) G = make_float2(q.x <= qmax ? G.x : 0.0f, q.y <= qmax ? G.y : 0.0f);
+  } else {
+    G = MASK ? make_float2(q.x <= qmax ? ex2(-q.x) : 0.0f, q.y <= qmax ? ex2(-q.y) : 0.0f)
+             : make_float2(ex2(-q.x), ex2(-q.y));
+  }
   const float2 r = __fmul2_rn(res, G);
   const float2 t = __fmul2_rn(r, y);
   A1 = __fadd2_rn(A1, t);
@@ -160,10 +176,14 @@ __device__ __forceinline__ void moment_block8(const float4* s4, float mf, const 
                                               float2& A3) {
   const float4 ra = s4[0], rb = s4[1];
   const float2 m2 = make_float2(mf, mf);
-  moment_pair_masked<STAGE, MASK>(make_float2(ra.x, ra.y), __ffma2_rn(m2, W.nsc2, c0), qmax, A0, A1, A2, A3);
-  moment_pair_masked<STAGE, MASK>(make_float2(ra.z, ra.w), __ffma2_rn(m2, W.nsc2, c1), qmax, A0, A1, A2, A3);
-  moment_pair_masked<STAGE, MASK>(make_float2(rb.x, rb.y), __ffma2_rn(m2, W.nsc2, c2), qmax, A0, A1, A2, A3);
-  moment_pair_masked<STAGE, MASK>(make_float2(rb.z, rb.w), __ffma2_rn(m2, W.nsc2, c3), qmax, A0, A1, A2, A3);
+  moment_pair_masked<STAGE, MASK, (PAB_POLY_PAIRS > 0)>(make_float2(ra.x, ra.y), __ffma2_rn(m2, W.nsc2, c0), qmax,
+                                                        A0, A1, A2, A3);
+  moment_pair_masked<STAGE, MASK, (PAB_POLY_PAIRS > 2)>(make_float2(ra.z, ra.w), __ffma2_rn(m2, W.nsc2, c1), qmax,
+                                                        A0, A1, A2, A3);
+  moment_pair_masked<STAGE, MASK, (PAB_POLY_PAIRS > 1)>(make_float2(rb.x, rb.y), __ffma2_rn(m2, W.nsc2, c2), qmax,
+                                                        A0, A1, A2, A3);
+  moment_pair_masked<STAGE, MASK, (PAB_POLY_PAIRS > 3)>(make_float2(rb.z, rb.w), __ffma2_rn(m2, W.nsc2, c3), qmax,
+                                                        A0, A1, A2, A3);
 }
 
 template <int STAGE, bool MASK>
@@ -215,10 +235,19 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
                double* __restrict__ gpart, int64_t n_pad, unsigned long long* __restrict__ ops_total,
                int* __restrict__ status) {
   __shared__ __align__(16) float seg_all[8][2][kSeg + kPad + 4];
+  __shared__ __align__(8) unsigned long long mbar[8][2];   // per warp and buffer: TMA completion
   const bool vec16 = (acq.n_out & 3) == 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
   if (g >= n_groups) return;
+  unsigned phase = 0;   // bit b: parity of buffer b's next mbarrier phase
+  if (lane == 0) {
+    for (int b = 0; b < 2; ++b)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&mbar[warp][b]))
+                   : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
   const int q = blockIdx.y;
   const int j0 = q * det_per_chunk;
   const int j1 = min(n_det, j0 + det_per_chunk);
@@ -260,41 +289,71 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
             (!nr && fits && rlo <= rhi && rhi - rlo + 1 <= kSeg ? kFlagUniform : 0);
       if (DIR != kDirNone) ddl = load_detdir(det_aux, jl);
     }
-    // stage res[j][lo .. hi] (lo a multiple of 4) + kPad zeros
-    auto stage_seg = [&](int jj, int buf) {
-      const int lo = __shfl_sync(0xffffffffu, rlo, jj);
-      const int hi = __shfl_sync(0xffffffffu, rhi, jj);
-      const int fl = __shfl_sync(0xffffffffu, rfl, jj);
-      if (fl & kFlagUniform) {
-        const float* src = res + (size_t)(jb + jj) * n_out + lo;
-        float* dst = seg_all[warp][buf];
-        const int len = hi - lo + 1;
-        const int len4 = (len + 3) >> 2;
-        if (vec16 && lo + 4 * len4 <= n_out) {   // 16-byte copies (16B-aligned rows and base)
-          for (int k = lane; k < len4; k += kWarp) cp_async16(dst + 4 * k, src + 4 * k);
-          // zero padding from the next 16-byte boundary (the partial vector
-          // above copied up to 3 extra finite residual samples: harmless)
-          float4* z = reinterpret_cast<float4*>(dst + 4 * len4);
-          if (lane < kPad / 4) z[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
-        } else {
-          for (int k = lane; k < len; k += kWarp) cp_async4(dst + k, src + k);
-          for (int k = lane; k < kPad; k += kWarp) dst[len + k] = 0.0f;
+    // stage res[j][lo .. hi] (lo a multiple of 4) + kPad zeros into buffer
+    // `buf`: one TMA bulk copy (16-B aligned rows) completing on the buffer's
+    // mbarrier, or 4-B cp.async when rows are not 16-B aligned
+    auto stage_seg = [&](int jj, int lo, int hi, int fl, int buf) {
+      if (!(fl & kFlagUniform)) return;
+      const float* src = res + (size_t)(jb + jj) * n_out + lo;
+      float* dst = seg_all[warp][buf];
+      const int len = hi - lo + 1;
+      if (vec16) {
+        const int len4 = (len + 3) >> 2;   // the last vector may carry up to 3 finite extra samples
+#if PAB_ADJ_TMA
+        if (lane == 0) {
+          const unsigned mb = (unsigned)__cvta_generic_to_shared(&mbar[warp][buf]);
+          const unsigned bytes = 16u * (unsigned)len4;
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  (unsigned)__cvta_generic_to_shared(dst)),
+              "l"(src), "r"(bytes), "r"(mb)
+              : "memory");
         }
+#else
+        static_assert(kSeg <= 8 * kWarp, "two 16-B vectors per lane cover the segment");
+        if (lane < len4) cp_async16(dst + 4 * lane, src + 4 * lane);
+        if (lane + kWarp < len4) cp_async16(dst + 4 * (lane + kWarp), src + 4 * (lane + kWarp));
+        cp_async_commit();
+#endif
+        float4* z = reinterpret_cast<float4*>(dst + 4 * len4);
+        if (lane < kPad / 4) z[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+      } else {
+        for (int k = lane; k < len; k += kWarp) cp_async4(dst + k, src + k);
+        for (int k = lane; k < kPad; k += kWarp) dst[len + k] = 0.0f;
+        cp_async_commit();
       }
-      cp_async_commit();
+    };
+    auto wait_seg = [&](int fl, int buf) {
+      if (!(fl & kFlagUniform)) return;
+#if PAB_ADJ_TMA
+      if (vec16) {
+        mbar_wait((unsigned)__cvta_generic_to_shared(&mbar[warp][buf]), (phase >> buf) & 1u);
+        phase ^= 1u << buf;
+        return;
+      }
+#endif
+      cp_async_wait_all();
     };
     float gb[5] = {0.f, 0.f, 0.f, 0.f, 0.f};   // FP32 batch sums of the pair terms
-    stage_seg(0, 0);
+    int nlo = __shfl_sync(0xffffffffu, rlo, 0);
+    int nhi = __shfl_sync(0xffffffffu, rhi, 0);
+    int nfl = __shfl_sync(0xffffffffu, rfl, 0);
+    stage_seg(0, nlo, nhi, nfl, 0);
     for (int jj = 0; jj < nd; ++jj) {
       const int buf = jj & 1;
-      const int lo = __shfl_sync(0xffffffffu, rlo, jj);
-      const int hi = __shfl_sync(0xffffffffu, rhi, jj);
-      const int fl = __shfl_sync(0xffffffffu, rfl, jj);
+      const int lo = nlo, hi = nhi, fl = nfl;
       GroupDet gd = shfl_gd_fast(gdl, jj);
       const DetDir dd = shfl_detdir<DIR>(ddl, jj);
-      cp_async_wait_all();
-      __syncwarp();
-      if (jj + 1 < nd) stage_seg(jj + 1, buf ^ 1);
+      wait_seg(fl, buf);
+      __syncwarp();   // every lane is past detector jj-1: its buffer may be refilled
+      if (jj + 1 < nd) {
+        nlo = __shfl_sync(0xffffffffu, rlo, jj + 1);
+        nhi = __shfl_sync(0xffffffffu, rhi, jj + 1);
+        nfl = __shfl_sync(0xffffffffu, rfl, jj + 1);
+        stage_seg(jj + 1, nlo, nhi, nfl, buf ^ 1);
+      }
       if (lo > hi) continue;
 
       Moments M;
@@ -374,7 +433,6 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
         gb[4] += gz;
       }
     }
-    cp_async_wait_all();
     __syncwarp();
 #pragma unroll
     for (int c = 0; c < 5; ++c) acc[c] += (double)gb[c];

@@ -156,10 +156,17 @@ struct Walk {
   float qmax;
 };
 
-template <bool MASK>
+template <bool MASK, bool POLY = false>
 __device__ __forceinline__ float2 rmw_pair(float2 o, float2 m2, float2 c, const Walk& w) {
   const float2 y = __ffma2_rn(m2, w.nsc2, c);
-  const float2 g = gauss2<MASK>(__fmul2_rn(y, y), w.qmax);
+  const float2 q = __fmul2_rn(y, y);
+  float2 g;
+  if (POLY) {
+    g = exp2_neg_poly2(q);
+    if (MASK) g = make_float2(q.x <= w.qmax ? g.x : 0.0f, q.y <= w.qmax ? g.y : 0.0f);
+  } else {
+    g = gauss2<MASK>(q, w.qmax);
+  }
   return __ffma2_rn(w.Ak2, __fmul2_rn(y, g), o);
 }
 
@@ -208,10 +215,11 @@ __device__ __forceinline__ void rmw_uniform(float* tile, int lane, int J0, int L
     const float2 a2 = make_float2(ta[4 * kWarp], ta[5 * kWarp]), a3 = make_float2(ta[6 * kWarp], ta[7 * kWarp]);
     const float2 b0 = make_float2(tb[0], tb[kWarp]), b1 = make_float2(tb[2 * kWarp], tb[3 * kWarp]);
     const float2 b2 = make_float2(tb[4 * kWarp], tb[5 * kWarp]), b3 = make_float2(tb[6 * kWarp], tb[7 * kWarp]);
-    const float2 na0 = rmw_pair<MASK>(a0, ma, w.c0, w), nb0 = rmw_pair<MASK>(b0, mb, w.c0, w);
-    const float2 na1 = rmw_pair<MASK>(a1, ma, w.c1, w), nb1 = rmw_pair<MASK>(b1, mb, w.c1, w);
-    const float2 na2 = rmw_pair<MASK>(a2, ma, w.c2, w), nb2 = rmw_pair<MASK>(b2, mb, w.c2, w);
-    const float2 na3 = rmw_pair<MASK>(a3, ma, w.c3, w), nb3 = rmw_pair<MASK>(b3, mb, w.c3, w);
+    constexpr int kP = PAB_POLY_PAIRS;
+    const float2 na0 = rmw_pair<MASK, (kP > 0)>(a0, ma, w.c0, w), nb0 = rmw_pair<MASK, (kP > 1)>(b0, mb, w.c0, w);
+    const float2 na1 = rmw_pair<MASK, (kP > 2)>(a1, ma, w.c1, w), nb1 = rmw_pair<MASK, (kP > 3)>(b1, mb, w.c1, w);
+    const float2 na2 = rmw_pair<MASK, (kP > 4)>(a2, ma, w.c2, w), nb2 = rmw_pair<MASK, (kP > 5)>(b2, mb, w.c2, w);
+    const float2 na3 = rmw_pair<MASK, (kP > 6)>(a3, ma, w.c3, w), nb3 = rmw_pair<MASK, (kP > 7)>(b3, mb, w.c3, w);
     ta[0] = na0.x; ta[kWarp] = na0.y; ta[2 * kWarp] = na1.x; ta[3 * kWarp] = na1.y;
     ta[4 * kWarp] = na2.x; ta[5 * kWarp] = na2.y; ta[6 * kWarp] = na3.x; ta[7 * kWarp] = na3.y;
     tb[0] = nb0.x; tb[kWarp] = nb0.y; tb[2 * kWarp] = nb1.x; tb[3 * kWarp] = nb1.y;
