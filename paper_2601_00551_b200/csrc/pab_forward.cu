@@ -110,20 +110,22 @@ __device__ __forceinline__ void rmw_window(float* tile, int lane, int lo, int hi
 }
 
 // Reduce rows [a, b) of the circular tile across lanes (lane l reduces one
-// row of each 32-row block, columns read in rotated order), zero them, and
-// hand each row sum to `sink(r, v)`.
+// row of each 32-row block, reading it as eight 16-byte chunks in rotated
+// order: the 8 lanes of a quarter-warp hit 8 distinct bank quads), zero them,
+// and hand each row sum to `sink(r, v)`.
 template <class Sink>
 __device__ __forceinline__ void flush_rows(float* tile, int lane, int a, int b, Sink sink) {
   for (int r0 = a; r0 < b; r0 += kWarp) {
     const int r = r0 + lane;
     if (r < b) {
-      float* trow = tile + (r % kTile) * kWarp;
+      float4* trow = reinterpret_cast<float4*>(tile + (r % kTile) * kWarp);
       float s = 0.0f;
-#pragma unroll 8
-      for (int i = 0; i < kWarp; ++i) {
-        const int col = (i + lane) & 31;
-        s += trow[col];
-        trow[col] = 0.0f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int c = (i + lane) & 7;
+        const float4 v = trow[c];
+        s += (v.x + v.y) + (v.z + v.w);
+        trow[c] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
       sink(r, s);
     }
@@ -183,9 +185,13 @@ __device__ __forceinline__ void rmw_block8(float* t, float mf, const Walk& w) {
   t[4 * kWarp] = n2.x; t[5 * kWarp] = n2.y; t[6 * kWarp] = n3.x; t[7 * kWarp] = n3.y;
 }
 
+#ifndef PAB_FWD_UNROLL
+#define PAB_FWD_UNROLL 2   // 8-sample blocks per loop trip
+#endif
 template <bool MASK>
 __device__ __forceinline__ void rmw_uniform(float* tile, int lane, int J0, int L, int lim, float mf, float fs,
                                             float sc, float ps, float Ak, float qmax) {
+  constexpr int K = PAB_FWD_UNROLL;
   Walk w;
   w.nsc2 = make_float2(-sc, -sc);
   w.Ak2 = make_float2(Ak, Ak);
@@ -201,32 +207,40 @@ __device__ __forceinline__ void rmw_uniform(float* tile, int lane, int J0, int L
   int Jb = J0;   // row of the current block's first sample
   int nb = L >> 3;
 #pragma unroll 1
-  for (; nb >= 2; nb -= 2) {
-    float* ta = Jb <= lim ? tile + s * kWarp + lane : dump;
-    s += 8;
-    if (s == kTile) s = 0;
-    float* tb = Jb + 8 <= lim ? tile + s * kWarp + lane : dump;
-    s += 8;
-    if (s == kTile) s = 0;
-    Jb += 16;
-    // both blocks' reads before either block's writes
-    const float2 ma = make_float2(mf, mf), mb = make_float2(mf + step, mf + step);
-    const float2 a0 = make_float2(ta[0], ta[kWarp]), a1 = make_float2(ta[2 * kWarp], ta[3 * kWarp]);
-    const float2 a2 = make_float2(ta[4 * kWarp], ta[5 * kWarp]), a3 = make_float2(ta[6 * kWarp], ta[7 * kWarp]);
-    const float2 b0 = make_float2(tb[0], tb[kWarp]), b1 = make_float2(tb[2 * kWarp], tb[3 * kWarp]);
-    const float2 b2 = make_float2(tb[4 * kWarp], tb[5 * kWarp]), b3 = make_float2(tb[6 * kWarp], tb[7 * kWarp]);
-    constexpr int kP = PAB_POLY_PAIRS;
-    const float2 na0 = rmw_pair<MASK, (kP > 0)>(a0, ma, w.c0, w), nb0 = rmw_pair<MASK, (kP > 1)>(b0, mb, w.c0, w);
-    const float2 na1 = rmw_pair<MASK, (kP > 2)>(a1, ma, w.c1, w), nb1 = rmw_pair<MASK, (kP > 3)>(b1, mb, w.c1, w);
-    const float2 na2 = rmw_pair<MASK, (kP > 4)>(a2, ma, w.c2, w), nb2 = rmw_pair<MASK, (kP > 5)>(b2, mb, w.c2, w);
-    const float2 na3 = rmw_pair<MASK, (kP > 6)>(a3, ma, w.c3, w), nb3 = rmw_pair<MASK, (kP > 7)>(b3, mb, w.c3, w);
-    ta[0] = na0.x; ta[kWarp] = na0.y; ta[2 * kWarp] = na1.x; ta[3 * kWarp] = na1.y;
-    ta[4 * kWarp] = na2.x; ta[5 * kWarp] = na2.y; ta[6 * kWarp] = na3.x; ta[7 * kWarp] = na3.y;
-    tb[0] = nb0.x; tb[kWarp] = nb0.y; tb[2 * kWarp] = nb1.x; tb[3 * kWarp] = nb1.y;
-    tb[4 * kWarp] = nb2.x; tb[5 * kWarp] = nb2.y; tb[6 * kWarp] = nb3.x; tb[7 * kWarp] = nb3.y;
-    mf += 2.0f * step;
+  for (; nb >= K; nb -= K) {
+    float* t[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      t[k] = Jb + 8 * k <= lim ? tile + s * kWarp + lane : dump;
+      s += 8;
+      if (s == kTile) s = 0;
+    }
+    Jb += 8 * K;
+    // every block's reads before any block's writes
+    float2 o[K][4];
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) o[k][i] = make_float2(t[k][2 * i * kWarp], t[k][(2 * i + 1) * kWarp]);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const float2 m2 = make_float2(mf + (float)k * step, mf + (float)k * step);
+      o[k][0] = rmw_pair<MASK>(o[k][0], m2, w.c0, w);
+      o[k][1] = rmw_pair<MASK>(o[k][1], m2, w.c1, w);
+      o[k][2] = rmw_pair<MASK>(o[k][2], m2, w.c2, w);
+      o[k][3] = rmw_pair<MASK>(o[k][3], m2, w.c3, w);
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        t[k][2 * i * kWarp] = o[k][i].x;
+        t[k][(2 * i + 1) * kWarp] = o[k][i].y;
+      }
+    mf += (float)K * step;
   }
-  if (nb) {
+#pragma unroll 1
+  for (; nb > 0; --nb) {
     rmw_block8<MASK>(Jb <= lim ? tile + s * kWarp + lane : dump, mf, w);
     mf += step;
     s += 8;
@@ -320,8 +334,11 @@ __device__ __forceinline__ void evaluate_pair(float* tile, int lane, const Acq& 
     rmw_window(tile, lane, max(nlo, clip_lo), min(nhi, clip_hi), nkc, acq.f, -sc, nphi, Ak);
 }
 
+#ifndef PAB_FWD_MINB
+#define PAB_FWD_MINB 2
+#endif
 template <int DIR, bool MASK>
-__global__ void __launch_bounds__(kMaxWarps * 32, 2)
+__global__ void __launch_bounds__(kMaxWarps * 32, PAB_FWD_MINB)
 forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
                const GroupMeta* __restrict__ gmeta, int64_t n_groups,
                const double* __restrict__ det_pos, const double* __restrict__ det_aux, int n_det,
@@ -453,19 +470,21 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       int touched = fp - 1;   // highest row any window of this sweep may have written
       for (int i0 = s_begin; i0 < s_end; i0 += kWarp) {
         const int nb = min(kWarp, s_end - i0);
-        // lane l prepares the geometry of the l-th group of this batch
+        // lane l prepares the geometry of the l-th group of this batch; its
+        // start bin, span and near flag travel in one word
         GroupDet gd_l = empty_gd();
         int64_t g_l = 0;
-        int bin_l = 0, near_l = 0, hi_l = -1;
+        unsigned word_l = 0;
         if (lane < nb) {
           const int gl = sorted[i0 + lane];
           g_l = cg0 + gl;
-          bin_l = gbin[gl];
+          const int bin = gbin[gl];
           const GroupMeta gm = gmeta[g_l];
           gd_l = group_det(gm, det.px, det.py, det.pz, acq);
-          near_l = group_near(acq, gd_l, gm) ? 1 : 0;
-          int glo;
-          group_range(acq, gd_l, gm, &glo, &hi_l);
+          int glo, ghi;
+          group_range(acq, gd_l, gm, &glo, &ghi);
+          word_l = (unsigned)bin | ((unsigned)(ghi - (bin << kBinShift)) << 16) |
+                   (group_near(acq, gd_l, gm) ? 0x80000000u : 0u);
         }
         // software pipeline: records of the next group are loaded while the
         // current one is evaluated
@@ -481,22 +500,29 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
             An = ra[g_next * kWarp + lane];
             Bn = rb[g_next * kWarp + lane];
           }
-          const int blo = __shfl_sync(0xffffffffu, bin_l, k) << kBinShift;
-          const int near = __shfl_sync(0xffffffffu, near_l, k);
-          const int ghi = __shfl_sync(0xffffffffu, hi_l, k);
-          if (blo > fp) {   // rows past the last touched one are still zero: skip them
-            flush_rows(tile, lane, fp, min(min(blo, fp + kTile), touched + 1), sink);
-            fp = blo;
+          const unsigned word = __shfl_sync(0xffffffffu, word_l, k);
+          const int blo = (int)(word & 0xFFFFu) << kBinShift;
+          const int ghi = blo + (int)((word >> 16) & 0x7FFFu);
+          const int near = (int)(word >> 31);
+          // lazy flush: rows below blo are complete; only those whose slots
+          // this group's rows [blo, ghi + 7] reuse must go now -- flushed in
+          // batches of >= 32 rows when possible
+          const int need = ghi + 8 - kTile;
+          if (need > fp) {
+            const int upto = min(blo, max(need, fp + kWarp));
+            flush_rows(tile, lane, fp, min(upto, touched + 1), sink);
+            fp = upto;
           }
           touched = max(touched, ghi + 7);
-          evaluate_pair_uniform<DIR, MASK>(tile, lane, acq, gd, dd, A, B, near, my_ops, fp);
+          evaluate_pair_uniform<DIR, MASK>(tile, lane, acq, gd, dd, A, B, near, my_ops, blo);
           __syncwarp();
         }
       }
-      if (s_begin < s_end) flush_rows(tile, lane, fp, min(min(fp + kTile, n_out), touched + 1), sink);
+      if (s_begin < s_end) flush_rows(tile, lane, fp, min(n_out, touched + 1), sink);
       // rows past the signal end (clipped windows' overrun) are never
       // flushed: clear the tile for the next chunk / the linear passes
-      for (int r = 0; r < kTile; ++r) tile[r * kWarp + lane] = 0.0f;
+      for (int i = lane; i < kTile * kWarp / 4; i += kWarp)
+        reinterpret_cast<float4*>(tile)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
       __syncwarp();
     }
     __syncthreads();
@@ -630,6 +656,7 @@ int pab_forward(const void* rec_a, const void* rec_b, const void* group_meta, in
   dim3 grid((unsigned)n_det, (unsigned)partitions);
   auto launch = [&](auto kernel) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     kernel<<<grid, warps * kWarp, smem, (cudaStream_t)stream>>>(
         (const BallA*)rec_a, (const BallB*)rec_b, (const GroupMeta*)group_meta, n_groups, det_pos, det_aux,
         n_det, acq, per_part, partial_rows, ops_total, status);
