@@ -50,82 +50,48 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
-// acc[slot] += Ak * y G over n consecutive samples starting at column pointer
-// t (row stride 32 floats, no wrap inside), m-offset mf, step fs.  Eight
-// samples per iteration ride four packed FP32x2 registers (FFMA2/FMUL2); all
-// eight shared-memory reads are issued before the arithmetic (ILP).
-__device__ __forceinline__ float2 contrib2(float2 y, float2 Ak2) {
-  const float2 q = __fmul2_rn(y, y);
-  return __fmul2_rn(Ak2, __fmul2_rn(y, make_float2(ex2(-q.x), ex2(-q.y))));
-}
+// Tile layout: per warp, slot (circular row) s of lane l lives at float
+// index tidx(s, l) = ((s / 4) * 32 + l) * 4 + s % 4, i.e. a lane owns four
+// consecutive rows as one 16-byte vector and the 32 lanes' vectors of a row
+// quad are adjacent.  A lane's 8-sample block is two LDS.128 + two STS.128,
+// and because lane l always addresses bank quad l % 8, those accesses are
+// conflict-free whatever row each lane is at.
+__device__ __forceinline__ int tidx(int slot, int lane) { return (((slot >> 2) * kWarp + lane) << 2) | (slot & 3); }
 
-__device__ __forceinline__ void rmw_run(float* t, int n, float mf, float fs, float sc, float ps, float Ak) {
-  const float2 nsc2 = make_float2(-sc, -sc);
-  const float2 Ak2 = make_float2(Ak, Ak);
-  // y of pair k of an 8-sample block: (mb + 2k fs, mb + (2k+1) fs) * -sc + ps
-  const float2 c0 = make_float2(ps, fmaf(fs, -sc, ps));
-  const float2 c1 = make_float2(fmaf(2.0f * fs, -sc, ps), fmaf(3.0f * fs, -sc, ps));
-  const float2 c2 = make_float2(fmaf(4.0f * fs, -sc, ps), fmaf(5.0f * fs, -sc, ps));
-  const float2 c3 = make_float2(fmaf(6.0f * fs, -sc, ps), fmaf(7.0f * fs, -sc, ps));
-  int i = 0;
-#pragma unroll 1
-  for (; i + 8 <= n; i += 8, mf += 8.0f * fs, t += 8 * kWarp) {
-    const float2 m2 = make_float2(mf, mf);
-    const float2 o0 = make_float2(t[0], t[kWarp]);
-    const float2 o1 = make_float2(t[2 * kWarp], t[3 * kWarp]);
-    const float2 o2 = make_float2(t[4 * kWarp], t[5 * kWarp]);
-    const float2 o3 = make_float2(t[6 * kWarp], t[7 * kWarp]);
-    const float2 n0 = __fadd2_rn(o0, contrib2(__ffma2_rn(m2, nsc2, c0), Ak2));
-    const float2 n1 = __fadd2_rn(o1, contrib2(__ffma2_rn(m2, nsc2, c1), Ak2));
-    const float2 n2 = __fadd2_rn(o2, contrib2(__ffma2_rn(m2, nsc2, c2), Ak2));
-    const float2 n3 = __fadd2_rn(o3, contrib2(__ffma2_rn(m2, nsc2, c3), Ak2));
-    t[0] = n0.x; t[kWarp] = n0.y; t[2 * kWarp] = n1.x; t[3 * kWarp] = n1.y;
-    t[4 * kWarp] = n2.x; t[5 * kWarp] = n2.y; t[6 * kWarp] = n3.x; t[7 * kWarp] = n3.y;
-  }
-#pragma unroll 1
-  for (; i + 2 <= n; i += 2, mf += 2.0f * fs, t += 2 * kWarp) {
-    const float2 o = make_float2(t[0], t[kWarp]);
-    const float2 nv = __fadd2_rn(o, contrib2(__ffma2_rn(make_float2(mf, mf), nsc2, c0), Ak2));
-    t[0] = nv.x;
-    t[kWarp] = nv.y;
-  }
-  if (i < n) {
-    const float y = fmaf(mf, -sc, ps);
-    *t += Ak * (y * ex2(-y * y));
-  }
-}
-
-// Window [lo, hi] of one pair into the circular tile (slot = J % kTile).
+// Window [lo, hi] of one pair into the circular tile (linear-pass path for
+// wide groups: scalar, exact window).
 __device__ __forceinline__ void rmw_window(float* tile, int lane, int lo, int hi, int m0, int f, float sc,
                                            float phi, float Ak) {
   if (lo > hi) return;
   const float ps = phi * sc;
   const float fs = (float)f;
-  const int s0 = lo % kTile;
-  const int n = hi - lo + 1;
-  const int n1 = min(n, kTile - s0);
-  const float mf = (float)(lo * f - m0);
-  rmw_run(tile + s0 * kWarp + lane, n1, mf, fs, sc, ps, Ak);
-  if (n > n1) rmw_run(tile + lane, n - n1, mf + (float)n1 * fs, fs, sc, ps, Ak);
+  int s = lo % kTile;
+  float mf = (float)(lo * f - m0);
+  for (int J = lo; J <= hi; ++J) {
+    const float y = fmaf(mf, -sc, ps);
+    tile[tidx(s, lane)] += Ak * (y * ex2(-y * y));
+    mf += fs;
+    if (++s == kTile) s = 0;
+  }
 }
 
-// Reduce rows [a, b) of the circular tile across lanes (lane l reduces one
-// row of each 32-row block, reading it as eight 16-byte chunks in rotated
-// order: the 8 lanes of a quarter-warp hit 8 distinct bank quads), zero them,
-// and hand each row sum to `sink(r, v)`.
+// Reduce rows [a, b) of the circular tile across lanes, zero them, and hand
+// each row sum to `sink(r, v)`.  Lane l reduces row a + 32k + l, visiting the
+// 32 columns in the order c(i, l) = ((i + l/4) % 8) + 8 (i / 8): for every i
+// the 32 lanes then hit 32 distinct banks (bank = 4 (c % 8) + row % 4).
 template <class Sink>
 __device__ __forceinline__ void flush_rows(float* tile, int lane, int a, int b, Sink sink) {
   for (int r0 = a; r0 < b; r0 += kWarp) {
     const int r = r0 + lane;
     if (r < b) {
-      float4* trow = reinterpret_cast<float4*>(tile + (r % kTile) * kWarp);
+      const int slot = r % kTile;
+      float* base = tile + ((slot >> 2) * kWarp << 2) + (slot & 3);
       float s = 0.0f;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int c = (i + lane) & 7;
-        const float4 v = trow[c];
-        s += (v.x + v.y) + (v.z + v.w);
-        trow[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int i = 0; i < kWarp; ++i) {
+        const int c = (((i & 7) + (lane >> 2)) & 7) | (i & 24);
+        s += base[c << 2];
+        base[c << 2] = 0.0f;
       }
       sink(r, s);
     }
@@ -172,17 +138,11 @@ __device__ __forceinline__ float2 rmw_pair(float2 o, float2 m2, float2 c, const 
   return __ffma2_rn(w.Ak2, __fmul2_rn(y, g), o);
 }
 
-template <bool MASK>
-__device__ __forceinline__ void rmw_block8(float* t, float mf, const Walk& w) {
-  const float2 m2 = make_float2(mf, mf);
-  const float2 o0 = make_float2(t[0], t[kWarp]);
-  const float2 o1 = make_float2(t[2 * kWarp], t[3 * kWarp]);
-  const float2 o2 = make_float2(t[4 * kWarp], t[5 * kWarp]);
-  const float2 o3 = make_float2(t[6 * kWarp], t[7 * kWarp]);
-  const float2 n0 = rmw_pair<MASK>(o0, m2, w.c0, w), n1 = rmw_pair<MASK>(o1, m2, w.c1, w);
-  const float2 n2 = rmw_pair<MASK>(o2, m2, w.c2, w), n3 = rmw_pair<MASK>(o3, m2, w.c3, w);
-  t[0] = n0.x; t[kWarp] = n0.y; t[2 * kWarp] = n1.x; t[3 * kWarp] = n1.y;
-  t[4 * kWarp] = n2.x; t[5 * kWarp] = n2.y; t[6 * kWarp] = n3.x; t[7 * kWarp] = n3.y;
+__device__ __forceinline__ float4 rmw4(float4 o, float2 m2, float2 ca, float2 cb, const Walk& w,
+                                       float2 (*pair)(float2, float2, float2, const Walk&)) {
+  const float2 lo = pair(make_float2(o.x, o.y), m2, ca, w);
+  const float2 hi = pair(make_float2(o.z, o.w), m2, cb, w);
+  return make_float4(lo.x, lo.y, hi.x, hi.y);
 }
 
 #ifndef PAB_FWD_UNROLL
@@ -201,58 +161,58 @@ __device__ __forceinline__ void rmw_uniform(float* tile, int lane, int J0, int L
   w.c2 = __fadd2_rn(w.c1, make_float2(dl2, dl2));
   w.c3 = __fadd2_rn(w.c2, make_float2(dl2, dl2));
   w.qmax = qmax;
-  float* const dump = tile + kTile * kWarp + lane;
+  float4* const T = reinterpret_cast<float4*>(tile) + lane;   // quad q of this lane: T[q * 32]
+  const int dump = kTile / 4;                                   // dump block = quads kTile/4, kTile/4 + 1
   const float step = 8.0f * fs;
-  int s = J0 % kTile;
-  int Jb = J0;   // row of the current block's first sample
+  int q = (J0 % kTile) >> 2;   // quad of the current block (even)
+  int Jb = J0;                 // row of the current block's first sample
   int nb = L >> 3;
 #pragma unroll 1
   for (; nb >= K; nb -= K) {
-    float* t[K];
+    int qq[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      t[k] = Jb + 8 * k <= lim ? tile + s * kWarp + lane : dump;
-      s += 8;
-      if (s == kTile) s = 0;
+      qq[k] = Jb + 8 * k <= lim ? q : dump;
+      q += 2;
+      if (q == kTile / 4) q = 0;
     }
     Jb += 8 * K;
     // every block's reads before any block's writes
-    float2 o[K][4];
+    float4 o[K][2];
 #pragma unroll
-    for (int k = 0; k < K; ++k)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) o[k][i] = make_float2(t[k][2 * i * kWarp], t[k][(2 * i + 1) * kWarp]);
+    for (int k = 0; k < K; ++k) {
+      o[k][0] = T[qq[k] * kWarp];
+      o[k][1] = T[(qq[k] + 1) * kWarp];
+    }
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const float2 m2 = make_float2(mf + (float)k * step, mf + (float)k * step);
-      o[k][0] = rmw_pair<MASK>(o[k][0], m2, w.c0, w);
-      o[k][1] = rmw_pair<MASK>(o[k][1], m2, w.c1, w);
-      o[k][2] = rmw_pair<MASK>(o[k][2], m2, w.c2, w);
-      o[k][3] = rmw_pair<MASK>(o[k][3], m2, w.c3, w);
+      o[k][0] = rmw4(o[k][0], m2, w.c0, w.c1, w, rmw_pair<MASK>);
+      o[k][1] = rmw4(o[k][1], m2, w.c2, w.c3, w, rmw_pair<MASK>);
     }
 #pragma unroll
-    for (int k = 0; k < K; ++k)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        t[k][2 * i * kWarp] = o[k][i].x;
-        t[k][(2 * i + 1) * kWarp] = o[k][i].y;
-      }
+    for (int k = 0; k < K; ++k) {
+      T[qq[k] * kWarp] = o[k][0];
+      T[(qq[k] + 1) * kWarp] = o[k][1];
+    }
     mf += (float)K * step;
   }
 #pragma unroll 1
   for (; nb > 0; --nb) {
-    rmw_block8<MASK>(Jb <= lim ? tile + s * kWarp + lane : dump, mf, w);
+    const int qb = Jb <= lim ? q : dump;
+    const float2 m2 = make_float2(mf, mf);
+    const float4 a = T[qb * kWarp], b = T[(qb + 1) * kWarp];
+    T[qb * kWarp] = rmw4(a, m2, w.c0, w.c1, w, rmw_pair<MASK>);
+    T[(qb + 1) * kWarp] = rmw4(b, m2, w.c2, w.c3, w, rmw_pair<MASK>);
     mf += step;
-    s += 8;
-    if (s == kTile) s = 0;
+    q += 2;
+    if (q == kTile / 4) q = 0;
     Jb += 8;
   }
   if (L & 4) {   // 4-sample tail (8-aligned start: no wrap inside)
-    float* t = Jb <= lim ? tile + s * kWarp + lane : dump;
+    const int qb = Jb <= lim ? q : dump;
     const float2 m2 = make_float2(mf, mf);
-    const float2 o0 = make_float2(t[0], t[kWarp]), o1 = make_float2(t[2 * kWarp], t[3 * kWarp]);
-    const float2 n0 = rmw_pair<MASK>(o0, m2, w.c0, w), n1 = rmw_pair<MASK>(o1, m2, w.c1, w);
-    t[0] = n0.x; t[kWarp] = n0.y; t[2 * kWarp] = n1.x; t[3 * kWarp] = n1.y;
+    T[qb * kWarp] = rmw4(T[qb * kWarp], m2, w.c0, w.c1, w, rmw_pair<MASK>);
   }
 }
 
@@ -373,6 +333,7 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
 #endif
   for (int i = tid; i < n_out; i += nthr) row[i] = 0.0f;
   for (int i = tid; i < W * kTileAlloc * kWarp; i += nthr) tiles[i] = 0.0f;
+  static_assert(kTile % 8 == 0, "8-sample blocks must not straddle the circular wrap");
   for (int i = tid; i < W * kTile; i += nthr) stage[i] = 0.0f;
 
   const Detector det = load_detector(det_pos, det_aux, j);
