@@ -216,51 +216,66 @@ __device__ __forceinline__ void rmw_uniform(float* tile, int lane, int J0, int L
   }
 }
 
-// One ball (lane) of one group against the CTA's detector in the time sweep:
-// setup, then the warp-uniform walk of the u- window (and, if any lane has
-// one, of the u+ near-field window).  `fp` is the first live tile row (the
-// start of empty windows, which are redirected to the dump block).  Groups
-// whose detector is close (slow geometry) take the linear-pass path instead.
-template <int DIR, bool MASK>
-__device__ __forceinline__ void evaluate_pair_uniform(float* tile, int lane, const Acq& acq, const GroupDet& gd,
-                                                      const DetDir& dd, const BallA& A, const BallB& B, int near,
-                                                      unsigned long long& ops, int fp) {
+// One ball (lane) of one group against the CTA's detector in the time sweep,
+// split into setup (geometry, window, weight: a latency-bound chain) and walk
+// so the sweep can compute two groups' setups side by side.  Groups whose
+// detector is close (slow geometry) take the linear-pass path instead.
+struct PairSetup {
+  int kc, jlo, jhi, J0, L;
+  float phi, d, rho, sc, Ak, qmax;
+  bool live;
+};
+
+template <int DIR>
+__device__ __forceinline__ PairSetup pair_setup(const Acq& acq, const GroupDet& gd, const DetDir& dd, const BallA& A,
+                                                const BallB& B, unsigned long long& ops, int fp) {
+  PairSetup p;
   const PairGeom pg = pair_geom_fast(gd, A, B, acq);
-  const float rho = acq.cutoff * A.a0 * acq.inv_vdt_f;
-  const float sc = acq.vdt_f * kSqrtHalfLog2e * B.inv_a0;
-  const float rs = rho * sc;
-  const float qmax = rs * rs;
-  int jlo, jhi;
-  pair_window(pg.kc, pg.phi, rho, acq, &jlo, &jhi);
-  const bool live = B.orig >= 0;
-  if (!live) { jlo = 1; jhi = 0; }
-  ops += (unsigned long long)max(jhi - jlo + 1, 0);
+  p.kc = pg.kc;
+  p.phi = pg.phi;
+  p.d = pg.d;
+  p.rho = acq.cutoff * A.a0 * acq.inv_vdt_f;
+  p.sc = acq.vdt_f * kSqrtHalfLog2e * B.inv_a0;
+  const float rs = p.rho * p.sc;
+  p.qmax = rs * rs;
+  pair_window(pg.kc, pg.phi, p.rho, acq, &p.jlo, &p.jhi);
+  p.live = B.orig >= 0;
+  if (!p.live) { p.jlo = 1; p.jhi = 0; }
+  ops += (unsigned long long)max(p.jhi - p.jlo + 1, 0);
   float D = 1.0f;
   if (DIR != kDirNone)
     D = dir_weight<DIR, false>(dd, pg.rx * pg.id, pg.ry * pg.id, pg.rz * pg.id, pg.id, acq.dir_param,
                                acq.dir_param, B.inv_a0, nullptr, nullptr);
   // u G amp = Ak * y G with Ak = amp * kappa = (p0 D / 2d) a0 sqrt(2 ln 2)
-  const float Ak = (0.5f * B.p0 * D) * pg.id * (A.a0 * kSqrt2Ln2);
+  p.Ak = (0.5f * B.p0 * D) * pg.id * (A.a0 * kSqrt2Ln2);
+  const bool empty = p.jlo > p.jhi;
+  p.J0 = (empty ? fp : p.jlo) & ~7;
+  p.L = __reduce_max_sync(0xffffffffu, empty ? 0 : p.jhi - p.J0 + 1);
+  return p;
+}
+
+// The warp-uniform walk of the u- window (and, if any lane has one, of the
+// u+ near-field window).  `fp` is a live tile row: the start of empty
+// windows, which are redirected to the dump block.
+template <bool MASK>
+__device__ __forceinline__ void pair_walk(float* tile, int lane, const Acq& acq, const PairSetup& p, int near,
+                                          unsigned long long& ops, int fp) {
   const float fs = (float)acq.f;
-  {
-    const bool empty = jlo > jhi;
-    const int J0 = (empty ? fp : jlo) & ~7;
-    const int L = __reduce_max_sync(0xffffffffu, empty ? 0 : jhi - J0 + 1);
-    if (L > 0)
-      rmw_uniform<MASK>(tile, lane, J0, (L + 3) & ~3, empty ? -1 : jhi, (float)(J0 * acq.f - pg.kc), fs, sc,
-                        pg.phi * sc, empty ? 0.0f : Ak, qmax);
-  }
+  const bool empty_u = p.jlo > p.jhi;
+  if (p.L > 0)
+    rmw_uniform<MASK>(tile, lane, p.J0, (p.L + 3) & ~3, empty_u ? -1 : p.jhi, (float)(p.J0 * acq.f - p.kc), fs,
+                      p.sc, p.phi * p.sc, empty_u ? 0.0f : p.Ak, p.qmax);
   if (near) {
     int nlo = 1, nhi = 0, nkc = 0;
     float nphi = 0.0f;
-    if (live) pair_near_window(pg.d, rho, acq, &nlo, &nhi, &nkc, &nphi);
+    if (p.live) pair_near_window(p.d, p.rho, acq, &nlo, &nhi, &nkc, &nphi);
     ops += (unsigned long long)max(nhi - nlo + 1, 0);
     if (__any_sync(0xffffffffu, nlo <= nhi)) {   // u+ = -kappa y: walk with -sc
       const bool empty = nlo > nhi;
       const int J0 = (empty ? fp : nlo) & ~7;
       const int L = __reduce_max_sync(0xffffffffu, empty ? 0 : nhi - J0 + 1);
-      rmw_uniform<MASK>(tile, lane, J0, (L + 3) & ~3, empty ? -1 : nhi, (float)(J0 * acq.f - nkc), fs, -sc,
-                        nphi * -sc, empty ? 0.0f : Ak, qmax);
+      rmw_uniform<MASK>(tile, lane, J0, (L + 3) & ~3, empty ? -1 : nhi, (float)(J0 * acq.f - nkc), fs, -p.sc,
+                        nphi * -p.sc, empty ? 0.0f : p.Ak, p.qmax);
     }
   }
 }
@@ -389,6 +404,9 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       if (lane == 0) {
         misc[0] = hist[n_bins];   // start of the oversize list = regular count
         misc[1] = carry;          // all listed groups
+#ifdef PAB_FWD_STATS   // tuning builds: oversize-group count in the op counter's high bits
+        if (ops_total) atomicAdd(ops_total, (unsigned long long)(carry - hist[n_bins]) << 40);
+#endif
       }
       for (int b0 = 0; b0 < cn; b0 += kWarp) {
         const int gl = b0 + lane;
@@ -447,36 +465,50 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
           word_l = (unsigned)bin | ((unsigned)(ghi - (bin << kBinShift)) << 16) |
                    (group_near(acq, gd_l, gm) ? 0x80000000u : 0u);
         }
-        // software pipeline: records of the next group are loaded while the
-        // current one is evaluated
-        int64_t g_next = __shfl_sync(0xffffffffu, g_l, 0);
-        BallA An = ra[g_next * kWarp + lane];
-        BallB Bn = rb[g_next * kWarp + lane];
-        for (int k = 0; k < nb; ++k) {
-          const GroupDet gd = shfl_gd_fast(gd_l, k);
-          const BallA A = An;
-          const BallB B = Bn;
-          if (k + 1 < nb) {
-            g_next = __shfl_sync(0xffffffffu, g_l, k + 1);
-            An = ra[g_next * kWarp + lane];
-            Bn = rb[g_next * kWarp + lane];
+        // two groups per trip: their setups (latency-bound chains) are
+        // computed side by side, then both walk in order; records of the
+        // next two groups are loaded while the current ones are evaluated
+        int64_t ga = __shfl_sync(0xffffffffu, g_l, 0), gb = __shfl_sync(0xffffffffu, g_l, min(1, nb - 1));
+        BallA Aa = ra[ga * kWarp + lane], Ab = ra[gb * kWarp + lane];
+        BallB Ba = rb[ga * kWarp + lane], Bb = rb[gb * kWarp + lane];
+        for (int k = 0; k < nb; k += 2) {
+          const bool two = k + 1 < nb;
+          const int kb = two ? k + 1 : k;
+          const GroupDet gda = shfl_gd_fast(gd_l, k), gdb = shfl_gd_fast(gd_l, kb);
+          const unsigned worda = __shfl_sync(0xffffffffu, word_l, k), wordb = __shfl_sync(0xffffffffu, word_l, kb);
+          const BallA A0 = Aa, A1 = Ab;
+          const BallB B0 = Ba, B1 = Bb;
+          if (k + 2 < nb) {
+            ga = __shfl_sync(0xffffffffu, g_l, k + 2);
+            gb = __shfl_sync(0xffffffffu, g_l, min(k + 3, nb - 1));
+            Aa = ra[ga * kWarp + lane];
+            Ab = ra[gb * kWarp + lane];
+            Ba = rb[ga * kWarp + lane];
+            Bb = rb[gb * kWarp + lane];
           }
-          const unsigned word = __shfl_sync(0xffffffffu, word_l, k);
-          const int blo = (int)(word & 0xFFFFu) << kBinShift;
-          const int ghi = blo + (int)((word >> 16) & 0x7FFFu);
-          const int near = (int)(word >> 31);
-          // lazy flush: rows below blo are complete; only those whose slots
-          // this group's rows [blo, ghi + 7] reuse must go now -- flushed in
-          // batches of >= 32 rows when possible
-          const int need = ghi + 8 - kTile;
-          if (need > fp) {
-            const int upto = min(blo, max(need, fp + kWarp));
-            flush_rows(tile, lane, fp, min(upto, touched + 1), sink);
-            fp = upto;
+          const int bloa = (int)(worda & 0xFFFFu) << kBinShift, blob = (int)(wordb & 0xFFFFu) << kBinShift;
+          const int ghia = bloa + (int)((worda >> 16) & 0x7FFFu), ghib = blob + (int)((wordb >> 16) & 0x7FFFu);
+          unsigned long long ops_b = 0;
+          const PairSetup pa = pair_setup<DIR>(acq, gda, dd, A0, B0, my_ops, bloa);
+          const PairSetup pb = pair_setup<DIR>(acq, gdb, dd, A1, B1, ops_b, blob);
+          if (two) my_ops += ops_b;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (h == 1 && !two) break;
+            const int blo = h ? blob : bloa, ghi = h ? ghib : ghia;
+            // lazy flush: rows below blo are complete; only those whose
+            // slots this group's rows [blo, ghi + 7] reuse must go now --
+            // flushed in batches of >= 32 rows when possible
+            const int need = ghi + 8 - kTile;
+            if (need > fp) {
+              const int upto = min(blo, max(need, fp + kWarp));
+              flush_rows(tile, lane, fp, min(upto, touched + 1), sink);
+              fp = upto;
+            }
+            touched = max(touched, ghi + 7);
+            pair_walk<MASK>(tile, lane, acq, h ? pb : pa, (int)((h ? wordb : worda) >> 31), my_ops, blo);
+            __syncwarp();
           }
-          touched = max(touched, ghi + 7);
-          evaluate_pair_uniform<DIR, MASK>(tile, lane, acq, gd, dd, A, B, near, my_ops, blo);
-          __syncwarp();
         }
       }
       if (s_begin < s_end) flush_rows(tile, lane, fp, min(n_out, touched + 1), sink);
