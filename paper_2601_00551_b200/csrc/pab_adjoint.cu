@@ -22,9 +22,6 @@
 
 namespace pab {
 
-#ifndef PAB_ADJ_TMA
-#define PAB_ADJ_TMA 0   // residual staging by TMA bulk copy (1) or 16-B cp.async (0)
-#endif
 constexpr int kSeg = 256;   // staged residual samples per warp and buffer
 constexpr int kPad = 96;    // zero padding after the staged samples (uniform-walk overrun)
 
@@ -37,13 +34,6 @@ __device__ __forceinline__ void cp_async16(float* smem_dst, const float* gsrc) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gsrc));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
-__device__ __forceinline__ void mbar_wait(unsigned addr, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
-          addr),
-      "r"(parity)
-      : "memory");
-}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 struct Moments {
@@ -234,20 +224,11 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
                Acq acq, const float* __restrict__ res, float res_sign, int det_per_chunk,
                double* __restrict__ gpart, int64_t n_pad, unsigned long long* __restrict__ ops_total,
                int* __restrict__ status) {
-  __shared__ __align__(16) float seg_all[8][2][kSeg + kPad + 4];
-  __shared__ __align__(8) unsigned long long mbar[8][2];   // per warp and buffer: TMA completion
+  __shared__ __align__(16) float seg_all[8][4][kSeg + kPad + 4];
   const bool vec16 = (acq.n_out & 3) == 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
   if (g >= n_groups) return;
-  unsigned phase = 0;   // bit b: parity of buffer b's next mbarrier phase
-  if (lane == 0) {
-    for (int b = 0; b < 2; ++b)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&mbar[warp][b]))
-                   : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
   const int q = blockIdx.y;
   const int j0 = q * det_per_chunk;
   const int j1 = min(n_det, j0 + det_per_chunk);
@@ -290,8 +271,7 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       if (DIR != kDirNone) ddl = load_detdir(det_aux, jl);
     }
     // stage res[j][lo .. hi] (lo a multiple of 4) + kPad zeros into buffer
-    // `buf`: one TMA bulk copy (16-B aligned rows) completing on the buffer's
-    // mbarrier, or 4-B cp.async when rows are not 16-B aligned
+    // `buf`: 16-B cp.async (16-B aligned rows) or 4-B cp.async
     auto stage_seg = [&](int jj, int lo, int hi, int fl, int buf) {
       if (!(fl & kFlagUniform)) return;
       const float* src = res + (size_t)(jb + jj) * n_out + lo;
@@ -299,24 +279,10 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       const int len = hi - lo + 1;
       if (vec16) {
         const int len4 = (len + 3) >> 2;   // the last vector may carry up to 3 finite extra samples
-#if PAB_ADJ_TMA
-        if (lane == 0) {
-          const unsigned mb = (unsigned)__cvta_generic_to_shared(&mbar[warp][buf]);
-          const unsigned bytes = 16u * (unsigned)len4;
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                  (unsigned)__cvta_generic_to_shared(dst)),
-              "l"(src), "r"(bytes), "r"(mb)
-              : "memory");
-        }
-#else
         static_assert(kSeg <= 8 * kWarp, "two 16-B vectors per lane cover the segment");
         if (lane < len4) cp_async16(dst + 4 * lane, src + 4 * lane);
         if (lane + kWarp < len4) cp_async16(dst + 4 * (lane + kWarp), src + 4 * (lane + kWarp));
         cp_async_commit();
-#endif
         float4* z = reinterpret_cast<float4*>(dst + 4 * len4);
         if (lane < kPad / 4) z[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
       } else {
@@ -325,88 +291,13 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
         cp_async_commit();
       }
     };
-    auto wait_seg = [&](int fl, int buf) {
-      if (!(fl & kFlagUniform)) return;
-#if PAB_ADJ_TMA
-      if (vec16) {
-        mbar_wait((unsigned)__cvta_generic_to_shared(&mbar[warp][buf]), (phase >> buf) & 1u);
-        phase ^= 1u << buf;
-        return;
-      }
-#endif
-      cp_async_wait_all();
+    auto wait_seg = [&](int fl) {
+      if (fl & kFlagUniform) cp_async_wait_all();
     };
     float gb[5] = {0.f, 0.f, 0.f, 0.f, 0.f};   // FP32 batch sums of the pair terms
-    int nlo = __shfl_sync(0xffffffffu, rlo, 0);
-    int nhi = __shfl_sync(0xffffffffu, rhi, 0);
-    int nfl = __shfl_sync(0xffffffffu, rfl, 0);
-    stage_seg(0, nlo, nhi, nfl, 0);
-    for (int jj = 0; jj < nd; ++jj) {
-      const int buf = jj & 1;
-      const int lo = nlo, hi = nhi, fl = nfl;
-      GroupDet gd = shfl_gd_fast(gdl, jj);
-      const DetDir dd = shfl_detdir<DIR>(ddl, jj);
-      wait_seg(fl, buf);
-      __syncwarp();   // every lane is past detector jj-1: its buffer may be refilled
-      if (jj + 1 < nd) {
-        nlo = __shfl_sync(0xffffffffu, rlo, jj + 1);
-        nhi = __shfl_sync(0xffffffffu, rhi, jj + 1);
-        nfl = __shfl_sync(0xffffffffu, rfl, jj + 1);
-        stage_seg(jj + 1, nlo, nhi, nfl, buf ^ 1);
-      }
-      if (lo > hi) continue;
 
-      Moments M;
-      PairGeom pg;
-      if (fl & kFlagUniform) {
-        pg = pair_geom_fast(gd, A, B, acq);
-        int jlo, jhi;
-        pair_window_cover(pg.kc, pg.phi, rho, acq, &jlo, &jhi);
-        const bool empty = !live || jlo > jhi;
-        const int J0 = empty ? lo : max(jlo & ~3, lo);
-        const int Lmax = __reduce_max_sync(0xffffffffu, empty ? 0 : jhi - J0 + 1);
-        if (ops_total && live) {   // exact sample count for the op counter
-          int elo, ehi;
-          pair_window(pg.kc, pg.phi, rho, acq, &elo, &ehi);
-          my_ops += (unsigned long long)max(ehi - elo + 1, 0);
-        }
-        moments_uniform<STAGE, MASK>(seg_all[warp][buf] + (J0 - lo), (Lmax + 3) & ~3, (float)(J0 * f - pg.kc),
-                                     W, pg.phi * sc, empty ? -1.0f : qmax, M);
-        if (!MASK && empty) M = {0.f, 0.f, 0.f, 0.f};
-      } else {
-        // near field / detector close to the group / wide windows: per-lane
-        // walks over the global residual row, FP64 geometry when slow
-        gd.slow = (fl & kFlagSlow) ? 1 : 0;
-        double px = 0.0, py = 0.0, pz = 0.0;
-        if (gd.slow) {
-          px = det_pos[3 * (jb + jj)];
-          py = det_pos[3 * (jb + jj) + 1];
-          pz = det_pos[3 * (jb + jj) + 2];
-        }
-        pg = pair_geom(gd, gm, px, py, pz, A, B, acq);
-        coinc |= pg.coincident;
-        int jlo, jhi;
-        pair_window(pg.kc, pg.phi, rho, acq, &jlo, &jhi);
-        if (!live) { jlo = 1; jhi = 0; }
-        int nlo = 1, nhi = 0, nkc = 0;
-        float nphi = 0.0f;
-        if ((fl & kFlagNear) && live) pair_near_window(pg.d, rho, acq, &nlo, &nhi, &nkc, &nphi);
-        my_ops += (unsigned long long)(max(jhi - jlo + 1, 0) + max(nhi - nlo + 1, 0));
-        M = {0.f, 0.f, 0.f, 0.f};
-        const float* row = res + (size_t)(jb + jj) * n_out;
-        moments_run<STAGE>(row, jlo, jhi - jlo + 1, (float)(jlo * f - pg.kc), fs, sc, pg.phi * sc, M);
-        if (nlo <= nhi) {   // u+ = -kappa y: odd moments flip sign
-          Moments N = {0.f, 0.f, 0.f, 0.f};
-          moments_run<STAGE>(row, nlo, nhi - nlo + 1, (float)(nlo * f - nkc), fs, sc, nphi * sc, N);
-          M.T0 += N.T0;
-          M.T1 -= N.T1;
-          M.T2 += N.T2;
-          M.T3 -= N.T3;
-        }
-      }
-      __syncwarp();
-
-      // per-pair gradient terms (reference radiator.py:275-286 in y units)
+    // per-pair gradient terms (reference radiator.py:275-286 in y units)
+    auto epilogue = [&](const PairGeom& pg, const Moments& M, const DetDir& dd) {
       float dDdr[3] = {0.f, 0.f, 0.f}, dDda0 = 0.f;
       const float id = pg.id;
       const float D = dir_weight<DIR, STAGE == kStageFine || DIR == kDirElement>(
@@ -431,6 +322,128 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
         gb[2] += gx;
         gb[3] += gy;
         gb[4] += gz;
+      }
+    };
+    // uniform path, part 1: geometry, covering window, block count
+    struct USetup {
+      PairGeom pg;
+      int J0, L;
+      bool empty;
+    };
+    auto usetup = [&](const GroupDet& gd, int lo) {
+      USetup u;
+      u.pg = pair_geom_fast(gd, A, B, acq);
+      int jlo, jhi;
+      pair_window_cover(u.pg.kc, u.pg.phi, rho, acq, &jlo, &jhi);
+      u.empty = !live || jlo > jhi;
+      u.J0 = u.empty ? lo : max(jlo & ~3, lo);
+      u.L = __reduce_max_sync(0xffffffffu, u.empty ? 0 : jhi - u.J0 + 1);
+      if (ops_total && live) {   // exact sample count for the op counter
+        int elo, ehi;
+        pair_window(u.pg.kc, u.pg.phi, rho, acq, &elo, &ehi);
+        my_ops += (unsigned long long)max(ehi - elo + 1, 0);
+      }
+      return u;
+    };
+    // uniform path, part 2: the moment walk over the staged segment
+    auto uwalk = [&](const USetup& u, int lo, int buf) {
+      Moments M;
+      moments_uniform<STAGE, MASK>(seg_all[warp][buf] + (u.J0 - lo), (u.L + 3) & ~3, (float)(u.J0 * f - u.pg.kc),
+                                   W, u.pg.phi * sc, u.empty ? -1.0f : qmax, M);
+      if (!MASK && u.empty) M = {0.f, 0.f, 0.f, 0.f};
+      return M;
+    };
+    // near field / detector close to the group / wide windows: per-lane
+    // walks over the global residual row, FP64 geometry when slow
+    auto fallback = [&](GroupDet gd, int fl, int jj, PairGeom& pg) {
+      gd.slow = (fl & kFlagSlow) ? 1 : 0;
+      double px = 0.0, py = 0.0, pz = 0.0;
+      if (gd.slow) {
+        px = det_pos[3 * (jb + jj)];
+        py = det_pos[3 * (jb + jj) + 1];
+        pz = det_pos[3 * (jb + jj) + 2];
+      }
+      pg = pair_geom(gd, gm, px, py, pz, A, B, acq);
+      coinc |= pg.coincident;
+      int jlo, jhi;
+      pair_window(pg.kc, pg.phi, rho, acq, &jlo, &jhi);
+      if (!live) { jlo = 1; jhi = 0; }
+      int nlo = 1, nhi = 0, nkc = 0;
+      float nphi = 0.0f;
+      if ((fl & kFlagNear) && live) pair_near_window(pg.d, rho, acq, &nlo, &nhi, &nkc, &nphi);
+      my_ops += (unsigned long long)(max(jhi - jlo + 1, 0) + max(nhi - nlo + 1, 0));
+      Moments M = {0.f, 0.f, 0.f, 0.f};
+      const float* row = res + (size_t)(jb + jj) * n_out;
+      moments_run<STAGE>(row, jlo, jhi - jlo + 1, (float)(jlo * f - pg.kc), fs, sc, pg.phi * sc, M);
+      if (nlo <= nhi) {   // u+ = -kappa y: odd moments flip sign
+        Moments N = {0.f, 0.f, 0.f, 0.f};
+        moments_run<STAGE>(row, nlo, nhi - nlo + 1, (float)(nlo * f - nkc), fs, sc, nphi * sc, N);
+        M.T0 += N.T0;
+        M.T1 -= N.T1;
+        M.T2 += N.T2;
+        M.T3 -= N.T3;
+      }
+      return M;
+    };
+    auto one = [&](int jj, int lo, int hi, int fl, int buf, const GroupDet& gd, const DetDir& dd) {
+      if (lo > hi) return;
+      PairGeom pg;
+      Moments M;
+      if (fl & kFlagUniform) {
+        const USetup u = usetup(gd, lo);
+        M = uwalk(u, lo, buf);
+        pg = u.pg;
+      } else {
+        M = fallback(gd, fl, jj, pg);
+      }
+      __syncwarp();
+      epilogue(pg, M, dd);
+    };
+
+    // detectors in pairs, four staging buffers per warp: while a pair is
+    // processed the next pair's segments are in flight; the two pairs'
+    // setups (latency-bound chains) and gradient epilogues are computed side
+    // by side
+    int loA = __shfl_sync(0xffffffffu, rlo, 0), hiA = __shfl_sync(0xffffffffu, rhi, 0);
+    int flA = __shfl_sync(0xffffffffu, rfl, 0);
+    int loB = __shfl_sync(0xffffffffu, rlo, 1), hiB = __shfl_sync(0xffffffffu, rhi, 1);
+    int flB = nd > 1 ? __shfl_sync(0xffffffffu, rfl, 1) : 0;
+    stage_seg(0, loA, hiA, flA, 0);
+    if (nd > 1) stage_seg(1, loB, hiB, flB, 1);
+    for (int jj = 0; jj < nd; jj += 2) {
+      const bool two = jj + 1 < nd;
+      const int bA = jj & 3, bB = bA + 1;
+      const int la = loA, ha = hiA, fa = flA, lb = loB, hb = hiB, fb = two ? flB : 0;
+      const GroupDet gdA = shfl_gd_fast(gdl, jj), gdB = shfl_gd_fast(gdl, two ? jj + 1 : jj);
+      const DetDir ddA = shfl_detdir<DIR>(ddl, jj), ddB = shfl_detdir<DIR>(ddl, two ? jj + 1 : jj);
+      wait_seg(fa | fb);
+      __syncwarp();   // every lane is past the previous pair: its buffers may be refilled
+      if (jj + 2 < nd) {
+        loA = __shfl_sync(0xffffffffu, rlo, jj + 2);
+        hiA = __shfl_sync(0xffffffffu, rhi, jj + 2);
+        flA = __shfl_sync(0xffffffffu, rfl, jj + 2);
+        stage_seg(jj + 2, loA, hiA, flA, bA ^ 2);
+        if (jj + 3 < nd) {
+          loB = __shfl_sync(0xffffffffu, rlo, jj + 3);
+          hiB = __shfl_sync(0xffffffffu, rhi, jj + 3);
+          flB = __shfl_sync(0xffffffffu, rfl, jj + 3);
+          stage_seg(jj + 3, loB, hiB, flB, bB ^ 2);
+        } else {
+          flB = 0;
+        }
+      }
+      const bool uA = (fa & kFlagUniform) && la <= ha, uB = two && (fb & kFlagUniform) && lb <= hb;
+      if (uA && uB) {
+        const USetup sA = usetup(gdA, la);
+        const USetup sB = usetup(gdB, lb);
+        const Moments MA = uwalk(sA, la, bA);
+        const Moments MB = uwalk(sB, lb, bB);
+        __syncwarp();
+        epilogue(sA.pg, MA, ddA);
+        epilogue(sB.pg, MB, ddB);
+      } else {
+        one(jj, la, ha, fa, bA, gdA, ddA);
+        if (two) one(jj + 1, lb, hb, fb, bB, gdB, ddB);
       }
     }
     __syncwarp();
