@@ -119,23 +119,22 @@ __device__ __forceinline__ float2 gauss2(float2 q, float qmax) {
   return make_float2(ex2(-q.x), ex2(-q.y));
 }
 
+// The amplitude rides in the exponent: Ak y 2^(-y^2) = sgn(Ak) y
+// 2^(-(y^2 - log2|Ak|)), with sgn(Ak) folded into the y coefficients, so a
+// sample costs y (FFMA2 half), y^2 - log2|Ak| (FFMA2 half), ex2 and the
+// accumulate (FFMA2 half).  Ak = 0 gives log2 = -inf and an exact +0 term.
 struct Walk {
-  float2 nsc2, c0, c1, c2, c3, Ak2;
-  float qmax;
+  float2 nsc2, c0, c1, c2, c3;
+  float2 nla2;   // (-log2|Ak|, -log2|Ak|)
+  float qmax;    // truncation bound on y^2 - log2|Ak| (MASK)
 };
 
-template <bool MASK, bool POLY = false>
+template <bool MASK>
 __device__ __forceinline__ float2 rmw_pair(float2 o, float2 m2, float2 c, const Walk& w) {
   const float2 y = __ffma2_rn(m2, w.nsc2, c);
-  const float2 q = __fmul2_rn(y, y);
-  float2 g;
-  if (POLY) {
-    g = exp2_neg_poly2(q);
-    if (MASK) g = make_float2(q.x <= w.qmax ? g.x : 0.0f, q.y <= w.qmax ? g.y : 0.0f);
-  } else {
-    g = gauss2<MASK>(q, w.qmax);
-  }
-  return __ffma2_rn(w.Ak2, __fmul2_rn(y, g), o);
+  const float2 e = __ffma2_rn(y, y, w.nla2);
+  const float2 g = gauss2<MASK>(e, w.qmax);
+  return __ffma2_rn(y, g, o);
 }
 
 __device__ __forceinline__ float4 rmw4(float4 o, float2 m2, float2 ca, float2 cb, const Walk& w,
@@ -153,14 +152,17 @@ __device__ __forceinline__ void rmw_uniform(float* tile, int lane, int J0, int L
                                             float sc, float ps, float Ak, float qmax) {
   constexpr int K = PAB_FWD_UNROLL;
   Walk w;
-  w.nsc2 = make_float2(-sc, -sc);
-  w.Ak2 = make_float2(Ak, Ak);
-  const float dl = fs * -sc, dl2 = 2.0f * dl;   // y step per sample / per sample pair
-  w.c0 = make_float2(ps, ps + dl);
+  const float sg = Ak < 0.0f ? -1.0f : 1.0f;   // sgn(Ak) folded into y
+  const float nla = -__log2f(fabsf(Ak));       // +inf for Ak = 0
+  w.nsc2 = make_float2(-sc * sg, -sc * sg);
+  const float dl = fs * -sc * sg, dl2 = 2.0f * dl;   // y step per sample / per sample pair
+  const float pss = ps * sg;
+  w.c0 = make_float2(pss, pss + dl);
   w.c1 = __fadd2_rn(w.c0, make_float2(dl2, dl2));
   w.c2 = __fadd2_rn(w.c1, make_float2(dl2, dl2));
   w.c3 = __fadd2_rn(w.c2, make_float2(dl2, dl2));
-  w.qmax = qmax;
+  w.nla2 = make_float2(nla, nla);
+  w.qmax = qmax + nla;
   float4* const T = reinterpret_cast<float4*>(tile) + lane;   // quad q of this lane: T[q * 32]
   const int dump = kTile / 4;                                   // dump block = quads kTile/4, kTile/4 + 1
   const float step = 8.0f * fs;
