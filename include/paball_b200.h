@@ -144,6 +144,23 @@ int pab_split_children(const double* pos, const double* p0, const double* a0, co
 int pab_duplicate(const double* pos, const double* p0, const double* a0, const double* unit, int64_t m,
                   double* out_pos, double* out_p0, double* out_a0, void* stream);
 
+/* ---- voxelisation ------------------------------------
+ * Replaces: render.voxelize (render.py:55-93).  order[r] = index of the r-th
+ * ball in the canonical lexicographic (x, y, z, p0, a0) order (render.py:67-70).
+ * Three passes: per-ball clipped voxel box and 8^3-brick count; (brick << 32 |
+ * rank) keys at exclusive-scan offsets (caller sorts them ascending); per-brick
+ * gather writing vol[nx][ny][nz] (FP64, every voxel written). */
+int64_t pab_vox_brick_count(int nx, int ny, int nz);
+int pab_vox_count(const double* pos, const double* p0, const double* a0, const int64_t* order, int64_t n, int nx,
+                  int ny, int nz, double spacing, double ox, double oy, double oz, double support,
+                  int* box /*[n][6]*/, int64_t* count /*[n]*/, void* stream);
+int pab_vox_emit(const int* box, const int64_t* offset, int64_t n, int nx, int ny, int nz, int64_t* keys,
+                 void* stream);
+int pab_vox_gather(const double* pos, const double* p0, const double* a0, const int64_t* order, const int* box,
+                   const int64_t* sorted_keys, int64_t total, int nx, int ny, int nz, double spacing, double ox,
+                   double oy, double oz, double support, int64_t* start /*[bricks]*/, int64_t* end /*[bricks]*/,
+                   double* vol, void* stream);
+
 #ifdef __cplusplus
 }
 #endif
