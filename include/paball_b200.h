@@ -144,6 +144,13 @@ int pab_split_children(const double* pos, const double* p0, const double* a0, co
 int pab_duplicate(const double* pos, const double* p0, const double* a0, const double* unit, int64_t m,
                   double* out_pos, double* out_p0, double* out_a0, void* stream);
 
+/* ---- positivity refinement ----------------------------
+ * Replaces: optimizer.softplus (optimizer.py:507-510) and the chain-rule
+ * factor d_a0 * sigmoid(a0_free) of positivity_refine (optimizer.py:526-533,
+ * :563); FP64, the reference's expression trees. */
+int pab_softplus_f64(const double* x, int64_t n, double* y, void* stream);
+int pab_mul_sigmoid_f64(const double* g, const double* x, int64_t n, double* out, void* stream);
+
 /* ---- voxelisation ------------------------------------
  * Replaces: render.voxelize (render.py:55-93).  order[r] = index of the r-th
  * ball in the canonical lexicographic (x, y, z, p0, a0) order (render.py:67-70).

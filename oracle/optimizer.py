@@ -175,3 +175,58 @@ def run_hierarchical(prob, state, real, levels, th, lr, duplication_period=200,
                 if abs(past - L) < PLATEAU_REL * max(abs(past), 1e-300):
                     break
     return state, losses_all, counts
+
+
+# ---------------------------------------------------------------------------
+# Positivity-constrained refinement (optimizer.py:507-573)
+# ---------------------------------------------------------------------------
+
+
+def softplus(x):
+    """log(1 + e^x), overflow-safe split form (optimizer.py:507-510)."""
+    x = np.asarray(x, dtype=np.float64)
+    return np.log1p(np.exp(-np.abs(x))) + np.maximum(x, 0.0)
+
+
+def inv_softplus(y):
+    """Preimage of softplus for y > 0 (optimizer.py:513-523)."""
+    y = np.asarray(y, dtype=np.float64)
+    if np.any(y <= 0.0):
+        raise ValueError("inv_softplus requires strictly positive input")
+    small = y < 0.7
+    out = np.empty_like(y)
+    out[small] = np.log(np.expm1(y[small]))
+    out[~small] = y[~small] + np.log1p(-np.exp(-y[~small]))
+    return out
+
+
+def sigmoid(x):
+    """Logistic function, split by sign (optimizer.py:526-533)."""
+    x = np.asarray(x, dtype=np.float64)
+    pos = x >= 0.0
+    out = np.empty_like(x)
+    out[pos] = 1.0 / (1.0 + np.exp(-x[pos]))
+    ex = np.exp(x[~pos])
+    out[~pos] = ex / (1.0 + ex)
+    return out
+
+
+def positivity_refine(prob, state, real, iters, lr):
+    """a0 = softplus(a0_free), fresh moments, fine backward at f = 1, Adam on
+    p0, a0_free (chain rule through sigmoid) and positions; no a0 floor
+    (optimizer.py:536-573).  Returns (pos, p0, a0, a0_free)."""
+    pos, p0, a0 = state["pos"].copy(), state["p0"].copy(), state["a0"].copy()
+    if len(p0) and np.any(a0 <= 0.0):
+        raise ValueError("positivity refinement requires a0 > 0 at entry")
+    free = inv_softplus(a0) if len(p0) else np.empty(0)
+    ref = new_state(pos, p0, a0, seed=state["seed"])
+    for _ in range(int(iters)):
+        a0 = softplus(free)
+        L, (gp0, ga0, gpos) = prob.backward(pos, p0, a0, real, 1, "fine")
+        if not math.isfinite(L):
+            raise FloatingPointError(f"non-finite loss during refinement: {L}")
+        ref["t"] += 1
+        p0 = adam(ref, "p0", p0, gp0, lr[0])
+        free = adam(ref, "a0", free, ga0 * sigmoid(free), lr[1])
+        pos = adam(ref, "position", pos, gpos, lr[2])
+    return pos, p0, softplus(free), free.copy()

@@ -44,6 +44,8 @@ _SIGS = {
     "pab_density_take_ties": ([_vp, _vp, _vp, _i, _i64, _vp, _vp], _i),
     "pab_split_children": ([_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp], _i),
     "pab_duplicate": ([_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp], _i),
+    "pab_softplus_f64": ([_vp, _i64, _vp, _vp], _i),
+    "pab_mul_sigmoid_f64": ([_vp, _vp, _i64, _vp, _vp], _i),
     "pab_vox_brick_count": ([_i, _i, _i], _i64),
     "pab_vox_count": ([_vp, _vp, _vp, _vp, _i64, _i, _i, _i, _d, _d, _d, _d, _d, _vp, _vp, _vp], _i),
     "pab_vox_emit": ([_vp, _vp, _i64, _i, _i, _i, _vp, _vp], _i),

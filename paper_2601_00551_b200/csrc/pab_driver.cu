@@ -33,6 +33,30 @@ __global__ void adam_kernel(double* __restrict__ param, const double* __restrict
   param[i] = out;
 }
 
+// softplus(x) = log1p(exp(-|x|)) + max(x, 0)   (optimizer.py:507-510, same op tree)
+__global__ void softplus_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ y) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double v = x[i];
+  y[i] = __dadd_rn(log1p(exp(-fabs(v))), v > 0.0 ? v : 0.0);
+}
+
+// out = g * sigmoid(x), sigmoid split by sign as optimizer.py:526-533
+__global__ void mul_sigmoid_kernel(const double* __restrict__ g, const double* __restrict__ x, int64_t n,
+                                   double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double v = x[i];
+  double s;
+  if (v >= 0.0) {
+    s = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-v)));
+  } else {
+    const double e = exp(v);
+    s = __ddiv_rn(e, __dadd_rn(1.0, e));
+  }
+  out[i] = __dmul_rn(g[i], s);
+}
+
 // flags: keep = (x < 0) if strict else (x <= 0)  [mode 0/1], x != 0 [mode 2],
 // x > 0 [mode 3], x == 0 [mode 4]
 __device__ __forceinline__ bool keep_pred(double x, int mode) {
@@ -160,6 +184,20 @@ int pab_adam(double* param, const double* grad, double* m, double* v, int64_t co
   if (!param || !grad || !m || !v) return 1;
   adam_kernel<<<(unsigned)((count + 255) / 256), 256, 0, (cudaStream_t)stream>>>(param, grad, m, v, count, lr,
                                                                                 bc1, bc2, floor_value, use_floor);
+  return cudaGetLastError() == cudaSuccess ? 0 : 4;
+}
+
+int pab_softplus_f64(const double* x, int64_t n, double* y, void* stream) {
+  if (n <= 0) return 0;
+  if (!x || !y) return 1;
+  softplus_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(x, n, y);
+  return cudaGetLastError() == cudaSuccess ? 0 : 4;
+}
+
+int pab_mul_sigmoid_f64(const double* g, const double* x, int64_t n, double* out, void* stream) {
+  if (n <= 0) return 0;
+  if (!g || !x || !out) return 1;
+  mul_sigmoid_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(g, x, n, out);
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 

@@ -609,3 +609,94 @@ def run_hierarchical(init: PointCloud, ctx, real, schedule: Schedule, thresholds
                 if abs(past - loss_value) < _PLATEAU_REL * max(abs(past), 1e-300):
                     break
     return state.cloud, trace
+
+
+# ---------------------------------------------------------------------------
+# Positivity-constrained refinement (optimizer.py:507-573), SURVEY §8f rank 3
+# ---------------------------------------------------------------------------
+
+
+def softplus(x: np.ndarray) -> np.ndarray:
+    """log(1 + exp(x)) with the overflow-safe split form; always > 0
+    (optimizer.py:507-510).  Host helper of the API; the refinement loop
+    evaluates it on the device (``pab_softplus_f64``)."""
+    x = np.asarray(x, dtype=np.float64)
+    return np.log1p(np.exp(-np.abs(x))) + np.maximum(x, 0.0)
+
+
+def inv_softplus(y: np.ndarray) -> np.ndarray:
+    """Preimage of softplus for y > 0, accurate over many decades
+    (optimizer.py:513-523)."""
+    y = np.asarray(y, dtype=np.float64)
+    if np.any(y <= 0.0):
+        raise ValueError("inv_softplus requires strictly positive input")
+    small = y < 0.7
+    out = np.empty_like(y)
+    out[small] = np.log(np.expm1(y[small]))
+    big = ~small
+    out[big] = y[big] + np.log1p(-np.exp(-y[big]))
+    return out
+
+
+def sigmoid(x: np.ndarray) -> np.ndarray:
+    """Logistic function split by sign (optimizer.py:526-533)."""
+    x = np.asarray(x, dtype=np.float64)
+    pos = x >= 0.0
+    out = np.empty_like(x)
+    out[pos] = 1.0 / (1.0 + np.exp(-x[pos]))
+    ex = np.exp(x[~pos])
+    out[~pos] = ex / (1.0 + ex)
+    return out
+
+
+def positivity_refine(state: OptimState, ctx, real, iters: int) -> PointCloud:
+    """Final fit with a0 = softplus(a0_free), density control frozen
+    (optimizer.py:536-573): fresh moments, fine backward at the native rate,
+    Adam on p0, a0_free (gradient d_a0 * sigmoid(a0_free)) and positions, no
+    a0 floor.  The whole loop stays on the device; the entry preimage is
+    taken on the host as in the reference."""
+    cloud = state.cloud
+    if len(cloud) and np.any(cloud.a0 <= 0.0):
+        raise ValueError("positivity refinement requires a0 > 0 at entry")
+    free_h = inv_softplus(cloud.a0) if len(cloud) else np.empty(0)
+    refine = create_state(cloud, lr=state.lr, seed=state.seed)
+    dc = refine._dc
+    n = dc.n
+    if n == 0 or int(iters) <= 0:
+        out = PointCloud(cloud.positions.copy(), cloud.p0.copy(),
+                         softplus(free_h) if n else cloud.a0.copy(), free_h.copy(), cloud.generation)
+        state.cloud = out
+        return out
+    free = torch.from_numpy(np.ascontiguousarray(free_h)).to(dc.dev)
+    g_free = torch.empty_like(free)
+    det = R.device_detectors(ctx)
+    acq = R._acq(ctx, 1)
+    real_local = R.device_supervision(real.data, det)
+    n_total = det.n_total * acq.n_out
+    s = E._stream()
+    for _ in range(int(iters)):
+        call("pab_softplus_f64", ptr(free), n, ptr(dc.a0), s)
+        dc.invalidate()
+        counters = E.PassCounters(dc.dev)
+        res, loss_rows = E.forward_rows(dc, det, acq, counters, real_local=real_local)
+        d_p0, d_a0, d_pos = E.adjoint_grads(dc, det, acq, res, 1.0, 2, 2.0 / n_total, counters)
+        loss_sum = float(loss_rows.sum().item())
+        if det.shard.world > 1:
+            loss_sum = E.allreduce_scalar(loss_sum, dc.dev)
+        loss_value = loss_sum / n_total
+        if int(counters.status.item()) & E.STATUS_COINCIDENT:
+            raise SimulationError("ball coincident with a sensor (zero source-sensor distance)")
+        if not math.isfinite(loss_value):
+            raise OptimizationError(f"non-finite loss during refinement: {loss_value}")
+        R._add_ops(int(counters.ops.item()))
+        refine.step_count += 1
+        t = refine.step_count
+        _adam_(dc.p0, d_p0, refine._m["p0"], refine._v["p0"], refine.lr.p0, t)
+        call("pab_mul_sigmoid_f64", ptr(d_a0), ptr(free), n, ptr(g_free), s)
+        _adam_(free, g_free, refine._m["a0"], refine._v["a0"], refine.lr.a0, t)
+        _adam_(dc.pos, d_pos, refine._m["position"], refine._v["position"], refine.lr.position, t)
+    call("pab_softplus_f64", ptr(free), n, ptr(dc.a0), s)
+    out = PointCloud(dc.pos.cpu().numpy(), dc.p0.cpu().numpy(), dc.a0.cpu().numpy(), free.cpu().numpy(),
+                     cloud.generation)
+    state.cloud = out
+    return out

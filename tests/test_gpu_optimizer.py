@@ -243,3 +243,59 @@ def test_toy_five_adam_steps_match_reference(P):
     init = sc.init.subset(keep)
     assert rel_l2(c.positions - init.positions, g["final_pos"] - init.positions) < 1e-2
     assert rel_l2(c.p0, g["final_p0"]) < 1e-4
+
+
+class TestPositivityRefine:
+    """positivity_refine (optimizer.py:536-573) on the device against the
+    reference run (tests/golden/refine.npz) and the reference's own tests
+    (test_optimizer.py:379-400)."""
+
+    def _start(self, P, g):
+        ctx, truth, real, _ = small_instance(P)
+        np.testing.assert_array_equal(truth.positions, g["true_pos"])
+        cloud = truth.copy()
+        cloud.p0 = cloud.p0 * 0.8
+        cloud.a0 = cloud.a0 * 1.3
+        return ctx, cloud, real
+
+    @pytest.mark.parametrize("iters", [3, 40])
+    def test_matches_reference(self, P, iters):
+        g = golden("refine.npz")
+        ctx, cloud, real = self._start(P, g)
+        np.testing.assert_allclose(real.data, g["real"], rtol=0, atol=1e-4 * np.abs(g["real"]).max())
+        state = P.create_state(cloud, lr=P.LearningRates.from_spacing(4e-4), seed=9)
+        out = P.positivity_refine(state, ctx, P.SignalSet(ctx.grid, g["real"]), iters)
+        # FP32 per-sample gradients (rel. 1e-5) through Adam's normalised steps
+        np.testing.assert_allclose(out.p0, g[f"it{iters}_p0"], rtol=2e-4)
+        np.testing.assert_allclose(out.a0, g[f"it{iters}_a0"], rtol=2e-4)
+        np.testing.assert_allclose(out.positions, g[f"it{iters}_pos"], rtol=0, atol=0.02 * iters * 0.05 * 4e-4)
+        np.testing.assert_allclose(out.a0_free, g[f"it{iters}_a0_free"], rtol=2e-3, atol=1e-6)
+        assert np.all(out.a0 > 0.0) and np.isfinite(out.a0_free).all()
+        L1 = P.loss(P.simulate_signals(out, ctx), P.SignalSet(ctx.grid, g["real"]))
+        assert abs(L1 - float(g[f"it{iters}_L1"])) <= 1e-3 * float(g[f"it{iters}_L1"])
+
+    def test_refinement_outputs_positive_sizes(self, P):
+        ctx, truth, real, _ = small_instance(P)
+        cloud = truth.copy()
+        cloud.p0 = cloud.p0 * 0.8
+        cloud.a0 = cloud.a0 * 1.3
+        state = P.create_state(cloud, lr=P.LearningRates.from_spacing(4e-4), seed=9)
+        L0 = P.loss(P.simulate_signals(cloud, ctx), real)
+        out = P.positivity_refine(state, ctx, real, 40)
+        assert np.all(out.a0 > 0.0)
+        assert np.isfinite(out.a0_free).all()
+        assert P.loss(P.simulate_signals(out, ctx), real) < L0
+
+    def test_nonpositive_entry_rejected(self, P):
+        ctx, truth, real, _ = small_instance(P)
+        bad = truth.copy()
+        bad.a0 = bad.a0.copy()
+        bad.a0[0] = -1e-4
+        state = P.create_state(bad, seed=9)
+        with pytest.raises(ValueError):
+            P.positivity_refine(state, ctx, real, 1)
+
+    def test_softplus_helpers(self, P):
+        x = np.array([-50.0, -3.0, -1e-3, 0.0, 1e-3, 3.0, 50.0])
+        np.testing.assert_allclose(P.inv_softplus(P.softplus(x[2:-1])), x[2:-1], rtol=1e-9, atol=1e-12)
+        np.testing.assert_allclose(P.sigmoid(x), 1.0 / (1.0 + np.exp(-x)), rtol=1e-15)

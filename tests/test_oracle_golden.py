@@ -206,3 +206,26 @@ def test_schedule_and_volume_match_reference():
     assert rel_l2(vol, g["volume"]) < 1e-8
     vt = ORend.voxelize(g["true_pos"], g["true_p0"], g["true_a0"], (31, 31, 31), 2e-4, (-3e-3,) * 3)
     assert rel_l2(vt, g["volume_truth"]) < 1e-14
+
+
+@pytest.mark.parametrize("iters", [3, 40])
+def test_positivity_refine_matches_reference(iters):
+    """Oracle restatement of positivity_refine (optimizer.py:536-573) against
+    the reference run (tests/golden/make_golden_refine.py)."""
+    g = golden("refine.npz")
+    prob = OO.Problem(g["sensors"], None, 1500.0, 0.0, 5e-8, 512)
+    st = OO.new_state(g["true_pos"], g["in_p0"], g["in_a0"], seed=9)
+    lr = (1e-2, 0.1 * 4e-4, 0.05 * 4e-4)   # LearningRates.from_spacing(4e-4)
+    pos, p0, a0, free = OO.positivity_refine(prob, st, g["real"], iters, lr)
+    assert np.allclose(pos, g[f"it{iters}_pos"], rtol=1e-10, atol=1e-16)
+    assert np.allclose(p0, g[f"it{iters}_p0"], rtol=1e-10)
+    assert np.allclose(a0, g[f"it{iters}_a0"], rtol=1e-10)
+    assert np.allclose(free, g[f"it{iters}_a0_free"], rtol=1e-9)
+    assert np.all(a0 > 0.0)
+
+
+def test_softplus_pair_round_trip():
+    y = np.array([1e-9, 1e-4, 0.3, 0.69999, 0.7, 2.0, 40.0])
+    np.testing.assert_allclose(OO.softplus(OO.inv_softplus(y)), y, rtol=1e-12)
+    with pytest.raises(ValueError):
+        OO.inv_softplus(np.array([0.0]))
