@@ -686,3 +686,39 @@ int pab_decimate(const float* src, int n_rows, int n_in, int f, float* dst, void
 }
 
 }  // extern "C"
+
+#ifdef PAB_WALK_BENCH
+// Tuning builds only: the forward's window walk in isolation (no setup, no
+// flush), `reps` walks of L samples per warp on its own tile, 4 warps per
+// CTA, 2 CTAs per SM -- cycles per 16-sample trip vs the XU bound.
+namespace pab {
+__global__ void __launch_bounds__(128, 2) walk_bench_kernel(int reps, int L, float* out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* tile = reinterpret_cast<float*>(smem_raw) + (threadIdx.x >> 5) * kTileAlloc * kWarp;
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < kTileAlloc * kWarp; i += 32) tile[i] = 0.0f;
+  __syncwarp();
+  float sc = 0.3f + 0.001f * lane, ps = 0.1f * lane;
+  for (int r = 0; r < reps; ++r) {
+    const int J0 = (r * 8 + lane * 8) % kTile;
+    rmw_uniform<false>(tile, lane, J0 & ~7, L, 1 << 30, (float)(-L / 2), 1.0f, sc, ps, 1.0f + 0.01f * lane, 30.0f);
+    __syncwarp();
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = tile[lane * 4];
+}
+}  // namespace pab
+extern "C" int pab_bench_walk(int blocks, int reps, int L, float* out, float* ms) {
+  const size_t smem = 4 * kTileAlloc * kWarp * sizeof(float);
+  cudaFuncSetAttribute(walk_bench_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  walk_bench_kernel<<<blocks, 128, smem>>>(reps, L, out);
+  cudaEventRecord(a);
+  walk_bench_kernel<<<blocks, 128, smem>>>(reps, L, out);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  cudaEventElapsedTime(ms, a, b);
+  return cudaGetLastError() == cudaSuccess ? 0 : 4;
+}
+#endif
