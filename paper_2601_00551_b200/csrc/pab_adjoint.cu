@@ -340,7 +340,7 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       u.L = __reduce_max_sync(0xffffffffu, u.empty ? 0 : jhi - u.J0 + 1);
       if (ops_total && live) {   // exact sample count for the op counter
         int elo, ehi;
-        pair_window(u.pg.kc, u.pg.phi, rho, acq, &elo, &ehi);
+        pair_window<true>(u.pg.kc, u.pg.phi, rho, acq, &elo, &ehi);
         my_ops += (unsigned long long)max(ehi - elo + 1, 0);
       }
       return u;
@@ -366,7 +366,7 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       pg = pair_geom(gd, gm, px, py, pz, A, B, acq);
       coinc |= pg.coincident;
       int jlo, jhi;
-      pair_window(pg.kc, pg.phi, rho, acq, &jlo, &jhi);
+      pair_window<true>(pg.kc, pg.phi, rho, acq, &jlo, &jhi);
       if (!live) { jlo = 1; jhi = 0; }
       int nlo = 1, nhi = 0, nkc = 0;
       float nphi = 0.0f;
@@ -512,6 +512,9 @@ static void launch_adjoint_dir(int dir, dim3 grid, int threads, cudaStream_t s, 
                                double* gpart, int64_t n_pad, unsigned long long* ops, int* status) {
   if (dir == kDirNone)
     launch_adjoint<STAGE, kDirNone>(grid, threads, s, A, B, G, n_groups, det_pos, det_aux, n_det, a, res, res_sign,
+                                    per_chunk, gpart, n_pad, ops, status);
+  else if (dir == kDirCosPower && a.dir_param == 2.0f)
+    launch_adjoint<STAGE, kDirCos2>(grid, threads, s, A, B, G, n_groups, det_pos, det_aux, n_det, a, res, res_sign,
                                     per_chunk, gpart, n_pad, ops, status);
   else if (dir == kDirCosPower)
     launch_adjoint<STAGE, kDirCosPower>(grid, threads, s, A, B, G, n_groups, det_pos, det_aux, n_det, a, res,

@@ -36,6 +36,8 @@ constexpr int kStatusNonFinite = 8;    // OptimizationError (optimizer.py:284-29
 // directivity kinds
 constexpr int kDirNone = 0;
 constexpr int kDirCosPower = 1;
+// (internal template value: cos power with p = 2, the branch-free common case)
+constexpr int kDirCos2 = 3;
 constexpr int kDirElement = 2;
 
 // adjoint stages
@@ -144,15 +146,19 @@ __device__ __forceinline__ int floor_div(int a, int b) {
 __device__ __forceinline__ int ceil_div(int a, int b) { return -floor_div(-a, b); }
 
 // floor(a / f) for f >= 1 without integer division: float estimate, then an
-// exact integer correction (|a| < 2^24).
+// exact integer correction (|a| < 2^24).  BF: branch-free (f = 1 is exact
+// through the estimate too) -- more instructions, but no basic-block split,
+// which matters where two pair setups are scheduled side by side.
+template <bool BF = false>
 __device__ __forceinline__ int floor_div_f(int a, int f, float inv_f) {
-  if (f == 1) return a;
+  if (!BF && f == 1) return a;
   int q = __float2int_rd((float)a * inv_f);
   q += (q + 1) * f <= a ? 1 : 0;
   q -= q * f > a ? 1 : 0;
   return q;
 }
-__device__ __forceinline__ int ceil_div_f(int a, int f, float inv_f) { return -floor_div_f(-a, f, inv_f); }
+template <bool BF = false>
+__device__ __forceinline__ int ceil_div_f(int a, int f, float inv_f) { return -floor_div_f<BF>(-a, f, inv_f); }
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -372,11 +378,11 @@ template <int DIR, bool GRAD>
 __device__ __forceinline__ float dir_weight(const DetDir& dd, float hx, float hy, float hz, float id, float power,
                                             float width, float inv_a0, float* dDdr, float* dDda0) {
   if (DIR == kDirNone) return 1.0f;
-  if (DIR == kDirCosPower) {
+  if (DIR == kDirCosPower || DIR == kDirCos2) {
     const float c = dd.fx * hx + dd.fy * hy + dd.fz * hz;
     const float cp = fmaxf(c, 0.0f);
     float D, dDdc;
-    if (power == 2.0f) { D = cp * cp; dDdc = 2.0f * cp; }
+    if (DIR == kDirCos2 || power == 2.0f) { D = cp * cp; dDdc = 2.0f * cp; }
     else if (power == 1.0f) { D = cp; dDdc = c > 0.0f ? 1.0f : 0.0f; }
     else { D = c > 0.0f ? __powf(cp, power) : 0.0f; dDdc = c > 0.0f ? power * D / cp : 0.0f; }
     if (GRAD) {
@@ -477,11 +483,12 @@ __device__ __forceinline__ void pair_window_cover(int kc, float phi, float rho, 
 }
 
 // u- window on the decimated grid, clipped to [0, n_out).
+template <bool BF = false>
 __device__ __forceinline__ void pair_window(int kc, float phi, float rho, const Acq& a, int* jlo, int* jhi) {
   const int klo = kc + __float2int_ru(phi - rho);
   const int khi = kc + __float2int_rd(phi + rho);
-  *jlo = max(ceil_div_f(klo, a.f, a.inv_f), 0);
-  *jhi = min(floor_div_f(khi, a.f, a.inv_f), a.n_out - 1);
+  *jlo = max(ceil_div_f<BF>(klo, a.f, a.inv_f), 0);
+  *jhi = min(floor_div_f<BF>(khi, a.f, a.inv_f), a.n_out - 1);
 }
 
 // u+ window (near field; only called when the group can have one).

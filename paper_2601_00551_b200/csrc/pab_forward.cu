@@ -659,6 +659,8 @@ int pab_forward(const void* rec_a, const void* rec_b, const void* group_meta, in
   // per-sample truncation test only where the walk's overrun could matter
   const bool mask = cutoff < kUnmaskedCutoff;
   if (dir_kind == kDirNone) mask ? launch(forward_kernel<kDirNone, true>) : launch(forward_kernel<kDirNone, false>);
+  else if (dir_kind == kDirCosPower && dir_param == 2.0)
+    mask ? launch(forward_kernel<kDirCos2, true>) : launch(forward_kernel<kDirCos2, false>);
   else if (dir_kind == kDirCosPower)
     mask ? launch(forward_kernel<kDirCosPower, true>) : launch(forward_kernel<kDirCosPower, false>);
   else mask ? launch(forward_kernel<kDirElement, true>) : launch(forward_kernel<kDirElement, false>);
