@@ -118,18 +118,12 @@ __device__ __forceinline__ void moments_run(const float* seg, int off, int n, fl
 //          (G <= exp(-cutoff^2/2) < 2^-24 for cutoff >= kUnmaskedCutoff):
 //          their terms are below FP32 resolution; lanes with an empty window
 //          discard their moments.
-template <int STAGE, bool MASK, bool POLY = false>
+template <int STAGE, bool MASK>
 __device__ __forceinline__ void moment_pair_masked(float2 res, float2 y, float qmax, float2& A0, float2& A1,
                                                    float2& A2, float2& A3) {
   const float2 q = __fmul2_rn(y, y);
-  float2 G;
-  if (POLY) {
-    G = exp2_neg_poly2(q);
-    if (MASK) G = make_float2(q.x <= qmax ? G.x : 0.0f, q.y <= qmax ? G.y : 0.0f);
-  } else {
-    G = MASK ? make_float2(q.x <= qmax ? ex2(-q.x) : 0.0f, q.y <= qmax ? ex2(-q.y) : 0.0f)
-             : make_float2(ex2(-q.x), ex2(-q.y));
-  }
+  const float2 G = MASK ? make_float2(q.x <= qmax ? ex2(-q.x) : 0.0f, q.y <= qmax ? ex2(-q.y) : 0.0f)
+                        : make_float2(ex2(-q.x), ex2(-q.y));
   const float2 r = __fmul2_rn(res, G);
   const float2 t = __fmul2_rn(r, y);
   A1 = __fadd2_rn(A1, t);
@@ -166,13 +160,13 @@ __device__ __forceinline__ void moment_block8(const float4* s4, float mf, const 
                                               float2& A3) {
   const float4 ra = s4[0], rb = s4[1];
   const float2 m2 = make_float2(mf, mf);
-  moment_pair_masked<STAGE, MASK, (PAB_POLY_PAIRS > 0)>(make_float2(ra.x, ra.y), __ffma2_rn(m2, W.nsc2, c0), qmax,
+  moment_pair_masked<STAGE, MASK>(make_float2(ra.x, ra.y), __ffma2_rn(m2, W.nsc2, c0), qmax,
                                                         A0, A1, A2, A3);
-  moment_pair_masked<STAGE, MASK, (PAB_POLY_PAIRS > 2)>(make_float2(ra.z, ra.w), __ffma2_rn(m2, W.nsc2, c1), qmax,
+  moment_pair_masked<STAGE, MASK>(make_float2(ra.z, ra.w), __ffma2_rn(m2, W.nsc2, c1), qmax,
                                                         A0, A1, A2, A3);
-  moment_pair_masked<STAGE, MASK, (PAB_POLY_PAIRS > 1)>(make_float2(rb.x, rb.y), __ffma2_rn(m2, W.nsc2, c2), qmax,
+  moment_pair_masked<STAGE, MASK>(make_float2(rb.x, rb.y), __ffma2_rn(m2, W.nsc2, c2), qmax,
                                                         A0, A1, A2, A3);
-  moment_pair_masked<STAGE, MASK, (PAB_POLY_PAIRS > 3)>(make_float2(rb.z, rb.w), __ffma2_rn(m2, W.nsc2, c3), qmax,
+  moment_pair_masked<STAGE, MASK>(make_float2(rb.z, rb.w), __ffma2_rn(m2, W.nsc2, c3), qmax,
                                                         A0, A1, A2, A3);
 }
 

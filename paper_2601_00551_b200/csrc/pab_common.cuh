@@ -179,30 +179,6 @@ __device__ __forceinline__ float rsqrt_ftz(float x) {
   return y;
 }
 
-// 2^(-q) for a pair of samples on the FP32 (FMA) pipe instead of MUFU.EX2:
-// round-to-nearest split -q = j + r (|r| <= 1/2, magic-number add), degree-5
-// minimax polynomial for 2^r (relative error 2.4e-7 in FP32, like
-// ex2.approx), exponent added as an integer.  q is clamped to 125 (G is then
-// ~2^-125 instead of smaller; only reached far outside a window).  Used for a
-// share of the samples so the FMA pipe takes load off the MUFU pipe.
-#ifndef PAB_POLY_PAIRS
-#define PAB_POLY_PAIRS 0
-#endif
-__device__ __forceinline__ float2 exp2_neg_poly2(float2 q) {
-  const float2 x = make_float2(-fminf(q.x, 125.0f), -fminf(q.y, 125.0f));
-  const float2 magic = make_float2(12582912.0f, 12582912.0f);   // 1.5 * 2^23
-  const float2 t = __fadd2_rn(x, magic);
-  const float2 j = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
-  const float2 r = __ffma2_rn(j, make_float2(-1.0f, -1.0f), x);
-  float2 p = __ffma2_rn(make_float2(1.3276358e-3f, 1.3276358e-3f), r, make_float2(9.6755028e-3f, 9.6755028e-3f));
-  p = __ffma2_rn(p, r, make_float2(5.5507131e-2f, 5.5507131e-2f));
-  p = __ffma2_rn(p, r, make_float2(2.4022120e-1f, 2.4022120e-1f));
-  p = __ffma2_rn(p, r, make_float2(6.9314694e-1f, 6.9314694e-1f));
-  p = __ffma2_rn(p, r, make_float2(1.0000001f, 1.0000001f));
-  return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
-                     __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
-}
-
 // Per (ball, detector) quantities.
 struct Pair {
   int kc;             // anchor full-rate sample (nearest to tau)
