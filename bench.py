@@ -44,9 +44,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--n-balls", type=int, default=1_000_000)
+    ap.add_argument("--config", type=int, choices=[2, 4], default=2,
+                    help="BASELINE config: 2 microbench (default, the headline), 4 planar tilted / element")
+    ap.add_argument("--n-balls", type=int, default=None, help="default: 1M (config 2), 4M (config 4)")
     ap.add_argument("--n-det", type=int, default=1024)
-    ap.add_argument("--n-samples", type=int, default=4096)
+    ap.add_argument("--n-samples", type=int, default=4096, help="config 2 only (config 4: 6144)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-balls", type=int, default=20000, help="oracle sample: balls x 64 detectors")
     ap.add_argument("--no-cpu", action="store_true")
@@ -55,7 +57,25 @@ def parse():
     return ap.parse_args()
 
 
+def make_scene(args):
+    """(scene, directivity kwargs for P.Directivity, oracle kind) of the
+    selected BASELINE config."""
+    from paper_2601_00551_b200 import scenes
+    if args.config == 4:
+        args.n_balls = args.n_balls or 4_000_000
+        args.n_det, args.n_samples = 1024, 6144
+        return scenes.planar_config(n_balls=args.n_balls), dict(kind="element", width=0.5e-3), ("element", 0.5e-3)
+    args.n_balls = args.n_balls or 1_000_000
+    scene = scenes.microbench_config(n_balls=args.n_balls, n_det=args.n_det, n_samples=args.n_samples)
+    return scene, dict(kind="cos_power", power=2.0), ("cos_power", 2.0)
+
+
 def config_dict(args, world):
+    if args.config == 4:
+        return {"workload": "config4-planar-tilted: fwd+fine-adjoint", "n_balls": args.n_balls,
+                "n_detectors": 1024, "n_samples": 6144, "sampling_hz": 40e6, "a0_mm": [0.05, 0.2],
+                "directivity": "element 0.5 mm", "parallelism": f"detector-shard x{world}",
+                "l2": "flushed between timed steps (256 MiB write)", "inputs": "device-resident"}
     return {"workload": "config2-microbench: fwd+fine-adjoint", "n_balls": args.n_balls,
             "n_detectors": args.n_det, "n_samples": args.n_samples, "sampling_hz": 40e6,
             "a0_mm": [0.05, 0.2], "directivity": "cos^2", "parallelism": f"detector-shard x{world}",
@@ -112,7 +132,7 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 
 def cpu_reference_pairs_per_s(scene, n_sample: int, steps: int = 1, threads: int | None = None,
-                              n_det: int = 64):
+                              n_det: int = 64, kind=("cos_power", 2.0)):
     """SURVEY.md §6 microbench slice: a strided ball subset x a strided
     detector subset of config 2 (pairs/s is linear in N*J*W)."""
     from oracle import radiator as OR   # the reference's CPU algorithm (restated); baseline only
@@ -120,7 +140,6 @@ def cpu_reference_pairs_per_s(scene, n_sample: int, steps: int = 1, threads: int
     c, t = scene.init, scene.truth
     stride = max(1, scene.array.positions.shape[0] // n_det)
     sens, nrm = scene.array.positions[::stride], scene.array.normals[::stride]
-    kind = ("cos_power", 2.0)
     sel = np.linspace(0, len(c) - 1, n_sample).astype(np.int64)
     real, _, _, _ = OR.run_model(t.positions[sel], t.p0[sel], t.a0[sel], sens, nrm, 1500.0, 0.0, scene.grid.dt,
                                  scene.grid.n_samples, 1, kind=kind, threads=threads)
@@ -138,17 +157,16 @@ def cpu_reference_pairs_per_s(scene, n_sample: int, steps: int = 1, threads: int
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    from paper_2601_00551_b200 import scenes
-    scene = scenes.microbench_config(n_balls=args.n_balls, n_det=args.n_det, n_samples=args.n_samples)
+    scene, _, kind = make_scene(args)
     vals = []
     for _ in range(args.warmup + args.steps):
-        v, cores, sample = cpu_reference_pairs_per_s(scene, args.cpu_balls, steps=1)
+        v, cores, sample = cpu_reference_pairs_per_s(scene, args.cpu_balls, steps=1, kind=kind)
         vals.append(v)
     v = statistics.median(vals[args.warmup:]) if args.steps else vals[-1]
     ms = args.n_balls * args.n_det / v * 1e3
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded CounterRng, BASELINE config 2)",
+            "vs_baseline": None, "dtype": "f64", "data": f"synthetic (seeded CounterRng, BASELINE config {args.config})",
             "config": config_dict(args, world), "impl": "reference",
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -211,8 +229,8 @@ def main():
     from paper_2601_00551_b200 import radiator as R
     from paper_2601_00551_b200 import scenes
 
-    scene = scenes.microbench_config(n_balls=args.n_balls, n_det=args.n_det, n_samples=args.n_samples)
-    ctx = P.ForwardContext(scene.array, scene.grid, directivity=P.Directivity("cos_power", power=2.0))
+    scene, dirkw, kind = make_scene(args)
+    ctx = P.ForwardContext(scene.array, scene.grid, directivity=P.Directivity(**dirkw))
     det = R.device_detectors(ctx)
     acq = R._acq(ctx, 1)
     n_total = det.n_total * acq.n_out
@@ -346,13 +364,13 @@ def main():
 
     cpu = None
     if world == 1 and not args.no_cpu:
-        v, cores, sample = cpu_reference_pairs_per_s(scene, args.cpu_balls, steps=1)
+        v, cores, sample = cpu_reference_pairs_per_s(scene, args.cpu_balls, steps=1, kind=kind)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32 per-sample, f64 per-ball accumulation",
-            "data": "synthetic (seeded CounterRng, BASELINE config 2)", "config": config_dict(args, world),
+            "data": f"synthetic (seeded CounterRng, BASELINE config {args.config})", "config": config_dict(args, world),
             "in_window_samples_per_step": samples, "samples_per_pair": samples / pairs,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": sampler.summary(),
             "gpu_launches": 4 * args.steps,

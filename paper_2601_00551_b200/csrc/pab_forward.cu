@@ -314,7 +314,7 @@ __device__ __forceinline__ void evaluate_pair(float* tile, int lane, const Acq& 
 #ifndef PAB_FWD_MINB
 #define PAB_FWD_MINB 2
 #endif
-template <int DIR, bool MASK>
+template <int DIR, bool MASK, bool SROW>
 __global__ void __launch_bounds__(kMaxWarps * 32, PAB_FWD_MINB)
 forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
                const GroupMeta* __restrict__ gmeta, int64_t n_groups,
@@ -324,13 +324,14 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int W = blockDim.x >> 5;
   const int n_out = acq.n_out;
+  const int j = blockIdx.x;
+  const int part = blockIdx.y;
   const int n_bins = (n_out + (1 << kBinShift) - 1) >> kBinShift;
-#ifdef PAB_FWD_GLOBAL_ROW
-  float* tiles = reinterpret_cast<float*>(smem_raw);
-#else
-  float* row = reinterpret_cast<float*>(smem_raw);
-  float* tiles = row + ((n_out + 3) & ~3);
-#endif
+  // SROW: the detector row in shared memory; otherwise (long records) the
+  // CTA's partial row in global memory (L2): written only by this CTA, each
+  // sample by one warp at a time, in a fixed order
+  float* row = SROW ? reinterpret_cast<float*>(smem_raw) : partial_rows + ((size_t)part * n_det + j) * (size_t)n_out;
+  float* tiles = reinterpret_cast<float*>(smem_raw) + (SROW ? ((n_out + 3) & ~3) : 0);
   float* stage = tiles + (size_t)W * kTileAlloc * kWarp;
   int* hist = reinterpret_cast<int*>(stage + W * kTile);        // [n_bins + 1]
   int* zs = hist + (n_bins + 1);                                // [W + 1]
@@ -338,16 +339,9 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   unsigned short* sorted = reinterpret_cast<unsigned short*>(misc + 4);
   unsigned short* gbin = sorted + kChunk;
 
-  const int j = blockIdx.x;
-  const int part = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tid = threadIdx.x, nthr = blockDim.x;
 
-  // the CTA's output row lives in global memory (L2): written only by this
-  // CTA, each sample by one warp at a time, in a fixed order
-#ifdef PAB_FWD_GLOBAL_ROW
-  float* row = partial_rows + ((size_t)part * n_det + j) * (size_t)n_out;
-#endif
   for (int i = tid; i < n_out; i += nthr) row[i] = 0.0f;
   for (int i = tid; i < W * kTileAlloc * kWarp; i += nthr) tiles[i] = 0.0f;
   static_assert(kTile % 8 == 0, "8-sample blocks must not straddle the circular wrap");
@@ -556,10 +550,10 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
     __syncthreads();
   }
 
-#ifndef PAB_FWD_GLOBAL_ROW
-  float* out = partial_rows + ((size_t)part * n_det + j) * (size_t)n_out;
-  for (int i = tid; i < n_out; i += nthr) out[i] = row[i];
-#endif
+  if (SROW) {
+    float* out = partial_rows + ((size_t)part * n_det + j) * (size_t)n_out;
+    for (int i = tid; i < n_out; i += nthr) out[i] = row[i];
+  }
   for (int o = 16; o > 0; o >>= 1) {
     my_ops += __shfl_xor_sync(0xffffffffu, my_ops, o);
     coinc |= __shfl_xor_sync(0xffffffffu, coinc, o);
@@ -609,13 +603,9 @@ __global__ void decimate_kernel(const float* __restrict__ src, int n_rows, int n
   dst[i] = src[r * n_in + k * f];
 }
 
-size_t forward_smem(int n_out, int warps) {
+size_t forward_smem(int n_out, int warps, bool srow) {
   const size_t n_bins = (size_t)((n_out + (1 << kBinShift) - 1) >> kBinShift);
-#ifdef PAB_FWD_GLOBAL_ROW
-  const size_t row_bytes = 0;
-#else
-  const size_t row_bytes = (size_t)((n_out + 3) & ~3) * 4;
-#endif
+  const size_t row_bytes = srow ? (size_t)((n_out + 3) & ~3) * 4 : 0;
   return row_bytes + (size_t)warps * kTileAlloc * kWarp * 4 + (size_t)warps * kTile * 4 + (n_bins + 1) * 4 +
          (size_t)(warps + 1) * 4 + 16 + 2 * kChunk * 2 + 16;
 }
@@ -626,9 +616,13 @@ using namespace pab;
 
 extern "C" {
 
+// The row stays in shared memory while two CTAs still fit on an SM
+// (2 x (smem + 1 KB reserve) <= 228 KB); longer records keep it in L2.
+static bool row_in_smem(int n_out, int warps) { return forward_smem(n_out, warps, true) <= 113 * 1024; }
+
 size_t pab_forward_smem_bytes(int n_out, int warps, int tile_rows) {
   (void)tile_rows;
-  return forward_smem(n_out, warps);
+  return forward_smem(n_out, warps, row_in_smem(n_out, warps));
 }
 
 int pab_forward(const void* rec_a, const void* rec_b, const void* group_meta, int64_t n_groups,
@@ -645,7 +639,8 @@ int pab_forward(const void* rec_a, const void* rec_b, const void* group_meta, in
   if ((int64_t)n_out * f > (1 << 24)) return 1;
   const Acq acq = make_acq(v, t0, dt, f, n_out, cutoff, dir_kind, dir_param);
   const int64_t per_part = (n_groups + partitions - 1) / partitions;
-  const size_t smem = forward_smem(n_out, warps);
+  const bool srow = row_in_smem(n_out, warps);
+  const size_t smem = forward_smem(n_out, warps, srow);
   if (smem > 227 * 1024) return 1;
   if (dir_kind < 0 || dir_kind > 2) return 1;
   dim3 grid((unsigned)n_det, (unsigned)partitions);
@@ -658,12 +653,16 @@ int pab_forward(const void* rec_a, const void* rec_b, const void* group_meta, in
   };
   // per-sample truncation test only where the walk's overrun could matter
   const bool mask = cutoff < kUnmaskedCutoff;
-  if (dir_kind == kDirNone) mask ? launch(forward_kernel<kDirNone, true>) : launch(forward_kernel<kDirNone, false>);
-  else if (dir_kind == kDirCosPower && dir_param == 2.0)
-    mask ? launch(forward_kernel<kDirCos2, true>) : launch(forward_kernel<kDirCos2, false>);
-  else if (dir_kind == kDirCosPower)
-    mask ? launch(forward_kernel<kDirCosPower, true>) : launch(forward_kernel<kDirCosPower, false>);
-  else mask ? launch(forward_kernel<kDirElement, true>) : launch(forward_kernel<kDirElement, false>);
+  auto by_row = [&](auto k_srow, auto k_grow) { srow ? launch(k_srow) : launch(k_grow); };
+  auto by_mask = [&](auto km_s, auto km_g, auto ku_s, auto ku_g) { mask ? by_row(km_s, km_g) : by_row(ku_s, ku_g); };
+#define PAB_FWD_VARIANTS(D) \
+  by_mask(forward_kernel<D, true, true>, forward_kernel<D, true, false>, forward_kernel<D, false, true>, \
+          forward_kernel<D, false, false>)
+  if (dir_kind == kDirNone) PAB_FWD_VARIANTS(kDirNone);
+  else if (dir_kind == kDirCosPower && dir_param == 2.0) PAB_FWD_VARIANTS(kDirCos2);
+  else if (dir_kind == kDirCosPower) PAB_FWD_VARIANTS(kDirCosPower);
+  else PAB_FWD_VARIANTS(kDirElement);
+#undef PAB_FWD_VARIANTS
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 
