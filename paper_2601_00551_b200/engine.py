@@ -31,7 +31,7 @@ FORWARD_WARPS = int(os.environ.get("PAB_FWD_WARPS", "4"))   # 2 CTAs per SM: one
 FORWARD_TILE_ROWS = 128
 ADJOINT_WARPS = 8
 GROUP = 32
-A0_BUCKETS = 8   # lane groups hold balls of similar radius (equal window lengths)
+A0_BUCKETS = int(os.environ.get("PAB_A0_BUCKETS", "8"))   # lane groups hold balls of similar radius (equal window lengths)
 GROUP_META_BYTES = 48
 
 
