@@ -207,18 +207,24 @@ constexpr int kFlagUniform = 1;   // staged uniform walk (far field, fits the se
 constexpr int kFlagNear = 2;      // a u+ window may exist
 constexpr int kFlagSlow = 4;      // detector within two group radii: FP64 per-pair geometry
 
-#ifndef PAB_ADJ_MINB
-#define PAB_ADJ_MINB 2
+// One warp (lane group) per CTA, 16 CTAs per SM (<= 128 registers): warps
+// retire independently (no CTA tail), measured best of 1/2/4/8 warps per CTA.
+#ifndef PAB_ADJ_WARPS
+#define PAB_ADJ_WARPS 1
 #endif
+#ifndef PAB_ADJ_MINB
+#define PAB_ADJ_MINB (16 / PAB_ADJ_WARPS)
+#endif
+constexpr int kAdjWarps = PAB_ADJ_WARPS;
 template <int STAGE, int DIR, bool MASK>
-__global__ void __launch_bounds__(256, PAB_ADJ_MINB)
+__global__ void __launch_bounds__(kAdjWarps * 32, PAB_ADJ_MINB)
 adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
                const GroupMeta* __restrict__ gmeta, int64_t n_groups,
                const double* __restrict__ det_pos, const double* __restrict__ det_aux, int n_det,
                Acq acq, const float* __restrict__ res, float res_sign, int det_per_chunk,
                double* __restrict__ gpart, int64_t n_pad, unsigned long long* __restrict__ ops_total,
                int* __restrict__ status) {
-  __shared__ __align__(16) float seg_all[8][4][kSeg + kPad + 4];
+  __shared__ __align__(16) float seg_all[kAdjWarps][4][kSeg + kPad + 4];
   const bool vec16 = (acq.n_out & 3) == 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
@@ -530,7 +536,8 @@ int pab_adjoint(const void* rec_a, const void* rec_b, const void* group_meta, in
                 float res_sign, int stage, int chunks, int warps, double* grad_partial,
                 unsigned long long* ops_total, int* status, void* stream) {
   if (n_groups <= 0 || n_det <= 0) return 0;
-  if (f < 1 || chunks < 1 || warps < 1 || warps > 8 || stage < 0 || stage > 2 || dir_kind < 0 || dir_kind > 2)
+  if (f < 1 || chunks < 1 || warps < 1 || warps > kAdjWarps || stage < 0 || stage > 2 || dir_kind < 0 ||
+      dir_kind > 2)
     return 1;
   if (!rec_a || !rec_b || !group_meta || !det_pos || !det_aux || !res || !grad_partial || !status) return 1;
   if ((int64_t)n_out * f > (1 << 24)) return 1;

@@ -29,7 +29,7 @@ STATUS_NONFINITE = 8
 
 FORWARD_WARPS = int(os.environ.get("PAB_FWD_WARPS", "4"))   # 2 CTAs per SM: one sorts while the other sweeps
 FORWARD_TILE_ROWS = 128
-ADJOINT_WARPS = 8
+ADJOINT_WARPS = int(os.environ.get("PAB_ADJ_WARPS", "1"))   # = PAB_ADJ_WARPS of the library build
 GROUP = 32
 A0_BUCKETS = int(os.environ.get("PAB_A0_BUCKETS", "8"))   # lane groups hold balls of similar radius (equal window lengths)
 GROUP_META_BYTES = 48
@@ -255,7 +255,7 @@ def plan_forward(cloud: DeviceCloud, det: DeviceDetectors, acq: Acq) -> ForwardP
 
 def plan_adjoint(cloud: DeviceCloud, det: DeviceDetectors) -> int:
     ctas = -(-cloud.n_groups // ADJOINT_WARPS)
-    target = 4 * sm_count(cloud.dev)
+    target = 2 * 16 * sm_count(cloud.dev) // ADJOINT_WARPS   # two waves of 16 resident warps per SM
     chunks = max(1, -(-target // max(ctas, 1)))
     return int(max(1, min(chunks, max(1, det.n_local // 16))))
 
