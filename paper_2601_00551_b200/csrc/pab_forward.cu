@@ -44,6 +44,22 @@ constexpr int kTile = PAB_FWD_TILE;    // tile rows per warp (circular, slot = J
 constexpr int kMaxWarps = PAB_FWD_MAXWARPS;
 constexpr int kTileAlloc = kTile + 8;  // + one 8-row dump block per warp
 
+// mbarrier helpers (warp-specialised sweep: producer/walker slot hand-off)
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+          (unsigned)__cvta_generic_to_shared(b)),
+      "r"(parity)
+      : "memory");
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -147,22 +163,38 @@ __device__ __forceinline__ float4 rmw4(float4 o, float2 m2, float2 ca, float2 cb
 #ifndef PAB_FWD_UNROLL
 #define PAB_FWD_UNROLL 2   // 8-sample blocks per loop trip
 #endif
-template <bool MASK>
-__device__ __forceinline__ void rmw_uniform(float* tile, int lane, int J0, int L, int lim, float mf, float fs,
-                                            float sc, float ps, float Ak, float qmax) {
-  constexpr int K = PAB_FWD_UNROLL;
+// Walk parameters of one pair: nsc = -sc sgn(Ak), pss = phi sc sgn(Ak),
+// nla = -log2|Ak| (+inf for Ak = 0), qmax_e = truncation bound on the
+// exponent (MASK).
+__device__ __forceinline__ Walk make_walk(float nsc, float pss, float fs, float nla, float qmax_e) {
   Walk w;
-  const float sg = Ak < 0.0f ? -1.0f : 1.0f;   // sgn(Ak) folded into y
-  const float nla = -__log2f(fabsf(Ak));       // +inf for Ak = 0
-  w.nsc2 = make_float2(-sc * sg, -sc * sg);
-  const float dl = fs * -sc * sg, dl2 = 2.0f * dl;   // y step per sample / per sample pair
-  const float pss = ps * sg;
+  w.nsc2 = make_float2(nsc, nsc);
+  const float dl = fs * nsc, dl2 = 2.0f * dl;   // y step per sample / per sample pair
   w.c0 = make_float2(pss, pss + dl);
   w.c1 = __fadd2_rn(w.c0, make_float2(dl2, dl2));
   w.c2 = __fadd2_rn(w.c1, make_float2(dl2, dl2));
   w.c3 = __fadd2_rn(w.c2, make_float2(dl2, dl2));
   w.nla2 = make_float2(nla, nla);
-  w.qmax = qmax + nla;
+  w.qmax = qmax_e;
+  return w;
+}
+
+template <bool MASK>
+__device__ __forceinline__ void rmw_walk(float* tile, int lane, int J0, int L, int lim, float mf, float fs,
+                                         const Walk& w);
+
+template <bool MASK>
+__device__ __forceinline__ void rmw_uniform(float* tile, int lane, int J0, int L, int lim, float mf, float fs,
+                                            float sc, float ps, float Ak, float qmax) {
+  const float sg = Ak < 0.0f ? -1.0f : 1.0f;   // sgn(Ak) folded into y
+  const float nla = -__log2f(fabsf(Ak));       // +inf for Ak = 0
+  rmw_walk<MASK>(tile, lane, J0, L, lim, mf, fs, make_walk(-sc * sg, ps * sg, fs, nla, qmax + nla));
+}
+
+template <bool MASK>
+__device__ __forceinline__ void rmw_walk(float* tile, int lane, int J0, int L, int lim, float mf, float fs,
+                                         const Walk& w) {
+  constexpr int K = PAB_FWD_UNROLL;
   float4* const T = reinterpret_cast<float4*>(tile) + lane;   // quad q of this lane: T[q * 32]
   const int dump = kTile / 4;                                   // dump block = quads kTile/4, kTile/4 + 1
   const float step = 8.0f * fs;
@@ -314,15 +346,18 @@ __device__ __forceinline__ void evaluate_pair(float* tile, int lane, const Acq& 
 #ifndef PAB_FWD_MINB
 #define PAB_FWD_MINB 2
 #endif
-template <int DIR, bool MASK, bool SROW>
-__global__ void __launch_bounds__(kMaxWarps * 32, PAB_FWD_MINB)
+template <int DIR, bool MASK, bool SROW, bool WS>
+__global__ void __launch_bounds__(kMaxWarps * 32 * (WS ? 2 : 1), PAB_FWD_MINB)
 forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
                const GroupMeta* __restrict__ gmeta, int64_t n_groups,
                const double* __restrict__ det_pos, const double* __restrict__ det_aux, int n_det,
                Acq acq, int64_t groups_per_part, float* __restrict__ partial_rows,
                unsigned long long* __restrict__ ops_total, int* __restrict__ status) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int W = blockDim.x >> 5;
+  // WS: warps [0, W) walk (one tile each), warps [W, 2W) compute the pair
+  // setups of walker (warp - W)'s slice and hand them over through a
+  // two-slot ring per walker (mbarrier full / empty)
+  const int W = (blockDim.x >> 5) / (WS ? 2 : 1);
   const int n_out = acq.n_out;
   const int j = blockIdx.x;
   const int part = blockIdx.y;
@@ -338,10 +373,26 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   int* misc = zs + W + 1;                                       // [4]
   unsigned short* sorted = reinterpret_cast<unsigned short*>(misc + 4);
   unsigned short* gbin = sorted + kChunk;
+  // WS hand-off ring: per walker and slot, 32 lane records (2 x float4) and
+  // a header (L, blo, ghi); mbarriers full / empty per walker and slot
+  float4* slot_a = reinterpret_cast<float4*>(
+      (reinterpret_cast<uintptr_t>(gbin + kChunk) + 15) & ~(uintptr_t)15);
+  float4* slot_b = slot_a + W * 2 * kWarp;
+  int4* slot_h = reinterpret_cast<int4*>(slot_b + W * 2 * kWarp);
+  unsigned long long* mb_full = reinterpret_cast<unsigned long long*>(slot_h + W * 2);
+  unsigned long long* mb_empty = mb_full + W * 2;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tid = threadIdx.x, nthr = blockDim.x;
 
+  if (WS && tid == 0) {
+    for (int b = 0; b < 2 * W; ++b) {
+      mbar_init(&mb_full[b], kWarp);
+      mbar_init(&mb_empty[b], kWarp);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  unsigned ring_par = WS ? (warp < W ? 0u : 3u) : 0u;   // per-slot wait parities (producers start at 1)
   for (int i = tid; i < n_out; i += nthr) row[i] = 0.0f;
   for (int i = tid; i < W * kTileAlloc * kWarp; i += nthr) tiles[i] = 0.0f;
   static_assert(kTile % 8 == 0, "8-sample blocks must not straddle the circular wrap");
@@ -350,7 +401,7 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   const Detector det = load_detector(det_pos, det_aux, j);
   DetDir dd{};
   if (DIR != kDirNone) dd = load_detdir(det_aux, j);
-  float* tile = tiles + (size_t)warp * kTileAlloc * kWarp;
+  float* tile = tiles + (size_t)(warp < W ? warp : 0) * kTileAlloc * kWarp;
   const int64_t g_begin = (int64_t)part * groups_per_part;
   const int64_t g_end = min(n_groups, g_begin + groups_per_part);
   unsigned long long my_ops = 0;
@@ -374,8 +425,12 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
         // run 7 rows past the window): the span must fit the live tile
         // wide groups and groups close to the detector (FP64 per-pair
         // geometry) take the linear-pass path (phase F)
-        bin = (hi + 7 - blo + 1 > kTile || gd.slow) ? (unsigned short)n_bins : (unsigned short)(lo >> kBinShift);
+        // (WS: near-field groups too -- the hand-off carries the u- walk only)
+        const bool wide = hi + 7 - blo + 1 > kTile;
+        const bool nr = WS && group_near(acq, gd, gm);
+        bin = (wide || gd.slow || nr) ? (unsigned short)n_bins : (unsigned short)(lo >> kBinShift);
         atomicAdd(&hist[bin], 1);   // counts only: order-independent
+
       }
       gbin[gl] = bin;
     }
@@ -422,6 +477,7 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
 
     const int n_reg = misc[0];
     const int n_all = misc[1];
+
     if (tid == 0) {
       zs[W] = n_out;
       for (int w = W - 1; w >= 0; --w) {
@@ -431,8 +487,26 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
     }
     __syncthreads();
 
-    // ---- D: time-ordered sweep of this warp's slice ----
-    {
+    // ---- D: time-ordered sweep of each walker's slice ----
+    // batch precompute: lane l of a 32-group batch computes the l-th group's
+    // FP64 geometry; its start bin, span and near flag travel in one word
+    auto batch_geometry = [&](int i0, int nb, GroupDet& gd_l, int64_t& g_l, unsigned& word_l) {
+      gd_l = empty_gd();
+      g_l = 0;
+      word_l = 0;
+      if (lane < nb) {
+        const int gl = sorted[i0 + lane];
+        g_l = cg0 + gl;
+        const int bin = gbin[gl];
+        const GroupMeta gm = gmeta[g_l];
+        gd_l = group_det(gm, det.px, det.py, det.pz, acq);
+        int glo, ghi;
+        group_range(acq, gd_l, gm, &glo, &ghi);
+        word_l = (unsigned)bin | ((unsigned)(ghi - (bin << kBinShift)) << 16) |
+                 (group_near(acq, gd_l, gm) ? 0x80000000u : 0u);
+      }
+    };
+    if (!WS || warp < W) {
       const int s_begin = (int)(((int64_t)n_reg * warp) / W);
       const int s_end = (int)(((int64_t)n_reg * (warp + 1)) / W);
       const int zone_end = zs[warp + 1];
@@ -443,24 +517,41 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       };
       int fp = zs[warp];
       int touched = fp - 1;   // highest row any window of this sweep may have written
+      // lazy flush: rows below blo are complete; only those whose slots the
+      // group's rows [blo, ghi + 7] reuse must go now -- flushed in batches
+      // of >= 32 rows when possible
+      auto make_room = [&](int blo, int ghi) {
+        const int need = ghi + 8 - kTile;
+        if (need > fp) {
+          const int upto = min(blo, max(need, fp + kWarp));
+          flush_rows(tile, lane, fp, min(upto, touched + 1), sink);
+          fp = upto;
+        }
+        touched = max(touched, ghi + 7);
+      };
+      if (WS) {
+        const float fs = (float)acq.f;
+        for (int i = s_begin; i < s_end; ++i) {
+          const int sl = i & 1;
+          mbar_wait(&mb_full[warp * 2 + sl], (ring_par >> sl) & 1u);
+          ring_par ^= 1u << sl;
+          const int4 h = slot_h[warp * 2 + sl];
+          const float4 ra4 = slot_a[(warp * 2 + sl) * kWarp + lane];
+          const float4 rb4 = slot_b[(warp * 2 + sl) * kWarp + lane];
+          mbar_arrive(&mb_empty[warp * 2 + sl]);
+          make_room(h.y, h.z);
+          if (h.x > 0)
+            rmw_walk<MASK>(tile, lane, __float_as_int(ra4.x), (h.x + 3) & ~3, __float_as_int(ra4.y), ra4.z, fs,
+                           make_walk(ra4.w, rb4.x, fs, rb4.y, rb4.z));
+          __syncwarp();
+        }
+      } else {
       for (int i0 = s_begin; i0 < s_end; i0 += kWarp) {
         const int nb = min(kWarp, s_end - i0);
-        // lane l prepares the geometry of the l-th group of this batch; its
-        // start bin, span and near flag travel in one word
-        GroupDet gd_l = empty_gd();
-        int64_t g_l = 0;
-        unsigned word_l = 0;
-        if (lane < nb) {
-          const int gl = sorted[i0 + lane];
-          g_l = cg0 + gl;
-          const int bin = gbin[gl];
-          const GroupMeta gm = gmeta[g_l];
-          gd_l = group_det(gm, det.px, det.py, det.pz, acq);
-          int glo, ghi;
-          group_range(acq, gd_l, gm, &glo, &ghi);
-          word_l = (unsigned)bin | ((unsigned)(ghi - (bin << kBinShift)) << 16) |
-                   (group_near(acq, gd_l, gm) ? 0x80000000u : 0u);
-        }
+        GroupDet gd_l;
+        int64_t g_l;
+        unsigned word_l;
+        batch_geometry(i0, nb, gd_l, g_l, word_l);
         // two groups per trip: their setups (latency-bound chains) are
         // computed side by side, then both walk in order; records of the
         // next two groups are loaded while the current ones are evaluated
@@ -492,20 +583,12 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
           for (int h = 0; h < 2; ++h) {
             if (h == 1 && !two) break;
             const int blo = h ? blob : bloa, ghi = h ? ghib : ghia;
-            // lazy flush: rows below blo are complete; only those whose
-            // slots this group's rows [blo, ghi + 7] reuse must go now --
-            // flushed in batches of >= 32 rows when possible
-            const int need = ghi + 8 - kTile;
-            if (need > fp) {
-              const int upto = min(blo, max(need, fp + kWarp));
-              flush_rows(tile, lane, fp, min(upto, touched + 1), sink);
-              fp = upto;
-            }
-            touched = max(touched, ghi + 7);
+            make_room(blo, ghi);
             pair_walk<MASK>(tile, lane, acq, h ? pb : pa, (int)((h ? wordb : worda) >> 31), my_ops, blo);
             __syncwarp();
           }
         }
+      }
       }
       if (s_begin < s_end) flush_rows(tile, lane, fp, min(n_out, touched + 1), sink);
       // rows past the signal end (clipped windows' overrun) are never
@@ -513,6 +596,65 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       for (int i = lane; i < kTile * kWarp / 4; i += kWarp)
         reinterpret_cast<float4*>(tile)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
       __syncwarp();
+    } else {
+      // producer for walker w: pair setups, two side by side, published in
+      // slice order through the ring
+      const int w = warp - W;
+      const int s_begin = (int)(((int64_t)n_reg * w) / W);
+      const int s_end = (int)(((int64_t)n_reg * (w + 1)) / W);
+      const float fs = (float)acq.f;
+      auto publish = [&](int i, const PairSetup& p, int blo, int ghi) {
+        const int sl = i & 1;
+        const bool empty_u = p.jlo > p.jhi;
+        const float Ak = empty_u ? 0.0f : p.Ak;
+        const float sg = Ak < 0.0f ? -1.0f : 1.0f;
+        const float nla = -__log2f(fabsf(Ak));   // +inf for Ak = 0
+        const float mf = (float)(p.J0 * acq.f - p.kc);
+        mbar_wait(&mb_empty[w * 2 + sl], (ring_par >> sl) & 1u);
+        ring_par ^= 1u << sl;
+        slot_a[(w * 2 + sl) * kWarp + lane] =
+            make_float4(__int_as_float(p.J0), __int_as_float(empty_u ? -1 : p.jhi), mf, -p.sc * sg);
+        slot_b[(w * 2 + sl) * kWarp + lane] = make_float4(p.phi * p.sc * sg, nla, p.qmax + nla, 0.0f);
+        if (lane == 0) slot_h[w * 2 + sl] = make_int4(p.L, blo, ghi, 0);
+        mbar_arrive(&mb_full[w * 2 + sl]);
+      };
+      (void)fs;
+      for (int i0 = s_begin; i0 < s_end; i0 += kWarp) {
+        const int nb = min(kWarp, s_end - i0);
+        GroupDet gd_l;
+        int64_t g_l;
+        unsigned word_l;
+        batch_geometry(i0, nb, gd_l, g_l, word_l);
+        int64_t ga = __shfl_sync(0xffffffffu, g_l, 0), gb = __shfl_sync(0xffffffffu, g_l, min(1, nb - 1));
+        BallA Aa = ra[ga * kWarp + lane], Ab = ra[gb * kWarp + lane];
+        BallB Ba = rb[ga * kWarp + lane], Bb = rb[gb * kWarp + lane];
+        for (int k = 0; k < nb; k += 2) {
+          const bool two = k + 1 < nb;
+          const int kb = two ? k + 1 : k;
+          const GroupDet gda = shfl_gd_fast(gd_l, k), gdb = shfl_gd_fast(gd_l, kb);
+          const unsigned worda = __shfl_sync(0xffffffffu, word_l, k), wordb = __shfl_sync(0xffffffffu, word_l, kb);
+          const BallA A0 = Aa, A1 = Ab;
+          const BallB B0 = Ba, B1 = Bb;
+          if (k + 2 < nb) {
+            ga = __shfl_sync(0xffffffffu, g_l, k + 2);
+            gb = __shfl_sync(0xffffffffu, g_l, min(k + 3, nb - 1));
+            Aa = ra[ga * kWarp + lane];
+            Ab = ra[gb * kWarp + lane];
+            Ba = rb[ga * kWarp + lane];
+            Bb = rb[gb * kWarp + lane];
+          }
+          const int bloa = (int)(worda & 0xFFFFu) << kBinShift, blob = (int)(wordb & 0xFFFFu) << kBinShift;
+          const int ghia = bloa + (int)((worda >> 16) & 0x7FFFu), ghib = blob + (int)((wordb >> 16) & 0x7FFFu);
+          unsigned long long ops_b = 0;
+          const PairSetup pa = pair_setup<DIR>(acq, gda, dd, A0, B0, my_ops, bloa);
+          const PairSetup pb = pair_setup<DIR>(acq, gdb, dd, A1, B1, ops_b, blob);
+          publish(i0 + k, pa, bloa, ghia);
+          if (two) {
+            my_ops += ops_b;
+            publish(i0 + k + 1, pb, blob, ghib);
+          }
+        }
+      }
     }
     __syncthreads();
 
@@ -603,11 +745,17 @@ __global__ void decimate_kernel(const float* __restrict__ src, int n_rows, int n
   dst[i] = src[r * n_in + k * f];
 }
 
+#ifndef PAB_FWD_WS
+#define PAB_FWD_WS 1   // warp-specialised sweep (setup producers + walkers)
+#endif
+constexpr bool kWS = PAB_FWD_WS != 0;
+
 size_t forward_smem(int n_out, int warps, bool srow) {
   const size_t n_bins = (size_t)((n_out + (1 << kBinShift) - 1) >> kBinShift);
   const size_t row_bytes = srow ? (size_t)((n_out + 3) & ~3) * 4 : 0;
+  const size_t ring = kWS ? 16 + (size_t)warps * 2 * (2 * kWarp * 16 + 16 + 2 * 8) : 0;
   return row_bytes + (size_t)warps * kTileAlloc * kWarp * 4 + (size_t)warps * kTile * 4 + (n_bins + 1) * 4 +
-         (size_t)(warps + 1) * 4 + 16 + 2 * kChunk * 2 + 16;
+         (size_t)(warps + 1) * 4 + 16 + 2 * kChunk * 2 + 16 + ring;
 }
 
 }  // namespace pab
@@ -647,7 +795,7 @@ int pab_forward(const void* rec_a, const void* rec_b, const void* group_meta, in
   auto launch = [&](auto kernel) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    kernel<<<grid, warps * kWarp, smem, (cudaStream_t)stream>>>(
+    kernel<<<grid, warps * kWarp * (kWS ? 2 : 1), smem, (cudaStream_t)stream>>>(
         (const BallA*)rec_a, (const BallB*)rec_b, (const GroupMeta*)group_meta, n_groups, det_pos, det_aux,
         n_det, acq, per_part, partial_rows, ops_total, status);
   };
@@ -656,8 +804,8 @@ int pab_forward(const void* rec_a, const void* rec_b, const void* group_meta, in
   auto by_row = [&](auto k_srow, auto k_grow) { srow ? launch(k_srow) : launch(k_grow); };
   auto by_mask = [&](auto km_s, auto km_g, auto ku_s, auto ku_g) { mask ? by_row(km_s, km_g) : by_row(ku_s, ku_g); };
 #define PAB_FWD_VARIANTS(D) \
-  by_mask(forward_kernel<D, true, true>, forward_kernel<D, true, false>, forward_kernel<D, false, true>, \
-          forward_kernel<D, false, false>)
+  by_mask(forward_kernel<D, true, true, kWS>, forward_kernel<D, true, false, kWS>,                 \
+          forward_kernel<D, false, true, kWS>, forward_kernel<D, false, false, kWS>)
   if (dir_kind == kDirNone) PAB_FWD_VARIANTS(kDirNone);
   else if (dir_kind == kDirCosPower && dir_param == 2.0) PAB_FWD_VARIANTS(kDirCos2);
   else if (dir_kind == kDirCosPower) PAB_FWD_VARIANTS(kDirCosPower);
