@@ -456,3 +456,33 @@ def test_windows_clipped_at_both_recording_ends(P, f):
     assert rel_l2(gr.d_p0, gp0) < GRAD_TOL
     assert rel_l2(gr.d_a0, ga0) < GRAD_TOL
     assert rel_l2(gr.d_position, gpos) < GRAD_TOL
+
+
+@pytest.mark.parametrize("a0_mm", [0.2, 0.6])
+def test_sparse_wide_groups_match_oracle(P, a0_mm):
+    """Lane groups spanning tens of millimetres (arrival ranges far wider
+    than the forward's live tile and the adjoint's staged segment) and, at
+    0.6 mm, windows too wide for the uniform walk: the forward's linear-pass
+    path and the adjoint's per-lane fallback, against the oracle."""
+    rng = np.random.default_rng(31)
+    n = 96
+    pos = rng.uniform(-15e-3, 15e-3, (n, 3))
+    p0 = rng.uniform(0.3, 1.0, n)
+    a0 = np.full(n, a0_mm * 1e-3) * rng.uniform(0.9, 1.1, n)
+    ang = rng.uniform(0, 2 * np.pi, 24)
+    sens = np.column_stack([0.05 * np.cos(ang), 0.05 * np.sin(ang), rng.uniform(-0.01, 0.01, 24)])
+    grid = P.TimeGrid(0.0, 2.5e-8, 3072)
+    ctx = P.ForwardContext(P.SensorArray(sens, 1500.0), grid)
+    rows, _, _, ops = OR.run_model(pos, p0, a0, sens, None, 1500.0, 0.0, grid.dt, grid.n_samples, 1)
+    P.reset_op_count()
+    got = P.simulate_signals(P.PointCloud(pos, p0, a0), ctx).data
+    assert rel_l2(got, rows) < SIG_TOL
+    assert abs(P.op_count() - ops) <= 2
+    cand = P.PointCloud(pos + rng.normal(scale=3e-5, size=pos.shape), p0 * 0.9, a0 * 1.05)
+    _, L, (gp0, ga0, gpos), _ = OR.run_model(cand.positions, cand.p0, cand.a0, sens, None, 1500.0, 0.0, grid.dt,
+                                             grid.n_samples, 1, real=rows, stage="fine")
+    Lg, gr = P.backward(cand, ctx, P.SignalSet(grid, rows), stage="fine")
+    assert abs(Lg - L) <= 1e-4 * L
+    assert rel_l2(gr.d_p0, gp0) < GRAD_TOL
+    assert rel_l2(gr.d_a0, ga0) < GRAD_TOL
+    assert rel_l2(gr.d_position, gpos) < GRAD_TOL
