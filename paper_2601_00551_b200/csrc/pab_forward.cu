@@ -30,7 +30,7 @@ namespace pab {
 
 constexpr int kBinShift = 3;           // 8 decimated samples per sort bin (bin starts 8-aligned)
 #ifndef PAB_FWD_CHUNK
-#define PAB_FWD_CHUNK 1536
+#define PAB_FWD_CHUNK 3072
 #endif
 #ifndef PAB_FWD_TILE
 #define PAB_FWD_TILE 160
@@ -43,7 +43,14 @@ constexpr unsigned short kEmptyBin = 0xFFFF;
 constexpr int kTile = PAB_FWD_TILE;    // tile rows per warp (circular, slot = J % kTile, multiple of 8)
 constexpr int kMaxWarps = PAB_FWD_MAXWARPS;
 constexpr int kTileAlloc = kTile + 8;  // + one 8-row dump block per warp
+#ifndef PAB_FWD_RING
+#define PAB_FWD_RING 2   // hand-off slots per walker (warp-specialised sweep)
+#endif
+constexpr int kRing = PAB_FWD_RING;
 
+#ifndef PAB_FWD_BACKOFF_NS
+#define PAB_FWD_BACKOFF_NS 100
+#endif
 // mbarrier helpers (warp-specialised sweep: producer/walker slot hand-off)
 __device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(count)
@@ -58,6 +65,22 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
           (unsigned)__cvta_generic_to_shared(b)),
       "r"(parity)
       : "memory");
+}
+
+// Producer side: back off between polls so a waiting producer leaves the
+// issue slots to the walker sharing its scheduler.
+__device__ __forceinline__ void mbar_wait_backoff(unsigned long long* b, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(b);
+  unsigned ok;
+  for (;;) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (ok) break;
+    __nanosleep(PAB_FWD_BACKOFF_NS);
+  }
 }
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -377,22 +400,22 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   // a header (L, blo, ghi); mbarriers full / empty per walker and slot
   float4* slot_a = reinterpret_cast<float4*>(
       (reinterpret_cast<uintptr_t>(gbin + kChunk) + 15) & ~(uintptr_t)15);
-  float4* slot_b = slot_a + W * 2 * kWarp;
-  int4* slot_h = reinterpret_cast<int4*>(slot_b + W * 2 * kWarp);
-  unsigned long long* mb_full = reinterpret_cast<unsigned long long*>(slot_h + W * 2);
-  unsigned long long* mb_empty = mb_full + W * 2;
+  float4* slot_b = slot_a + W * kRing * kWarp;
+  int4* slot_h = reinterpret_cast<int4*>(slot_b + W * kRing * kWarp);
+  unsigned long long* mb_full = reinterpret_cast<unsigned long long*>(slot_h + W * kRing);
+  unsigned long long* mb_empty = mb_full + W * kRing;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tid = threadIdx.x, nthr = blockDim.x;
 
   if (WS && tid == 0) {
-    for (int b = 0; b < 2 * W; ++b) {
+    for (int b = 0; b < kRing * W; ++b) {
       mbar_init(&mb_full[b], kWarp);
       mbar_init(&mb_empty[b], kWarp);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  unsigned ring_par = WS ? (warp < W ? 0u : 3u) : 0u;   // per-slot wait parities (producers start at 1)
+  unsigned ring_par = WS ? (warp < W ? 0u : (1u << kRing) - 1u) : 0u;   // per-slot wait parities (producers start at 1)
   for (int i = tid; i < n_out; i += nthr) row[i] = 0.0f;
   for (int i = tid; i < W * kTileAlloc * kWarp; i += nthr) tiles[i] = 0.0f;
   static_assert(kTile % 8 == 0, "8-sample blocks must not straddle the circular wrap");
@@ -532,15 +555,19 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       if (WS) {
         const float fs = (float)acq.f;
         for (int i = s_begin; i < s_end; ++i) {
-          const int sl = i & 1;
-          mbar_wait(&mb_full[warp * 2 + sl], (ring_par >> sl) & 1u);
+          const int sl = i % kRing;
+          mbar_wait(&mb_full[warp * kRing + sl], (ring_par >> sl) & 1u);
           ring_par ^= 1u << sl;
-          const int4 h = slot_h[warp * 2 + sl];
-          const float4 ra4 = slot_a[(warp * 2 + sl) * kWarp + lane];
-          const float4 rb4 = slot_b[(warp * 2 + sl) * kWarp + lane];
-          mbar_arrive(&mb_empty[warp * 2 + sl]);
+          const int4 h = slot_h[warp * kRing + sl];
+          const float4 ra4 = slot_a[(warp * kRing + sl) * kWarp + lane];
+          const float4 rb4 = slot_b[(warp * kRing + sl) * kWarp + lane];
+          mbar_arrive(&mb_empty[warp * kRing + sl]);
           make_room(h.y, h.z);
+#ifdef PAB_FWD_NOWALK   // tuning builds only: time everything but the walk
+          if (false)
+#else
           if (h.x > 0)
+#endif
             rmw_walk<MASK>(tile, lane, __float_as_int(ra4.x), (h.x + 3) & ~3, __float_as_int(ra4.y), ra4.z, fs,
                            make_walk(ra4.w, rb4.x, fs, rb4.y, rb4.z));
           __syncwarp();
@@ -604,19 +631,19 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       const int s_end = (int)(((int64_t)n_reg * (w + 1)) / W);
       const float fs = (float)acq.f;
       auto publish = [&](int i, const PairSetup& p, int blo, int ghi) {
-        const int sl = i & 1;
+        const int sl = i % kRing;
         const bool empty_u = p.jlo > p.jhi;
         const float Ak = empty_u ? 0.0f : p.Ak;
         const float sg = Ak < 0.0f ? -1.0f : 1.0f;
         const float nla = -__log2f(fabsf(Ak));   // +inf for Ak = 0
         const float mf = (float)(p.J0 * acq.f - p.kc);
-        mbar_wait(&mb_empty[w * 2 + sl], (ring_par >> sl) & 1u);
+        mbar_wait_backoff(&mb_empty[w * kRing + sl], (ring_par >> sl) & 1u);
         ring_par ^= 1u << sl;
-        slot_a[(w * 2 + sl) * kWarp + lane] =
+        slot_a[(w * kRing + sl) * kWarp + lane] =
             make_float4(__int_as_float(p.J0), __int_as_float(empty_u ? -1 : p.jhi), mf, -p.sc * sg);
-        slot_b[(w * 2 + sl) * kWarp + lane] = make_float4(p.phi * p.sc * sg, nla, p.qmax + nla, 0.0f);
-        if (lane == 0) slot_h[w * 2 + sl] = make_int4(p.L, blo, ghi, 0);
-        mbar_arrive(&mb_full[w * 2 + sl]);
+        slot_b[(w * kRing + sl) * kWarp + lane] = make_float4(p.phi * p.sc * sg, nla, p.qmax + nla, 0.0f);
+        if (lane == 0) slot_h[w * kRing + sl] = make_int4(p.L, blo, ghi, 0);
+        mbar_arrive(&mb_full[w * kRing + sl]);
       };
       (void)fs;
       for (int i0 = s_begin; i0 < s_end; i0 += kWarp) {
@@ -646,8 +673,12 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
           const int bloa = (int)(worda & 0xFFFFu) << kBinShift, blob = (int)(wordb & 0xFFFFu) << kBinShift;
           const int ghia = bloa + (int)((worda >> 16) & 0x7FFFu), ghib = blob + (int)((wordb >> 16) & 0x7FFFu);
           unsigned long long ops_b = 0;
+#ifdef PAB_FWD_NOSETUP   // tuning builds only: publish without computing setups
+          PairSetup pa{}, pb{};
+#else
           const PairSetup pa = pair_setup<DIR>(acq, gda, dd, A0, B0, my_ops, bloa);
           const PairSetup pb = pair_setup<DIR>(acq, gdb, dd, A1, B1, ops_b, blob);
+#endif
           publish(i0 + k, pa, bloa, ghia);
           if (two) {
             my_ops += ops_b;
@@ -753,7 +784,7 @@ constexpr bool kWS = PAB_FWD_WS != 0;
 size_t forward_smem(int n_out, int warps, bool srow) {
   const size_t n_bins = (size_t)((n_out + (1 << kBinShift) - 1) >> kBinShift);
   const size_t row_bytes = srow ? (size_t)((n_out + 3) & ~3) * 4 : 0;
-  const size_t ring = kWS ? 16 + (size_t)warps * 2 * (2 * kWarp * 16 + 16 + 2 * 8) : 0;
+  const size_t ring = kWS ? 16 + (size_t)warps * kRing * (2 * kWarp * 16 + 16 + 2 * 8) : 0;
   return row_bytes + (size_t)warps * kTileAlloc * kWarp * 4 + (size_t)warps * kTile * 4 + (n_bins + 1) * 4 +
          (size_t)(warps + 1) * 4 + 16 + 2 * kChunk * 2 + 16 + ring;
 }
