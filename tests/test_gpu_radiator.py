@@ -486,3 +486,35 @@ def test_sparse_wide_groups_match_oracle(P, a0_mm):
     assert rel_l2(gr.d_p0, gp0) < GRAD_TOL
     assert rel_l2(gr.d_a0, ga0) < GRAD_TOL
     assert rel_l2(gr.d_position, gpos) < GRAD_TOL
+
+
+@pytest.mark.parametrize("n_samples,f", [(1023, 1), (1021, 3), (16384, 1)])
+def test_unaligned_and_long_records_match_oracle(P, n_samples, f):
+    """Records whose length is not a multiple of 4 (4-byte residual staging,
+    unaligned rows) and a long record (detector row in L2, large bin
+    histogram), forward and fine gradients against the oracle."""
+    rng = np.random.default_rng(41)
+    n = 1500
+    pos = rng.uniform(-4e-3, 4e-3, (n, 3))
+    p0 = rng.uniform(0.2, 1.0, n)
+    a0 = rng.uniform(0.05e-3, 0.2e-3, n)
+    ang = rng.uniform(0, 2 * np.pi, 16)
+    dist = 0.02 if n_samples < 4096 else 0.2
+    sens = np.column_stack([dist * np.cos(ang), dist * np.sin(ang), rng.uniform(-0.005, 0.005, 16)])
+    dt = 2.5e-8 if n_samples < 4096 else 1e-8
+    grid = P.TimeGrid(0.0, dt, n_samples)
+    ctx = P.ForwardContext(P.SensorArray(sens, 1500.0), grid)
+    rows, _, _, ops = OR.run_model(pos, p0, a0, sens, None, 1500.0, 0.0, dt, n_samples, f)
+    P.reset_op_count()
+    got = P.simulate_at_rate(P.PointCloud(pos, p0, a0), ctx, f).data
+    assert got.shape == rows.shape
+    assert rel_l2(got, rows) < SIG_TOL
+    assert abs(P.op_count() - ops) <= 2
+    cand = P.PointCloud(pos + rng.normal(scale=1e-5, size=pos.shape), p0 * 1.05, a0 * 0.98)
+    _, L, (gp0, ga0, gpos), _ = OR.run_model(cand.positions, cand.p0, cand.a0, sens, None, 1500.0, 0.0, dt,
+                                             n_samples, f, real=rows, stage="fine")
+    Lg, gr = P.backward(cand, ctx, P.SignalSet(grid.decimated(f), rows), stage="fine")
+    assert abs(Lg - L) <= 1e-4 * L
+    assert rel_l2(gr.d_p0, gp0) < GRAD_TOL
+    assert rel_l2(gr.d_a0, ga0) < GRAD_TOL
+    assert rel_l2(gr.d_position, gpos) < GRAD_TOL
