@@ -112,19 +112,6 @@ __device__ __forceinline__ GroupDet empty_gd() {
   return g;
 }
 
-__device__ __forceinline__ GroupDet shfl_gd(const GroupDet& g, int src) {
-  GroupDet r;
-  r.Sx = __shfl_sync(0xffffffffu, g.Sx, src);
-  r.Sy = __shfl_sync(0xffffffffu, g.Sy, src);
-  r.Sz = __shfl_sync(0xffffffffu, g.Sz, src);
-  r.Sn = __shfl_sync(0xffffffffu, g.Sn, src);
-  r.isn = __shfl_sync(0xffffffffu, g.isn, src);
-  r.phg = __shfl_sync(0xffffffffu, g.phg, src);
-  r.kg = __shfl_sync(0xffffffffu, g.kg, src);
-  r.slow = __shfl_sync(0xffffffffu, g.slow, src);
-  return r;
-}
-
 // Broadcast without the slow flag (callers carry it in their own flag word).
 __device__ __forceinline__ GroupDet shfl_gd_fast(const GroupDet& g, int src) {
   GroupDet r;
@@ -177,139 +164,6 @@ __device__ __forceinline__ float rsqrt_ftz(float x) {
   float y;
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
-}
-
-// Per (ball, detector) quantities.
-struct Pair {
-  int kc;             // anchor full-rate sample (nearest to tau)
-  float phi;          // tau - kc
-  float d, id;        // distance, 1/d
-  float rx, ry, rz;   // r_ball - r_det
-  float base;         // p0 / (2 d)
-  float D;            // directivity weight
-  float amp;          // base * D
-  float sc;           // y per unit x  (v dt sqrt(log2e/2) / a0)
-  float rho;          // support half-width in full-rate samples
-  int jlo, jhi;       // u- window on the decimated grid, clipped (empty if jlo > jhi)
-  int nlo, nhi;       // u+ window (near field), usually empty
-  int nkc;            // u+ anchor
-  float nphi;         // u+ fraction
-  int coincident;
-};
-
-// Directivity weight and (optionally) its derivatives w.r.t. the ball position
-// (dDdr) and a0 (dDda0).  cos_power: D = max(cos,0)^p, cos = face . rhat.
-// element: D = sinc(w s1 / 2a0) sinc(w s2 / 2a0), s_k = e_k . rhat.
-template <bool WANT_GRAD>
-__device__ __forceinline__ float directivity(const Acq& a, const Detector& det, float rx, float ry, float rz,
-                                             float id, float a0, float inv_a0, float* dDdr, float* dDda0) {
-  if (a.dir_kind == kDirNone) return 1.0f;
-  const float hx = rx * id, hy = ry * id, hz = rz * id;
-  if (a.dir_kind == kDirCosPower) {
-    const float c = det.fx * hx + det.fy * hy + det.fz * hz;
-    if (c <= 0.0f) {
-      if (WANT_GRAD) { dDdr[0] = dDdr[1] = dDdr[2] = 0.0f; *dDda0 = 0.0f; }
-      return 0.0f;
-    }
-    const float p = a.dir_param;
-    float D, dDdc;
-    if (p == 2.0f) { D = c * c; dDdc = 2.0f * c; }
-    else if (p == 1.0f) { D = c; dDdc = 1.0f; }
-    else { D = __powf(c, p); dDdc = p * D / c; }
-    if (WANT_GRAD) {
-      const float s = dDdc * id;
-      dDdr[0] = s * (det.fx - c * hx);
-      dDdr[1] = s * (det.fy - c * hy);
-      dDdr[2] = s * (det.fz - c * hz);
-      *dDda0 = 0.0f;
-    }
-    return D;
-  }
-  // element (square piston, far-field weight at the pulse's spectral peak)
-  const float s1 = det.e1x * hx + det.e1y * hy + det.e1z * hz;
-  const float s2 = det.e2x * hx + det.e2y * hy + det.e2z * hz;
-  const float sc = 0.5f * a.dir_param * inv_a0;
-  const float x1 = sc * s1, x2 = sc * s2;
-  float f1, g1, f2, g2;
-  if (fabsf(x1) < 1e-3f) { f1 = 1.0f - x1 * x1 * (1.0f / 6.0f); g1 = -x1 * (1.0f / 3.0f); }
-  else { float sn, cs; sincosf(x1, &sn, &cs); f1 = sn / x1; g1 = (cs - f1) / x1; }
-  if (fabsf(x2) < 1e-3f) { f2 = 1.0f - x2 * x2 * (1.0f / 6.0f); g2 = -x2 * (1.0f / 3.0f); }
-  else { float sn, cs; sincosf(x2, &sn, &cs); f2 = sn / x2; g2 = (cs - f2) / x2; }
-  if (WANT_GRAD) {
-    const float a1 = g1 * f2 * sc, a2 = f1 * g2 * sc;
-    dDdr[0] = (a1 * (det.e1x - s1 * hx) + a2 * (det.e2x - s2 * hx)) * id;
-    dDdr[1] = (a1 * (det.e1y - s1 * hy) + a2 * (det.e2y - s2 * hy)) * id;
-    dDdr[2] = (a1 * (det.e1z - s1 * hz) + a2 * (det.e2z - s2 * hz)) * id;
-    *dDda0 = -(a1 * s1 + a2 * s2) * inv_a0;
-  }
-  return f1 * f2;
-}
-
-// Per-pair setup.  gd: group/detector geometry; gm: the ball's group (slow
-// path only); A/B: the ball record.
-template <bool WANT_GRAD>
-__device__ __forceinline__ Pair make_pair(const Acq& a, const GroupDet& gd, const GroupMeta& gm,
-                                          const Detector& det, const BallA& A, const BallB& B,
-                                          float* dDdr, float* dDda0) {
-  Pair p;
-  p.coincident = 0;
-  float tr;   // tau - kbase (FP32, small)
-  int kbase;
-  if (!gd.slow) {
-    const float sd = gd.Sx * A.dx + gd.Sy * A.dy + gd.Sz * A.dz;
-    const float num = B.r2 - 2.0f * sd;               // d^2 - |S|^2
-    const float e1 = fmaf(num * gd.isn, gd.isn, 1.0f);  // (d / |S|)^2
-    const float sq = e1 * rsqrtf(e1);                  // d / |S|
-    const float dd = __fdividef(num * gd.isn, 1.0f + sq);   // d - |S|
-    p.d = gd.Sn + dd;
-    tr = fmaf(dd, a.inv_vdt_f, gd.phg);
-    kbase = gd.kg;
-    p.rx = A.dx - gd.Sx; p.ry = A.dy - gd.Sy; p.rz = A.dz - gd.Sz;
-  } else {
-    // exact FP64 distance when the detector sits near/inside the group
-    const double bx = gm.cx + (double)A.dx, by = gm.cy + (double)A.dy, bz = gm.cz + (double)A.dz;
-    const double dx = bx - det.px, dy = by - det.py, dz = bz - det.pz;
-    const double d = sqrt(dx * dx + dy * dy + dz * dz);
-    if (d < 1e-12) p.coincident = 1;
-    const double tau = (d - a.vt0) * a.inv_vdt;
-    const double kf = floor(tau);
-    kbase = (int)kf;
-    tr = (float)(tau - kf);
-    p.d = (float)(d > 1e-30 ? d : 1e-30);
-    p.rx = (float)dx; p.ry = (float)dy; p.rz = (float)dz;
-  }
-  const float kr = rintf(tr);
-  p.kc = kbase + (int)kr;
-  p.phi = tr - kr;
-  p.id = __fdividef(1.0f, p.d);
-  p.base = 0.5f * B.p0 * p.id;
-  p.D = directivity<WANT_GRAD>(a, det, p.rx, p.ry, p.rz, p.id, A.a0, B.inv_a0, dDdr, dDda0);
-  p.amp = p.base * p.D;
-  p.sc = a.vdt_f * kSqrtHalfLog2e * B.inv_a0;
-  p.rho = a.cutoff * A.a0 * a.inv_vdt_f;
-  // u- window: full-rate k in [kc + ceil(phi - rho), kc + floor(phi + rho)]
-  {
-    const int klo = p.kc + __float2int_ru(p.phi - p.rho);
-    const int khi = p.kc + __float2int_rd(p.phi + p.rho);
-    p.jlo = max(ceil_div_f(klo, a.f, a.inv_f), 0);
-    p.jhi = min(floor_div_f(khi, a.f, a.inv_f), a.n_out - 1);
-  }
-  // u+ window: tau+ = -(d + v t0) / (v dt); non-empty only in the near field
-  p.nlo = 1; p.nhi = 0; p.nkc = 0; p.nphi = 0.0f;
-  if (-(p.d + a.vt0_f) * a.inv_vdt_f + p.rho >= -2.0f) {
-    const double taup = -((double)p.d + a.vt0) * a.inv_vdt;
-    if (taup + (double)p.rho >= 0.0) {
-      const double kp = rint(taup);
-      p.nkc = (int)kp;
-      p.nphi = (float)(taup - kp);
-      const int klo = p.nkc + __float2int_ru(p.nphi - p.rho);
-      const int khi = p.nkc + __float2int_rd(p.nphi + p.rho);
-      p.nlo = max(ceil_div(klo, a.f), 0);
-      p.nhi = min(floor_div(khi, a.f), a.n_out - 1);
-    }
-  }
-  if (B.orig < 0) { p.jlo = 1; p.jhi = 0; p.nlo = 1; p.nhi = 0; }
-  return p;
 }
 
 // ---------------------------------------------------------------------------
