@@ -360,6 +360,10 @@ def main():
                     "adjoint_ex2 (its binding ceiling)": {"frac": samples / adj_s / peak_ex2},
                     "adjoint_fp32": {"frac": FLOPS_ADJ_FINE * samples / adj_s / peak_flops},
                     "path_ex2 (fwd+adj, 2 ex2 per sample)": {"frac": 2 * samples / (ms_max * 1e-3) / peak_ex2}},
+                "traffic_note": "traffic is defined on DRAM bytes; this kernel is on-chip bound.  The ncu capture "
+                                "in profiles/ (r01_v7) gives 39 MB DRAM and 4.5e9 shared-memory wavefronts "
+                                "(577 GB, 1.76x the algorithmic 328 GB: 11% walk overrun, 11% setup hand-off "
+                                "ring, 2% row flushes, the rest 128-B wavefront granularity)",
                 "kernel_ms": {"forward+residual": fwd_mean, "adjoint+finalize": adj_mean}}
 
     cpu = None
@@ -369,7 +373,7 @@ def main():
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32 per-sample, f64 per-ball accumulation",
+            "vs_baseline": None, "dtype": "f32", "accumulation": "f64 per ball across detectors (adjoint)",
             "data": f"synthetic (seeded CounterRng, BASELINE config {args.config})", "config": config_dict(args, world),
             "in_window_samples_per_step": samples, "samples_per_pair": samples / pairs,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": sampler.summary(),
