@@ -362,8 +362,9 @@ def main():
                     "path_ex2 (fwd+adj, 2 ex2 per sample)": {"frac": 2 * samples / (ms_max * 1e-3) / peak_ex2}},
                 "traffic_note": "traffic is defined on DRAM bytes; this kernel is on-chip bound.  The ncu capture "
                                 "in profiles/ (r01_v7) gives 39 MB DRAM and 4.5e9 shared-memory wavefronts "
-                                "(577 GB, 1.76x the algorithmic 328 GB: 11% walk overrun, 11% setup hand-off "
-                                "ring, 2% row flushes, the rest 128-B wavefront granularity)",
+                                "(577 GB, 1.76x the algorithmic 328 GB; by construction ~37 GB of it is the "
+                                "walk overrun, ~65 GB the setup hand-off ring and ~13 GB row flushes; the "
+                                "remaining ~130 GB is not attributed)",
                 "kernel_ms": {"forward+residual": fwd_mean, "adjoint+finalize": adj_mean}}
 
     cpu = None
