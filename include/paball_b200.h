@@ -60,6 +60,9 @@ int pab_pack(const double* pos, const double* p0, const double* a0, const int32_
 
 /* Forward model: partial_rows[partitions][n_det][n_out] (FP32) for the given
  * detector set.  ops_total += in-window samples (the reference op counter).
+ * `warps` = walker warps per CTA (the CTA also runs as many setup-producer
+ * warps); `groups_per_cell` and `tile_rows` are reserved (ignored: the tile
+ * height is a build constant).
  * Replaces: radiator._block_pass forward (radiator.py:157-261). */
 size_t pab_forward_smem_bytes(int n_out, int warps, int tile_rows);
 int pab_forward(const void* rec_a, const void* rec_b, const void* group_meta, int64_t n_groups,
