@@ -886,7 +886,72 @@ __global__ void __launch_bounds__(128, 2) walk_bench_kernel(int reps, int L, flo
   }
   out[blockIdx.x * blockDim.x + threadIdx.x] = tile[lane * 4];
 }
+// Two balls per lane sharing each read-modify-write (the dual-walk
+// hypothesis): per 8-sample block, both balls' terms are added in registers.
+__global__ void __launch_bounds__(128, 2) walk_bench_dual_kernel(int reps, int L, float* out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* tile = reinterpret_cast<float*>(smem_raw) + (threadIdx.x >> 5) * kTileAlloc * kWarp;
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < kTileAlloc * kWarp; i += 32) tile[i] = 0.0f;
+  __syncwarp();
+  const float sc = 0.3f + 0.001f * lane, ps = 0.1f * lane;
+  const Walk wa = make_walk(-sc, ps, 1.0f, -__log2f(1.0f + 0.01f * lane), 30.0f);
+  const Walk wb = make_walk(-sc * 1.02f, ps + 0.05f, 1.0f, -__log2f(1.0f + 0.02f * lane), 30.0f);
+  float4* const T = reinterpret_cast<float4*>(tile) + lane;
+  for (int r = 0; r < reps; ++r) {
+    const int J0 = ((r * 8 + lane * 8) % kTile) & ~7;
+    int q = J0 >> 2;
+    float mfa = (float)(-L / 2), mfb = mfa + 2.0f;
+#pragma unroll 1
+    for (int nb = L >> 3; nb >= 2; nb -= 2) {
+      int qq[2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        qq[k] = q;
+        q += 2;
+        if (q == kTile / 4) q = 0;
+      }
+      float4 o[2][2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        o[k][0] = T[qq[k] * kWarp];
+        o[k][1] = T[(qq[k] + 1) * kWarp];
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const float2 ma = make_float2(mfa + 8.0f * k, mfa + 8.0f * k), mb = make_float2(mfb + 8.0f * k, mfb + 8.0f * k);
+        o[k][0] = rmw4(o[k][0], ma, wa.c0, wa.c1, wa, rmw_pair<false>);
+        o[k][1] = rmw4(o[k][1], ma, wa.c2, wa.c3, wa, rmw_pair<false>);
+        o[k][0] = rmw4(o[k][0], mb, wb.c0, wb.c1, wb, rmw_pair<false>);
+        o[k][1] = rmw4(o[k][1], mb, wb.c2, wb.c3, wb, rmw_pair<false>);
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        T[qq[k] * kWarp] = o[k][0];
+        T[(qq[k] + 1) * kWarp] = o[k][1];
+      }
+      mfa += 16.0f;
+      mfb += 16.0f;
+    }
+    __syncwarp();
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = tile[lane * 4];
+}
 }  // namespace pab
+extern "C" int pab_bench_walk_dual(int blocks, int reps, int L, float* out, float* ms) {
+  const size_t smem = 4 * kTileAlloc * kWarp * sizeof(float);
+  cudaFuncSetAttribute(walk_bench_dual_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  walk_bench_dual_kernel<<<blocks, 128, smem>>>(reps, L, out);
+  cudaEventRecord(a);
+  walk_bench_dual_kernel<<<blocks, 128, smem>>>(reps, L, out);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  cudaEventElapsedTime(ms, a, b);
+  return cudaGetLastError() == cudaSuccess ? 0 : 4;
+}
 extern "C" int pab_bench_walk(int blocks, int reps, int L, float* out, float* ms) {
   const size_t smem = 4 * kTileAlloc * kWarp * sizeof(float);
   cudaFuncSetAttribute(walk_bench_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

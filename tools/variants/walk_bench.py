@@ -21,3 +21,9 @@ for L in (16, 48, 96):
     samples = sms * 2 * 128 * reps * L
     print(f"L={L}: rc={rc} {ms.value:.2f} ms, {cyc:.1f} cycles per 16-sample trip per warp "
           f"(XU bound 128 at 2 warps/SMSP -> 256 per trip pair), {samples / (ms.value * 1e-3) / 1e12:.2f} T samples/s")
+for L in (48,):
+    reps = 4000
+    ms = ctypes.c_float()
+    rc = lib.pab_bench_walk_dual(sms * 2, reps, L, ctypes.c_void_p(out.data_ptr()), ctypes.byref(ms))
+    samples = 2 * sms * 2 * 128 * reps * L   # two balls per lane
+    print(f"dual L={L}: rc={rc} {ms.value:.2f} ms, {samples / (ms.value * 1e-3) / 1e12:.2f} T ball-samples/s")
