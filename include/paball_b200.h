@@ -171,6 +171,18 @@ int pab_vox_gather(const double* pos, const double* p0, const double* a0, const 
                    double oy, double oz, double support, int64_t* start /*[bricks]*/, int64_t* end /*[bricks]*/,
                    double* vol, void* stream);
 
+/* ---- universal back-projection baseline --------------
+ * Replaces: baseline.ubp_reconstruct (baseline.py:52-89).  signals[n_det][n]
+ * FP64 rows; det_pos[n_det][3]; vol[nx][ny][nz] receives
+ * (1/J) sum_j [2 p_j(t) - 2 t dp_j/dt], t = |x - r_j| / v, detectors summed in
+ * index order; *skipped (zeroed by the caller) += voxel-sensor pairs with t
+ * outside [t0, t0 + (n-1) dt].  deriv_scratch: n_det * n doubles (np.gradient
+ * of the rows).  Returns 1 for n < 2 with detectors, empty dims or null
+ * buffers. */
+int pab_ubp(const double* signals, int n_det, int n_samples, double t0, double dt, const double* det_pos,
+            double sound_speed, int nx, int ny, int nz, double spacing, double ox, double oy, double oz,
+            double* deriv_scratch, double* vol, unsigned long long* skipped, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -50,6 +50,7 @@ _SIGS = {
     "pab_vox_count": ([_vp, _vp, _vp, _vp, _i64, _i, _i, _i, _d, _d, _d, _d, _d, _vp, _vp, _vp], _i),
     "pab_vox_emit": ([_vp, _vp, _i64, _i, _i, _i, _vp, _vp], _i),
     "pab_vox_gather": ([_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i, _i, _i, _d, _d, _d, _d, _d, _vp, _vp, _vp, _vp], _i),
+    "pab_ubp": ([_vp, _i, _i, _d, _d, _vp, _d, _i, _i, _i, _d, _d, _d, _d, _vp, _vp, _vp, _vp], _i),
 }
 EXPORTED = tuple(_SIGS)
 
