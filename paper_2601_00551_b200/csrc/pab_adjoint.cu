@@ -216,6 +216,14 @@ constexpr int kFlagSlow = 4;      // detector within two group radii: FP64 per-p
 #define PAB_ADJ_MINB (16 / PAB_ADJ_WARPS)
 #endif
 constexpr int kAdjWarps = PAB_ADJ_WARPS;
+#ifdef PAB_ADJ_PROF   // tuning builds only: per-part clock totals (lane 0 of each warp)
+__device__ unsigned long long g_adj_prof[16];
+#define APROF_T(v) long long v = clock64()
+#define APROF_ACC(i, t0) prof[(i)] += clock64() - (t0)
+#else
+#define APROF_T(v)
+#define APROF_ACC(i, t0)
+#endif
 template <int STAGE, int DIR, bool MASK>
 __global__ void __launch_bounds__(kAdjWarps * 32, PAB_ADJ_MINB)
 adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
@@ -254,9 +262,14 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
   unsigned long long my_ops = 0;
   int coinc = 0;
+#ifdef PAB_ADJ_PROF
+  long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  APROF_T(t_all);
+#endif
 
   for (int jb = j0; jb < j1; jb += kWarp) {
     const int nd = min(kWarp, j1 - jb);
+    APROF_T(t_geo);
     GroupDet gdl = empty_gd();
     DetDir ddl{};
     int rlo = 0, rhi = -1, rfl = 0;
@@ -408,6 +421,7 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
     int flA = __shfl_sync(0xffffffffu, rfl, 0);
     int loB = __shfl_sync(0xffffffffu, rlo, 1), hiB = __shfl_sync(0xffffffffu, rhi, 1);
     int flB = nd > 1 ? __shfl_sync(0xffffffffu, rfl, 1) : 0;
+    APROF_ACC(0, t_geo);
     stage_seg(0, loA, hiA, flA, 0);
     if (nd > 1) stage_seg(1, loB, hiB, flB, 1);
     for (int jj = 0; jj < nd; jj += 2) {
@@ -416,8 +430,11 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       const int la = loA, ha = hiA, fa = flA, lb = loB, hb = hiB, fb = two ? flB : 0;
       const GroupDet gdA = shfl_gd_fast(gdl, jj), gdB = shfl_gd_fast(gdl, two ? jj + 1 : jj);
       const DetDir ddA = shfl_detdir<DIR>(ddl, jj), ddB = shfl_detdir<DIR>(ddl, two ? jj + 1 : jj);
+      APROF_T(t_w);
       wait_seg(fa | fb);
       __syncwarp();   // every lane is past the previous pair: its buffers may be refilled
+      APROF_ACC(1, t_w);
+      APROF_T(t_st);
       if (jj + 2 < nd) {
         loA = __shfl_sync(0xffffffffu, rlo, jj + 2);
         hiA = __shfl_sync(0xffffffffu, rhi, jj + 2);
@@ -433,23 +450,43 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
         }
       }
       const bool uA = (fa & kFlagUniform) && la <= ha, uB = two && (fb & kFlagUniform) && lb <= hb;
+      APROF_ACC(2, t_st);
       if (uA && uB) {
+        APROF_T(t_s);
         const USetup sA = usetup(gdA, la);
         const USetup sB = usetup(gdB, lb);
+#ifdef PAB_ADJ_PROF
+        __syncwarp();
+#endif
+        APROF_ACC(3, t_s);
+        APROF_T(t_k);
         const Moments MA = uwalk(sA, la, bA);
         const Moments MB = uwalk(sB, lb, bB);
         __syncwarp();
+        APROF_ACC(4, t_k);
+        APROF_T(t_e);
         epilogue(sA.pg, MA, ddA);
         epilogue(sB.pg, MB, ddB);
+#ifdef PAB_ADJ_PROF
+        __syncwarp();
+#endif
+        APROF_ACC(5, t_e);
       } else {
+        APROF_T(t_o);
         one(jj, la, ha, fa, bA, gdA, ddA);
         if (two) one(jj + 1, lb, hb, fb, bB, gdB, ddB);
+        APROF_ACC(6, t_o);
       }
     }
     __syncwarp();
 #pragma unroll
     for (int c = 0; c < 5; ++c) acc[c] += (double)gb[c];
   }
+#ifdef PAB_ADJ_PROF
+  APROF_ACC(7, t_all);
+  if (lane == 0)
+    for (int i = 0; i < 8; ++i) atomicAdd(&g_adj_prof[i], (unsigned long long)prof[i]);
+#endif
   double* out = gpart + (size_t)q * 5 * n_pad;
 #pragma unroll
   for (int c = 0; c < 5; ++c) out[c * n_pad + bi] = acc[c];
@@ -573,3 +610,14 @@ int pab_grad_finalize(const double* grad_partial, int chunks, int64_t n_groups, 
 }
 
 }  // extern "C"
+
+#ifdef PAB_ADJ_PROF
+extern "C" int pab_adj_prof(unsigned long long* out /*[16]*/, int reset) {
+  cudaMemcpyFromSymbol(out, pab::g_adj_prof, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(pab::g_adj_prof, z, sizeof(z));
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : 4;
+}
+#endif

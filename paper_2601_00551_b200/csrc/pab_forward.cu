@@ -139,15 +139,15 @@ __device__ __forceinline__ void flush_rows(float* tile, int lane, int a, int b, 
 }
 
 // Warp-uniform window walk.  Every lane walks the same number L (a multiple
-// of 4) of samples from its own 8-aligned start J0 (tile slots J0 % kTile:
-// kTile is a multiple of 8, so an 8-sample block never straddles the circular
-// wrap).  Blocks that start past the lane's last sample `lim` are redirected
+// of 4) of samples from its own 4-aligned start J0 in 8-sample blocks (two
+// row quads; the second quad of a block wraps to quad 0 at the circular end
+// of the tile).  Blocks that start past the lane's last sample `lim` are redirected
 // to a per-warp dump block, so a lane writes at most 7 rows beyond its window
 // (the bin criterion keeps those rows inside the live tile).  Inside the
 // walked range:
 //   MASK   samples with q = y^2 > qmax get G = 0 (exact truncation at
 //          cutoff sigmas, any cutoff);
-//   !MASK  no per-sample test: the <= 7 samples walked past either end of a
+//   !MASK  no per-sample test: the <= 3 / <= 7 samples walked before / after a
 //          window lie beyond cutoff sigmas, where G <= exp(-cutoff^2/2) <=
 //          2^-24 (cutoff >= 5.77, host-checked), below the FP32 resolution
 //          of the ball's own contribution.
@@ -221,17 +221,20 @@ __device__ __forceinline__ void rmw_walk(float* tile, int lane, int J0, int L, i
   float4* const T = reinterpret_cast<float4*>(tile) + lane;   // quad q of this lane: T[q * 32]
   const int dump = kTile / 4;                                   // dump block = quads kTile/4, kTile/4 + 1
   const float step = 8.0f * fs;
-  int q = (J0 % kTile) >> 2;   // quad of the current block (even)
+  constexpr int Q = kTile / 4;
+  int q = (J0 % kTile) >> 2;   // first quad of the current block
   int Jb = J0;                 // row of the current block's first sample
   int nb = L >> 3;
 #pragma unroll 1
   for (; nb >= K; nb -= K) {
-    int qq[K];
+    int qq[K], qn[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      qq[k] = Jb + 8 * k <= lim ? q : dump;
+      const bool live = Jb + 8 * k <= lim;
+      qq[k] = live ? q : dump;
+      qn[k] = live ? (q + 1 == Q ? 0 : q + 1) : dump + 1;
       q += 2;
-      if (q == kTile / 4) q = 0;
+      if (q >= Q) q -= Q;
     }
     Jb += 8 * K;
     // every block's reads before any block's writes
@@ -239,7 +242,7 @@ __device__ __forceinline__ void rmw_walk(float* tile, int lane, int J0, int L, i
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       o[k][0] = T[qq[k] * kWarp];
-      o[k][1] = T[(qq[k] + 1) * kWarp];
+      o[k][1] = T[qn[k] * kWarp];
     }
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -250,23 +253,24 @@ __device__ __forceinline__ void rmw_walk(float* tile, int lane, int J0, int L, i
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       T[qq[k] * kWarp] = o[k][0];
-      T[(qq[k] + 1) * kWarp] = o[k][1];
+      T[qn[k] * kWarp] = o[k][1];
     }
     mf += (float)K * step;
   }
 #pragma unroll 1
   for (; nb > 0; --nb) {
-    const int qb = Jb <= lim ? q : dump;
+    const bool live = Jb <= lim;
+    const int qb = live ? q : dump, qc = live ? (q + 1 == Q ? 0 : q + 1) : dump + 1;
     const float2 m2 = make_float2(mf, mf);
-    const float4 a = T[qb * kWarp], b = T[(qb + 1) * kWarp];
+    const float4 a = T[qb * kWarp], b = T[qc * kWarp];
     T[qb * kWarp] = rmw4(a, m2, w.c0, w.c1, w, rmw_pair<MASK>);
-    T[(qb + 1) * kWarp] = rmw4(b, m2, w.c2, w.c3, w, rmw_pair<MASK>);
+    T[qc * kWarp] = rmw4(b, m2, w.c2, w.c3, w, rmw_pair<MASK>);
     mf += step;
     q += 2;
-    if (q == kTile / 4) q = 0;
+    if (q >= Q) q -= Q;
     Jb += 8;
   }
-  if (L & 4) {   // 4-sample tail (8-aligned start: no wrap inside)
+  if (L & 4) {   // 4-sample tail: one quad
     const int qb = Jb <= lim ? q : dump;
     const float2 m2 = make_float2(mf, mf);
     T[qb * kWarp] = rmw4(T[qb * kWarp], m2, w.c0, w.c1, w, rmw_pair<MASK>);
@@ -306,7 +310,7 @@ __device__ __forceinline__ PairSetup pair_setup(const Acq& acq, const GroupDet& 
   // u G amp = Ak * y G with Ak = amp * kappa = (p0 D / 2d) a0 sqrt(2 ln 2)
   p.Ak = (0.5f * B.p0 * D) * pg.id * (A.a0 * kSqrt2Ln2);
   const bool empty = p.jlo > p.jhi;
-  p.J0 = (empty ? fp : p.jlo) & ~7;
+  p.J0 = (empty ? fp : p.jlo) & ~3;
   p.L = __reduce_max_sync(0xffffffffu, empty ? 0 : p.jhi - p.J0 + 1);
   return p;
 }
@@ -329,7 +333,7 @@ __device__ __forceinline__ void pair_walk(float* tile, int lane, const Acq& acq,
     ops += (unsigned long long)max(nhi - nlo + 1, 0);
     if (__any_sync(0xffffffffu, nlo <= nhi)) {   // u+ = -kappa y: walk with -sc
       const bool empty = nlo > nhi;
-      const int J0 = (empty ? fp : nlo) & ~7;
+      const int J0 = (empty ? fp : nlo) & ~3;
       const int L = __reduce_max_sync(0xffffffffu, empty ? 0 : nhi - J0 + 1);
       rmw_uniform<MASK>(tile, lane, J0, (L + 3) & ~3, empty ? -1 : nhi, (float)(J0 * acq.f - nkc), fs, -p.sc,
                         nphi * -p.sc, empty ? 0.0f : p.Ak, p.qmax);
@@ -369,6 +373,17 @@ __device__ __forceinline__ void evaluate_pair(float* tile, int lane, const Acq& 
 #ifndef PAB_FWD_MINB
 #define PAB_FWD_MINB 2
 #endif
+#ifdef PAB_FWD_PROF   // tuning builds only: per-phase clock totals (lane 0 of each warp)
+__device__ unsigned long long g_fwd_prof[32];
+#define PROF_T(v) long long v = clock64()
+#define PROF_ADD(i, t0) do { if (lane == 0) atomicAdd(&g_fwd_prof[(i)], (unsigned long long)(clock64() - (t0))); } while (0)
+#define PROF_ACC(acc, t0) (acc) += clock64() - (t0)
+#else
+#define PROF_T(v)
+#define PROF_ADD(i, t0)
+#define PROF_ACC(acc, t0)
+#endif
+
 template <int DIR, bool MASK, bool SROW, bool WS>
 __global__ void __launch_bounds__(kMaxWarps * 32 * (WS ? 2 : 1), PAB_FWD_MINB)
 forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
@@ -430,8 +445,13 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   unsigned long long my_ops = 0;
   int coinc = 0;
 
+#ifdef PAB_FWD_PROF
+  long long pw_wait = 0, pw_room = 0, pw_walk = 0, pp_setup = 0, pp_pub = 0, pp_geo = 0, pw_lanes = 0, pw_groups = 0;
+  const int pslot = (WS && warp >= W) ? 16 : 0;   // walkers 0.., producers 16..
+#endif
   for (int64_t cg0 = g_begin; cg0 < g_end; cg0 += kChunk) {
     const int cn = (int)min((int64_t)kChunk, g_end - cg0);
+    PROF_T(t_a);
     for (int i = tid; i < n_bins + 1; i += nthr) hist[i] = 0;
     __syncthreads();
 
@@ -444,7 +464,7 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       unsigned short bin = kEmptyBin;
       if (lo <= hi) {
         const int blo = lo & ~((1 << kBinShift) - 1);
-        // a lane writes rows [blo, hi + 7] (8-aligned starts, last block may
+        // a lane writes rows [blo, hi + 7] (4-aligned starts, last block may
         // run 7 rows past the window): the span must fit the live tile
         // wide groups and groups close to the detector (FP64 per-pair
         // geometry) take the linear-pass path (phase F)
@@ -457,7 +477,11 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       }
       gbin[gl] = bin;
     }
+    PROF_ADD(pslot + 0, t_a);
+    PROF_T(t_a2);
     __syncthreads();
+    PROF_ADD(pslot + 1, t_a2);
+    PROF_T(t_b);
 
     // ---- B+C (warp 0): exclusive scan, then a stable in-order scatter ----
     if (warp == 0) {
@@ -497,6 +521,8 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       }
     }
     __syncthreads();
+    PROF_ADD(pslot + 2, t_b);
+    PROF_T(t_d);
 
     const int n_reg = misc[0];
     const int n_all = misc[1];
@@ -554,15 +580,25 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       };
       if (WS) {
         const float fs = (float)acq.f;
+        PROF_T(t_loop);
         for (int i = s_begin; i < s_end; ++i) {
           const int sl = i % kRing;
+          PROF_T(t_w);
           mbar_wait(&mb_full[warp * kRing + sl], (ring_par >> sl) & 1u);
+          PROF_ACC(pw_wait, t_w);
           ring_par ^= 1u << sl;
           const int4 h = slot_h[warp * kRing + sl];
           const float4 ra4 = slot_a[(warp * kRing + sl) * kWarp + lane];
           const float4 rb4 = slot_b[(warp * kRing + sl) * kWarp + lane];
           mbar_arrive(&mb_empty[warp * kRing + sl]);
+          PROF_T(t_r);
           make_room(h.y, h.z);
+          PROF_ACC(pw_room, t_r);
+#ifdef PAB_FWD_PROF
+          pw_lanes += (h.x > 0) ? (long long)((h.x + 3) & ~3) * 32 : 0;
+          pw_groups += 1;
+#endif
+          PROF_T(t_k);
 #ifdef PAB_FWD_NOWALK   // tuning builds only: time everything but the walk
           if (false)
 #else
@@ -571,7 +607,9 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
             rmw_walk<MASK>(tile, lane, __float_as_int(ra4.x), (h.x + 3) & ~3, __float_as_int(ra4.y), ra4.z, fs,
                            make_walk(ra4.w, rb4.x, fs, rb4.y, rb4.z));
           __syncwarp();
+          PROF_ACC(pw_walk, t_k);
         }
+        PROF_ADD(13, t_loop);
       } else {
       for (int i0 = s_begin; i0 < s_end; i0 += kWarp) {
         const int nb = min(kWarp, s_end - i0);
@@ -617,12 +655,14 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
         }
       }
       }
+      PROF_T(t_fl);
       if (s_begin < s_end) flush_rows(tile, lane, fp, min(n_out, touched + 1), sink);
       // rows past the signal end (clipped windows' overrun) are never
       // flushed: clear the tile for the next chunk / the linear passes
       for (int i = lane; i < kTile * kWarp / 4; i += kWarp)
         reinterpret_cast<float4*>(tile)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
       __syncwarp();
+      PROF_ADD(6, t_fl);
     } else {
       // producer for walker w: pair setups, two side by side, published in
       // slice order through the ring
@@ -637,7 +677,9 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
         const float sg = Ak < 0.0f ? -1.0f : 1.0f;
         const float nla = -__log2f(fabsf(Ak));   // +inf for Ak = 0
         const float mf = (float)(p.J0 * acq.f - p.kc);
+        PROF_T(t_pw);
         mbar_wait_backoff(&mb_empty[w * kRing + sl], (ring_par >> sl) & 1u);
+        PROF_ACC(pp_pub, t_pw);
         ring_par ^= 1u << sl;
         slot_a[(w * kRing + sl) * kWarp + lane] =
             make_float4(__int_as_float(p.J0), __int_as_float(empty_u ? -1 : p.jhi), mf, -p.sc * sg);
@@ -651,7 +693,9 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
         GroupDet gd_l;
         int64_t g_l;
         unsigned word_l;
+        PROF_T(t_g);
         batch_geometry(i0, nb, gd_l, g_l, word_l);
+        PROF_ACC(pp_geo, t_g);
         int64_t ga = __shfl_sync(0xffffffffu, g_l, 0), gb = __shfl_sync(0xffffffffu, g_l, min(1, nb - 1));
         BallA Aa = ra[ga * kWarp + lane], Ab = ra[gb * kWarp + lane];
         BallB Ba = rb[ga * kWarp + lane], Bb = rb[gb * kWarp + lane];
@@ -673,11 +717,15 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
           const int bloa = (int)(worda & 0xFFFFu) << kBinShift, blob = (int)(wordb & 0xFFFFu) << kBinShift;
           const int ghia = bloa + (int)((worda >> 16) & 0x7FFFu), ghib = blob + (int)((wordb >> 16) & 0x7FFFu);
           unsigned long long ops_b = 0;
+          PROF_T(t_s);
 #ifdef PAB_FWD_NOSETUP   // tuning builds only: publish without computing setups
           PairSetup pa{}, pb{};
 #else
           const PairSetup pa = pair_setup<DIR>(acq, gda, dd, A0, B0, my_ops, bloa);
           const PairSetup pb = pair_setup<DIR>(acq, gdb, dd, A1, B1, ops_b, blob);
+#endif
+#ifdef PAB_FWD_PROF
+          pp_setup += clock64() - t_s;   // includes the record loads' latency
 #endif
           publish(i0 + k, pa, bloa, ghia);
           if (two) {
@@ -687,7 +735,11 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
         }
       }
     }
+    PROF_ADD(pslot + 3, t_d);
+    PROF_T(t_e);
     __syncthreads();
+    PROF_ADD(pslot + 4, t_e);
+    PROF_T(t_e2);
 
     // ---- E: overlap rows, merged in warp order ----
     for (int w = 0; w + 1 < W; ++w) {
@@ -699,6 +751,8 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       __syncthreads();
     }
 
+    PROF_ADD(pslot + 5, t_e2);
+    PROF_T(t_f);
     // ---- F: groups wider than the tile (rare): warp 0, linear passes ----
     if (warp == 0) {
       for (int idx = n_reg; idx < n_all; ++idx) {
@@ -721,7 +775,20 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       }
     }
     __syncthreads();
+    PROF_ADD(pslot + 7, t_f);
   }
+#ifdef PAB_FWD_PROF
+  if (lane == 0) {
+    atomicAdd(&g_fwd_prof[8], (unsigned long long)pw_wait);
+    atomicAdd(&g_fwd_prof[9], (unsigned long long)pw_room);
+    atomicAdd(&g_fwd_prof[10], (unsigned long long)pw_walk);
+    atomicAdd(&g_fwd_prof[11], (unsigned long long)pw_lanes);
+    atomicAdd(&g_fwd_prof[12], (unsigned long long)pw_groups);
+    atomicAdd(&g_fwd_prof[24], (unsigned long long)pp_setup);
+    atomicAdd(&g_fwd_prof[25], (unsigned long long)pp_pub);
+    atomicAdd(&g_fwd_prof[26], (unsigned long long)pp_geo);
+  }
+#endif
 
   if (SROW) {
     float* out = partial_rows + ((size_t)part * n_det + j) * (size_t)n_out;
@@ -964,6 +1031,17 @@ extern "C" int pab_bench_walk(int blocks, int reps, int L, float* out, float* ms
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   cudaEventElapsedTime(ms, a, b);
+  return cudaGetLastError() == cudaSuccess ? 0 : 4;
+}
+#endif
+
+#ifdef PAB_FWD_PROF
+extern "C" int pab_fwd_prof(unsigned long long* out /*[32]*/, int reset) {
+  cudaMemcpyFromSymbol(out, pab::g_fwd_prof, sizeof(unsigned long long) * 32);
+  if (reset) {
+    unsigned long long z[32] = {};
+    cudaMemcpyToSymbol(pab::g_fwd_prof, z, sizeof(z));
+  }
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 #endif
