@@ -282,6 +282,8 @@ def main():
     adj_ms = [e[1].elapsed_time(e[2]) for e in evs]
     step_ms = [e[0].elapsed_time(e[2]) for e in evs]
     mean_step = sum(step_ms) / len(step_ms)
+    print("step_ms " + " ".join(f"{x:.2f}" for x in step_ms) + " | fwd " + " ".join(f"{x:.2f}" for x in fwd_ms)
+          + " | adj " + " ".join(f"{x:.2f}" for x in adj_ms), file=sys.stderr)
     t = torch.tensor([mean_step], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -413,8 +413,10 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   unsigned short* gbin = sorted + kChunk;
   // WS hand-off ring: per walker and slot, 32 lane records (2 x float4) and
   // a header (L, blo, ghi); mbarriers full / empty per walker and slot
-  float4* slot_a = reinterpret_cast<float4*>(
-      (reinterpret_cast<uintptr_t>(gbin + kChunk) + 15) & ~(uintptr_t)15);
+  // (offset arithmetic on smem_raw, not an integer round trip, so the
+  // compiler keeps the shared address space: LDS/STS instead of generic LD/ST)
+  const size_t ring_off = (reinterpret_cast<unsigned char*>(gbin + kChunk) - smem_raw + 15) & ~(size_t)15;
+  float4* slot_a = reinterpret_cast<float4*>(smem_raw + ring_off);
   float4* slot_b = slot_a + W * kRing * kWarp;
   int4* slot_h = reinterpret_cast<int4*>(slot_b + W * kRing * kWarp);
   unsigned long long* mb_full = reinterpret_cast<unsigned long long*>(slot_h + W * kRing);
