@@ -87,26 +87,63 @@ def config_dict(args, world):
 # ---------------------------------------------------------------------------
 
 class ClockSampler:
+    """SM clock and clock-event (throttle) reasons sampled during the timed
+    region.  In-process NVML (the library nvidia-smi reads), initialised and
+    sampled once BEFORE the timed region so no process spawn or NVML start-up
+    lands inside it; falls back to the nvidia-smi CLI without pynvml."""
+
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, dev=None, period: float = 0.05):
         self.index = index
+        self.period = period
         self.rows = []
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
+        self._nv = None
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = None
+            if dev is not None:
+                try:
+                    pr = torch_props(dev)
+                    h = nv.nvmlDeviceGetHandleByPciBusId(
+                        f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0")
+                except Exception:
+                    h = None
+            self._h = h if h is not None else nv.nvmlDeviceGetHandleByIndex(index)
+            self._bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                          nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+            self._nv = nv
+            self._max = float(nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM))
+            self._sample()   # warm path, discarded
+            self.rows.clear()
+        except Exception:
+            self._nv = None
+
+    def _sample(self):
+        if self._nv is not None:
+            nv = self._nv
+            sm = float(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            self.rows.append([str(sm), str(self._max)] + ["Active" if r & b else "Not Active" for b in self._bits])
+            return
+        out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip()
+        if out:
+            self.rows.append([x.strip() for x in out.split(",")])
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                self._sample()
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(self.period if self._nv is not None else 0.2)
 
     def __enter__(self):
         self._t.start()
@@ -118,13 +155,18 @@ class ClockSampler:
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"], "samples": 0}
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].strip() == "Active"})
+        reasons = sorted({self.NAMES[i] for r in self.rows for i in range(4) if r[2 + i].strip() == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows),
+                "source": "NVML (in-process)" if self._nv is not None else "nvidia-smi"}
+
+
+def torch_props(dev):
+    import torch
+    return torch.cuda.get_device_properties(dev)
 
 
 # ---------------------------------------------------------------------------
@@ -267,7 +309,7 @@ def main():
 
     # kernel-level events: pack+forward+residual, adjoint+finalize(+allreduce)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(local, dev)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
