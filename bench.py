@@ -405,10 +405,10 @@ def main():
                     "adjoint_fp32": {"frac": FLOPS_ADJ_FINE * samples / adj_s / peak_flops},
                     "path_ex2 (fwd+adj, 2 ex2 per sample)": {"frac": 2 * samples / (ms_max * 1e-3) / peak_ex2}},
                 "traffic_note": "traffic is defined on DRAM bytes; this kernel is on-chip bound.  The ncu capture "
-                                "in profiles/ (r01_v7) gives 39 MB DRAM and 4.5e9 shared-memory wavefronts "
-                                "(577 GB, 1.76x the algorithmic 328 GB; by construction ~37 GB of it is the "
-                                "walk overrun, ~65 GB the setup hand-off ring and ~13 GB row flushes; the "
-                                "remaining ~130 GB is not attributed)",
+                                "in profiles/ (r01_v8) gives 39 MB DRAM and 4.25e9 shared-memory wavefronts "
+                                "(544 GB, 1.66x the algorithmic 328 GB): the walks touch 1.17x the in-window "
+                                "samples (4-aligned starts, warp-uniform block counts; 385 GB), the setup "
+                                "hand-off ring ~65 GB, row flushes ~13 GB, the rest is sort/merge scratch",
                 "kernel_ms": {"forward+residual": fwd_mean, "adjoint+finalize": adj_mean}}
 
     cpu = None
