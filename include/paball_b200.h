@@ -58,14 +58,25 @@ int pab_morton_keys(const double* pos /*[n][3]*/, const double* a0, int64_t n, d
 int pab_pack(const double* pos, const double* p0, const double* a0, const int32_t* perm, int64_t n,
              void* rec_a, void* rec_b, void* group_meta, void* stream);
 
+/* Dual-walk pairing table of a packed cloud (performance only): for each pair
+ * of consecutive lane groups and each of 64 fixed directions, the 64 balls in
+ * projection order (pab_pair_table_bytes(n_groups) bytes).  Rebuild after
+ * every pab_pack.
+ * Replaces: nothing (the reference evaluates balls one by one). */
+size_t pab_pair_table_bytes(int64_t n_groups);
+int pab_pair_table(const void* rec_a, const void* group_meta, int64_t n_groups, unsigned char* table,
+                   void* stream);
+
 /* Forward model: partial_rows[partitions][n_det][n_out] (FP32) for the given
  * detector set.  ops_total += in-window samples (the reference op counter).
  * `warps` = walker warps per CTA (the CTA also runs as many setup-producer
  * warps); `groups_per_cell` and `tile_rows` are reserved (ignored: the tile
- * height is a build constant).
+ * height is a build constant).  `pair_table` (nullable) enables the dual
+ * walk (two balls per lane) for cutoffs >= 5.8 sigma.
  * Replaces: radiator._block_pass forward (radiator.py:157-261). */
 size_t pab_forward_smem_bytes(int n_out, int warps, int tile_rows);
-int pab_forward(const void* rec_a, const void* rec_b, const void* group_meta, int64_t n_groups,
+int pab_forward(const void* rec_a, const void* rec_b, const void* group_meta, const unsigned char* pair_table,
+                int64_t n_groups,
                 const double* det_pos /*[n_det][3]*/, const double* det_aux /*[n_det][9]*/, int n_det,
                 double v, double t0, double dt, int f, int n_out, double cutoff, int dir_kind,
                 double dir_param, int groups_per_cell, int partitions, int warps, int tile_rows,

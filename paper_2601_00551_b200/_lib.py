@@ -22,7 +22,9 @@ _SIGS = {
     "pab_morton_keys": ([_vp, _vp, _i64, _d, _d, _d, _d, _d, _d, _i, _vp, _vp], _i),
     "pab_pack": ([_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp], _i),
     "pab_forward_smem_bytes": ([_i, _i, _i], C.c_size_t),
-    "pab_forward": ([_vp, _vp, _vp, _i64, _vp, _vp, _i, _d, _d, _d, _i, _i, _d, _i, _d, _i, _i, _i, _i,
+    "pab_pair_table_bytes": ([_i64], C.c_size_t),
+    "pab_pair_table": ([_vp, _vp, _i64, _vp, _vp], _i),
+    "pab_forward": ([_vp, _vp, _vp, _vp, _i64, _vp, _vp, _i, _d, _d, _d, _i, _i, _d, _i, _d, _i, _i, _i, _i,
                      _vp, _vp, _vp, _vp], _i),
     "pab_residual": ([_vp, _i, _i, _i, _vp, _vp, _vp, _vp], _i),
     "pab_adjoint": ([_vp, _vp, _vp, _i64, _vp, _vp, _i, _d, _d, _d, _i, _i, _d, _i, _d, _vp, _f, _i, _i, _i,

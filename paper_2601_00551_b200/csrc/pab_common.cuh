@@ -371,6 +371,31 @@ __device__ __forceinline__ void group_range(const Acq& a, const GroupDet& gd, co
   *hi = min(ceil_div(khi, a.f), a.n_out - 1);
 }
 
+// Dual-walk pairing directions (forward kernel): the 8 x 8 cells of a
+// hemi-octahedral map of the unit hemisphere (a pairing along u equals the
+// pairing along -u).  For every pair of consecutive lane groups (a 64-ball
+// "unit") and every cell, pab_pair_table stores the 64 balls sorted by their
+// projection on the cell's centre direction; at a detector the forward pairs
+// neighbours of that order for the cell containing the detector direction:
+// the two balls a lane walks together then have nearly equal arrival windows.
+constexpr int kPairDirs = 64;
+__device__ __forceinline__ void pair_dir(int k, float* ux, float* uy, float* uz) {   // cell centre
+  const float a = ((float)(k >> 3) + 0.5f) * 0.25f - 1.0f, b = ((float)(k & 7) + 0.5f) * 0.25f - 1.0f;
+  const float px = 0.5f * (a + b), py = 0.5f * (a - b), pz = 1.0f - fabsf(px) - fabsf(py);
+  const float inv = rsqrtf(px * px + py * py + pz * pz);
+  *ux = px * inv;
+  *uy = py * inv;
+  *uz = pz * inv;
+}
+__device__ __forceinline__ int pair_cell(float x, float y, float z) {   // cell of direction +-(x, y, z)
+  if (z < 0.0f) { x = -x; y = -y; z = -z; }
+  const float inv = 1.0f / fmaxf(fabsf(x) + fabsf(y) + z, 1e-30f);
+  const float px = x * inv, py = y * inv;
+  const int i = min(max(__float2int_rd((px + py + 1.0f) * 4.0f), 0), 7);
+  const int j = min(max(__float2int_rd((px - py + 1.0f) * 4.0f), 0), 7);
+  return (i << 3) | j;
+}
+
 __host__ __device__ inline Acq make_acq(double v, double t0, double dt, int f, int n_out, double cutoff,
                                         int dir_kind, double dir_param) {
   Acq a;

@@ -22,6 +22,7 @@
 //      order.
 // Every sample is therefore a fixed-order sum: results are bitwise
 // reproducible run to run.  Partitions are summed in order by the epilogue.
+#include <algorithm>
 #include <climits>
 
 #include "pab_common.cuh"
@@ -40,6 +41,7 @@ constexpr int kBinShift = 3;           // 8 decimated samples per sort bin (bin 
 #endif
 constexpr int kChunk = PAB_FWD_CHUNK;  // lane groups per sort chunk
 constexpr unsigned short kEmptyBin = 0xFFFF;
+constexpr unsigned short kDualTail = 0xFFFE;   // second slot of a dual sort entry
 constexpr int kTile = PAB_FWD_TILE;    // tile rows per warp (circular, slot = J % kTile, multiple of 8)
 constexpr int kMaxWarps = PAB_FWD_MAXWARPS;
 constexpr int kTileAlloc = kTile + 8;  // + one 8-row dump block per warp
@@ -277,6 +279,146 @@ __device__ __forceinline__ void rmw_walk(float* tile, int lane, int J0, int L, i
   }
 }
 
+// ---------------------------------------------------------------------------
+// Dual walk: two balls per lane share every tile read-modify-write, and the
+// Gaussian is advanced by a ratio recurrence for three of the four sample
+// pairs of a block, so the walk needs 0.5 ex2 and 4 FP32 lane-ops per
+// ball-sample and 4 bytes of shared-memory RMW per ball-sample (half the
+// single walk's): the three per-SM ceilings (FP32 128, XU 16, shared 128 B
+// per clock) all sit at 32 ball-samples per clock, 2x the single walk's.
+//
+// Per ball, y advances by dl = f * nsc per sample, e = y^2 + nla, G = 2^-e.
+// Stepping a sample pair (y -> y + 2 dl) multiplies G by
+//   R(y) = 2^-(4 dl y + 4 dl^2),  and R itself by C = 2^(-8 dl^2).
+// Each 8-sample block computes pair 0 exactly (2 ex2) and R at pair 0 (2 ex2)
+// from its own y, then pairs 1-3 by the recurrence: no state is carried
+// between blocks, so rounding cannot accumulate past three steps (measured
+// relative error of a term ~1e-6).  Underflow: pair 0's G flushes to zero
+// only for e > 126; three pair steps later e has dropped by at most
+// 12 |dl| (|y| + 3 |dl|), so with |dl| <= kDualMaxDl every term lost that way
+// lies beyond cutoff sigmas and below 2^-40 of the ball's peak.  Overflow of
+// R: the exponent is linear in y; the producer keeps every live walked sample
+// at |y| <= kDualMaxY (else the pair walks singly), so R < 2^127 there;
+// blocks past a lane's window go to the dump block and never reach the row.
+// ---------------------------------------------------------------------------
+constexpr float kDualMaxDl = 0.75f;   // max |y| step per sample for the recurrence (host-checked)
+constexpr float kDualMaxY = 30.0f;    // max |y| over a dual walk's live samples (producer-checked)
+
+struct DWalk {
+  float2 nsc2, c0, d2, nla2, kr2, br2, cc2;
+  float mf;
+};
+
+__device__ __forceinline__ DWalk make_dwalk(float nsc, float pss, float fs, float nla, float mf) {
+  DWalk w;
+  const float dl = fs * nsc;
+  w.nsc2 = make_float2(nsc, nsc);
+  w.c0 = make_float2(pss, pss + dl);
+  w.d2 = make_float2(2.0f * dl, 2.0f * dl);
+  w.nla2 = make_float2(nla, nla);
+  w.kr2 = make_float2(-4.0f * dl, -4.0f * dl);
+  w.br2 = make_float2(-4.0f * dl * dl, -4.0f * dl * dl);
+  const float c = ex2(-8.0f * dl * dl);
+  w.cc2 = make_float2(c, c);
+  w.mf = mf;
+  return w;
+}
+
+// one ball's 8-sample block added into (o0, o1): block m-offset m
+__device__ __forceinline__ void dual_block(float4& o0, float4& o1, float m, const DWalk& w) {
+  const float2 m2 = make_float2(m, m);
+  const float2 y0 = __ffma2_rn(m2, w.nsc2, w.c0);
+  const float2 y1 = __fadd2_rn(y0, w.d2);
+  const float2 y2 = __fadd2_rn(y1, w.d2);
+  const float2 y3 = __fadd2_rn(y2, w.d2);
+  const float2 e0 = __ffma2_rn(y0, y0, w.nla2);
+  const float2 er = __ffma2_rn(y0, w.kr2, w.br2);
+  const float2 g0 = make_float2(ex2(-e0.x), ex2(-e0.y));
+  const float2 r0 = make_float2(ex2(er.x), ex2(er.y));
+  const float2 g1 = __fmul2_rn(g0, r0);
+  const float2 r1 = __fmul2_rn(r0, w.cc2);
+  const float2 g2 = __fmul2_rn(g1, r1);
+  const float2 r2 = __fmul2_rn(r1, w.cc2);
+  const float2 g3 = __fmul2_rn(g2, r2);
+  float2 a = __ffma2_rn(y0, g0, make_float2(o0.x, o0.y));
+  float2 b = __ffma2_rn(y1, g1, make_float2(o0.z, o0.w));
+  float2 c = __ffma2_rn(y2, g2, make_float2(o1.x, o1.y));
+  float2 d = __ffma2_rn(y3, g3, make_float2(o1.z, o1.w));
+  o0 = make_float4(a.x, a.y, b.x, b.y);
+  o1 = make_float4(c.x, c.y, d.x, d.y);
+}
+
+#ifndef PAB_DUAL_UNROLL
+#define PAB_DUAL_UNROLL 1   // 8-sample blocks per loop trip (each block carries two balls)
+#endif
+// Warp-uniform walk of L samples (multiple of 4) from the lane's 4-aligned
+// union start J0; blocks starting past `lim` go to the dump block.
+__device__ __forceinline__ void rmw_walk_dual(float* tile, int lane, int J0, int L, int lim, float fs,
+                                              const DWalk& wa, const DWalk& wb) {
+  constexpr int K = PAB_DUAL_UNROLL;
+  float4* const T = reinterpret_cast<float4*>(tile) + lane;
+  const int dump = kTile / 4;
+  const float step = 8.0f * fs;
+  constexpr int Q = kTile / 4;
+  int q = (J0 % kTile) >> 2;
+  int Jb = J0;
+  float ma = wa.mf, mb = wb.mf;
+  int nb = L >> 3;
+#pragma unroll 1
+  for (; nb >= K; nb -= K) {
+    int qq[K], qn[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const bool live = Jb + 8 * k <= lim;
+      qq[k] = live ? q : dump;
+      qn[k] = live ? (q + 1 == Q ? 0 : q + 1) : dump + 1;
+      q += 2;
+      if (q >= Q) q -= Q;
+    }
+    Jb += 8 * K;
+    float4 o[K][2];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      o[k][0] = T[qq[k] * kWarp];
+      o[k][1] = T[qn[k] * kWarp];
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      dual_block(o[k][0], o[k][1], ma + (float)k * step, wa);
+      dual_block(o[k][0], o[k][1], mb + (float)k * step, wb);
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      T[qq[k] * kWarp] = o[k][0];
+      T[qn[k] * kWarp] = o[k][1];
+    }
+    ma += (float)K * step;
+    mb += (float)K * step;
+  }
+#pragma unroll 1
+  for (; nb > 0; --nb) {
+    const bool live = Jb <= lim;
+    const int qb = live ? q : dump, qc = live ? (q + 1 == Q ? 0 : q + 1) : dump + 1;
+    float4 o0 = T[qb * kWarp], o1 = T[qc * kWarp];
+    dual_block(o0, o1, ma, wa);
+    dual_block(o0, o1, mb, wb);
+    T[qb * kWarp] = o0;
+    T[qc * kWarp] = o1;
+    ma += step;
+    mb += step;
+    q += 2;
+    if (q >= Q) q -= Q;
+    Jb += 8;
+  }
+  if (L & 4) {   // 4-sample tail: the block's first quad only
+    const int qb = Jb <= lim ? q : dump;
+    float4 o0 = T[qb * kWarp], o1 = make_float4(0.f, 0.f, 0.f, 0.f);
+    dual_block(o0, o1, ma, wa);
+    dual_block(o0, o1, mb, wb);
+    T[qb * kWarp] = o0;
+  }
+}
+
 // One ball (lane) of one group against the CTA's detector in the time sweep,
 // split into setup (geometry, window, weight: a latency-bound chain) and walk
 // so the sweep can compute two groups' setups side by side.  Groups whose
@@ -287,7 +429,7 @@ struct PairSetup {
   bool live;
 };
 
-template <int DIR>
+template <int DIR, bool RED = true>
 __device__ __forceinline__ PairSetup pair_setup(const Acq& acq, const GroupDet& gd, const DetDir& dd, const BallA& A,
                                                 const BallB& B, unsigned long long& ops, int fp) {
   PairSetup p;
@@ -311,7 +453,7 @@ __device__ __forceinline__ PairSetup pair_setup(const Acq& acq, const GroupDet& 
   p.Ak = (0.5f * B.p0 * D) * pg.id * (A.a0 * kSqrt2Ln2);
   const bool empty = p.jlo > p.jhi;
   p.J0 = (empty ? fp : p.jlo) & ~3;
-  p.L = __reduce_max_sync(0xffffffffu, empty ? 0 : p.jhi - p.J0 + 1);
+  p.L = RED ? __reduce_max_sync(0xffffffffu, empty ? 0 : p.jhi - p.J0 + 1) : 0;
   return p;
 }
 
@@ -384,10 +526,15 @@ __device__ unsigned long long g_fwd_prof[32];
 #define PROF_ACC(acc, t0)
 #endif
 
-template <int DIR, bool MASK, bool SROW, bool WS>
+#ifndef PAB_FWD_DUAL
+#define PAB_FWD_DUAL 1   // warp-specialised unmasked sweeps walk two balls per lane (dual walk)
+#endif
+constexpr bool kDual = PAB_FWD_DUAL != 0;
+
+template <int DIR, bool MASK, bool SROW, bool WS, bool DL>
 __global__ void __launch_bounds__(kMaxWarps * 32 * (WS ? 2 : 1), PAB_FWD_MINB)
 forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
-               const GroupMeta* __restrict__ gmeta, int64_t n_groups,
+               const GroupMeta* __restrict__ gmeta, const unsigned char* __restrict__ ptab, int64_t n_groups,
                const double* __restrict__ det_pos, const double* __restrict__ det_aux, int n_det,
                Acq acq, int64_t groups_per_part, float* __restrict__ partial_rows,
                unsigned long long* __restrict__ ops_total, int* __restrict__ status) {
@@ -395,6 +542,12 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   // WS: warps [0, W) walk (one tile each), warps [W, 2W) compute the pair
   // setups of walker (warp - W)'s slice and hand them over through a
   // two-slot ring per walker (mbarrier full / empty)
+  // DUAL: the sort / sweep unit is a pair of consecutive lane groups (a
+  // "super-group" of 64 balls); lane l walks balls 2l, 2l+1 of the pair's
+  // 64 (consecutive in the Hilbert order: nearly the same arrival window)
+  constexpr bool DUAL = DL;   // host: WS && !MASK && pair table given
+  constexpr int kCU = kChunk;                       // group slots per chunk
+  constexpr int kUG = DUAL ? 2 : 1;                 // lane groups per sort unit
   const int W = (blockDim.x >> 5) / (WS ? 2 : 1);
   const int n_out = acq.n_out;
   const int j = blockIdx.x;
@@ -410,15 +563,16 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   int* zs = hist + (n_bins + 1);                                // [W + 1]
   int* misc = zs + W + 1;                                       // [4]
   unsigned short* sorted = reinterpret_cast<unsigned short*>(misc + 4);
-  unsigned short* gbin = sorted + kChunk;
+  unsigned short* gbin = sorted + kCU;
   // WS hand-off ring: per walker and slot, 32 lane records (2 x float4) and
   // a header (L, blo, ghi); mbarriers full / empty per walker and slot
   // (offset arithmetic on smem_raw, not an integer round trip, so the
   // compiler keeps the shared address space: LDS/STS instead of generic LD/ST)
-  const size_t ring_off = (reinterpret_cast<unsigned char*>(gbin + kChunk) - smem_raw + 15) & ~(size_t)15;
+  const size_t ring_off = (reinterpret_cast<unsigned char*>(gbin + kCU) - smem_raw + 15) & ~(size_t)15;
   float4* slot_a = reinterpret_cast<float4*>(smem_raw + ring_off);
   float4* slot_b = slot_a + W * kRing * kWarp;
-  int4* slot_h = reinterpret_cast<int4*>(slot_b + W * kRing * kWarp);
+  float4* slot_c = slot_b + W * kRing * kWarp;   // DUAL only
+  int4* slot_h = reinterpret_cast<int4*>(slot_b + (DUAL ? 2 : 1) * W * kRing * kWarp);
   unsigned long long* mb_full = reinterpret_cast<unsigned long long*>(slot_h + W * kRing);
   unsigned long long* mb_empty = mb_full + W * kRing;
 
@@ -452,32 +606,55 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   const int pslot = (WS && warp >= W) ? 16 : 0;   // walkers 0.., producers 16..
 #endif
   for (int64_t cg0 = g_begin; cg0 < g_end; cg0 += kChunk) {
-    const int cn = (int)min((int64_t)kChunk, g_end - cg0);
+    const int cgn = (int)min((int64_t)kChunk, g_end - cg0);   // lane groups in this chunk
+    const int cn = (cgn + kUG - 1) / kUG;                      // sort units in this chunk
     PROF_T(t_a);
     for (int i = tid; i < n_bins + 1; i += nthr) hist[i] = 0;
     __syncthreads();
 
     // ---- A: bin every group of the chunk by its first sample ----
+    // DUAL: a pair of consecutive groups is one sort entry (walked two balls
+    // per lane) when its union range fits the tile; otherwise each group is
+    // its own entry (single walk) or, if it alone is too wide, oversize.
+    // gbin is per group slot; a pair's second slot holds kDualTail.
     for (int gl = tid; gl < cn; gl += nthr) {
-      const GroupMeta gm = gmeta[cg0 + gl];
-      const GroupDet gd = group_det(gm, det.px, det.py, det.pz, acq);
-      int lo, hi;
-      group_range(acq, gd, gm, &lo, &hi);
-      unsigned short bin = kEmptyBin;
-      if (lo <= hi) {
-        const int blo = lo & ~((1 << kBinShift) - 1);
-        // a lane writes rows [blo, hi + 7] (4-aligned starts, last block may
-        // run 7 rows past the window): the span must fit the live tile
-        // wide groups and groups close to the detector (FP64 per-pair
-        // geometry) take the linear-pass path (phase F)
-        // (WS: near-field groups too -- the hand-off carries the u- walk only)
-        const bool wide = hi + 7 - blo + 1 > kTile;
-        const bool nr = WS && group_near(acq, gd, gm);
-        bin = (wide || gd.slow || nr) ? (unsigned short)n_bins : (unsigned short)(lo >> kBinShift);
-        atomicAdd(&hist[bin], 1);   // counts only: order-independent
-
+      int lo[kUG], hi[kUG];
+      bool slow[kUG], nr[kUG];
+      for (int u = 0; u < kUG; ++u) {
+        lo[u] = 1; hi[u] = 0; slow[u] = false; nr[u] = false;
+        if (kUG * gl + u >= cgn) break;
+        const GroupMeta gm = gmeta[cg0 + kUG * gl + u];
+        const GroupDet gd = group_det(gm, det.px, det.py, det.pz, acq);
+        group_range(acq, gd, gm, &lo[u], &hi[u]);
+        slow[u] = gd.slow != 0;
+        nr[u] = WS && group_near(acq, gd, gm);
       }
-      gbin[gl] = bin;
+      // a lane writes rows [blo, hi + 7] (4-aligned starts, last block may
+      // run 7 rows past the window): the span must fit the live tile; wide
+      // groups and groups close to the detector (FP64 per-pair geometry)
+      // take the linear-pass path (phase F) (WS: near-field groups too --
+      // the hand-off carries the u- walk only)
+      auto bin_of = [&](int l, int h, bool sl, bool n) -> unsigned short {
+        if (l > h) return kEmptyBin;
+        const int blo = l & ~((1 << kBinShift) - 1);
+        const bool wide = h + 7 - blo + 1 > kTile;
+        return (wide || sl || n) ? (unsigned short)n_bins : (unsigned short)(l >> kBinShift);
+      };
+      if (DUAL && kUG * gl + 1 < cgn && lo[0] <= hi[0] && lo[kUG - 1] <= hi[kUG - 1]) {
+        const unsigned short b = bin_of(min(lo[0], lo[kUG - 1]), max(hi[0], hi[kUG - 1]),
+                                        slow[0] || slow[kUG - 1], nr[0] || nr[kUG - 1]);
+        if (b != (unsigned short)n_bins) {   // the pair fits: one dual entry
+          atomicAdd(&hist[b], 1);            // counts only: order-independent
+          gbin[kUG * gl] = b;
+          gbin[kUG * gl + kUG - 1] = kDualTail;
+          continue;
+        }
+      }
+      for (int u = 0; u < kUG && kUG * gl + u < cgn; ++u) {
+        const unsigned short b = bin_of(lo[u], hi[u], slow[u], nr[u]);
+        if (b != kEmptyBin) atomicAdd(&hist[b], 1);
+        gbin[kUG * gl + u] = b;
+      }
     }
     PROF_ADD(pslot + 0, t_a);
     PROF_T(t_a2);
@@ -508,15 +685,18 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
         if (ops_total) atomicAdd(ops_total, (unsigned long long)(carry - hist[n_bins]) << 40);
 #endif
       }
-      for (int b0 = 0; b0 < cn; b0 += kWarp) {
+      for (int b0 = 0; b0 < cgn; b0 += kWarp) {
         const int gl = b0 + lane;
-        const unsigned short bin = gl < cn ? gbin[gl] : kEmptyBin;
+        unsigned short bin = gl < cgn ? gbin[gl] : kEmptyBin;
+        // DUAL entries are listed by their first slot, flagged in bit 15
+        const bool pair = DUAL && bin < kDualTail && gl + 1 < cgn && gbin[gl + 1] == kDualTail;
+        if (bin == kDualTail) bin = kEmptyBin;
         const unsigned mask = __match_any_sync(0xffffffffu, (int)bin);
         int pos = 0;
         if (bin != kEmptyBin) pos = hist[bin] + __popc(mask & lanemask_lt());
         __syncwarp();
         if (bin != kEmptyBin) {
-          sorted[pos] = (unsigned short)gl;
+          sorted[pos] = (unsigned short)(gl | (pair ? 0x8000 : 0));
           if ((mask & lanemask_lt()) == 0) hist[bin] += __popc(mask);
         }
         __syncwarp();
@@ -533,7 +713,7 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       zs[W] = n_out;
       for (int w = W - 1; w >= 0; --w) {
         const int s = (int)(((int64_t)n_reg * w) / W), e = (int)(((int64_t)n_reg * (w + 1)) / W);
-        zs[w] = (s < e) ? ((int)gbin[sorted[s]] << kBinShift) : zs[w + 1];
+        zs[w] = (s < e) ? ((int)gbin[sorted[s] & 0x7FFF] << kBinShift) : zs[w + 1];
       }
     }
     __syncthreads();
@@ -592,7 +772,42 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
           const int4 h = slot_h[warp * kRing + sl];
           const float4 ra4 = slot_a[(warp * kRing + sl) * kWarp + lane];
           const float4 rb4 = slot_b[(warp * kRing + sl) * kWarp + lane];
+          const int mode = h.w & 3;
+          float4 rc4;
+          if (DUAL && mode != 0) rc4 = slot_c[(warp * kRing + sl) * kWarp + lane];
           mbar_arrive(&mb_empty[warp * kRing + sl]);
+          if (DUAL && mode != 0) {
+            // record: a = (J0a, jhia, mfa, nsca), b = (pssa, nlaa, J0b, jhib),
+            // c = (mfb, nscb, pssb, nlab); header (Lu | La, blo, ghi, mode | Lb << 16)
+            PROF_T(t_r2);
+            make_room(h.y, h.z);
+            PROF_ACC(pw_room, t_r2);
+#ifdef PAB_FWD_PROF
+            pw_groups += 2;
+            pw_lanes += 2 * (long long)((h.x + 3) & ~3) * 32 + (mode == 2 ? 2 * (long long)(((h.w >> 16) + 3) & ~3) * 32 : 0);
+            if (lane == 0) atomicAdd(&g_fwd_prof[mode == 2 ? 14 : 15], 1ull);
+#endif
+            PROF_T(t_k2);
+            const int J0a = __float_as_int(ra4.x), jha = __float_as_int(ra4.y);
+            const int J0b = __float_as_int(rb4.z), jhb = __float_as_int(rb4.w);
+            if (mode == 1) {   // dual walk over the lane's union window
+              if (h.x > 0) {
+                const int J0u = jha < 0 ? J0b : (jhb < 0 ? J0a : min(J0a, J0b));
+                const DWalk wa = make_dwalk(ra4.w, rb4.x, fs, rb4.y, ra4.z + (float)((J0u - J0a) * acq.f));
+                const DWalk wb = make_dwalk(rc4.y, rc4.z, fs, rc4.w, rc4.x + (float)((J0u - J0b) * acq.f));
+                rmw_walk_dual(tile, lane, J0u, (h.x + 3) & ~3, max(jha, jhb), fs, wa, wb);
+              }
+            } else {           // the pair's windows lie far apart: two single walks
+              const int La = h.x, Lb = h.w >> 16;
+              if (La > 0) rmw_walk<false>(tile, lane, J0a, (La + 3) & ~3, jha, ra4.z, fs,
+                                         make_walk(ra4.w, rb4.x, fs, rb4.y, 0.0f));
+              if (Lb > 0) rmw_walk<false>(tile, lane, J0b, (Lb + 3) & ~3, jhb, rc4.x, fs,
+                                         make_walk(rc4.y, rc4.z, fs, rc4.w, 0.0f));
+            }
+            __syncwarp();
+            PROF_ACC(pw_walk, t_k2);
+            continue;
+          }
           PROF_T(t_r);
           make_room(h.y, h.z);
           PROF_ACC(pw_room, t_r);
@@ -690,6 +905,162 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
         mbar_arrive(&mb_full[w * kRing + sl]);
       };
       (void)fs;
+      if constexpr (DUAL) {
+        // entries are single lane groups (32 lanes, one ball each: the
+        // single walk) or dual pairs of groups (lanes 0-15 take balls
+        // (2l, 2l+1) of the first group, lanes 16-31 those of the second)
+        // dual entry: lane l walks the balls at positions 2l, 2l+1 of the
+        // unit's projection order for the detector direction's cell (ball
+        // ids 0-31 first group, 32-63 second: record g0 * 32 + id)
+        auto load_ids = [&](int64_t g0, int cell) -> unsigned {
+          return reinterpret_cast<const unsigned short*>(ptab + ((size_t)(g0 >> 1) * kPairDirs + cell) * 64)[lane];
+        };
+        auto load_recs = [&](int64_t g0, bool pair, unsigned ids, BallA& A0, BallA& A1, BallB& B0, BallB& B1) {
+          const int64_t bi = pair ? g0 * kWarp + (ids & 0xFFu) : g0 * kWarp + lane;
+          A0 = ra[bi];
+          B0 = rb[bi];
+          if (pair) {
+            A1 = ra[g0 * kWarp + (ids >> 8)];
+            B1 = rb[g0 * kWarp + (ids >> 8)];
+          }
+        };
+        auto publish = [&](int i, int mode, int x, int blo, int ghi, int hw, float4 va, float4 vb, float4 vc) {
+          const int sl = i % kRing;
+          PROF_T(t_pw);
+          mbar_wait_backoff(&mb_empty[w * kRing + sl], (ring_par >> sl) & 1u);
+          PROF_ACC(pp_pub, t_pw);
+          ring_par ^= 1u << sl;
+          const int ix = (w * kRing + sl) * kWarp + lane;
+          slot_a[ix] = va;
+          slot_b[ix] = vb;
+          if (mode != 0) slot_c[ix] = vc;
+          if (lane == 0) slot_h[w * kRing + sl] = make_int4(x, blo, ghi, mode | (hw << 16));
+          mbar_arrive(&mb_full[w * kRing + sl]);
+        };
+        for (int i0 = s_begin; i0 < s_end; i0 += kWarp) {
+          const int nb = min(kWarp, s_end - i0);
+          GroupDet gdA_l = empty_gd(), gdB_l = empty_gd();
+          int64_t g_l = 0;
+          unsigned word_l = 0;
+          int cell_l = 0;
+          PROF_T(t_g);
+          if (lane < nb) {
+            const int e = sorted[i0 + lane];
+            const int slot = e & 0x7FFF;
+            const bool pair = (e >> 15) != 0;
+            g_l = cg0 + slot;
+            const int bin = gbin[slot];
+            const GroupMeta gmA = gmeta[g_l];
+            gdA_l = group_det(gmA, det.px, det.py, det.pz, acq);
+            int lo, hi;
+            group_range(acq, gdA_l, gmA, &lo, &hi);
+            int ghi = hi;
+            if (pair) {
+              const GroupMeta gmB = gmeta[g_l + 1];
+              gdB_l = group_det(gmB, det.px, det.py, det.pz, acq);
+              group_range(acq, gdB_l, gmB, &lo, &hi);
+              ghi = max(ghi, hi);
+            }
+            word_l = (unsigned)bin | ((unsigned)(ghi - (bin << kBinShift)) << 16) | (pair ? 0x80000000u : 0u);
+            cell_l = pair ? pair_cell(gdA_l.Sx, gdA_l.Sy, gdA_l.Sz) : 0;
+          }
+          PROF_ACC(pp_geo, t_g);
+          // two-stage prefetch: pairing ids two entries ahead, records one ahead
+          auto entry = [&](int k, int64_t& g0, bool& pair, int& cell) {
+            g0 = __shfl_sync(0xffffffffu, g_l, k);
+            pair = __shfl_sync(0xffffffffu, word_l, k) >> 31;
+            cell = __shfl_sync(0xffffffffu, cell_l, k);
+          };
+          int64_t gn, gn2 = 0;
+          bool pn, pn2 = false;
+          int cn_, cn2;
+          entry(0, gn, pn, cn_);
+          unsigned idn = pn ? load_ids(gn, cn_) : 0u, idn2 = 0u;
+          if (nb > 1) {
+            entry(1, gn2, pn2, cn2);
+            if (pn2) idn2 = load_ids(gn2, cn2);
+          }
+          BallA An0, An1;
+          BallB Bn0, Bn1;
+          load_recs(gn, pn, idn, An0, An1, Bn0, Bn1);
+          for (int k = 0; k < nb; ++k) {
+            const BallA A0 = An0, A1 = An1;
+            const BallB B0 = Bn0, B1 = Bn1;
+            const bool pair = pn;
+            const unsigned ids = idn;
+            if (k + 1 < nb) {   // next entry's records in flight during this setup
+              gn = gn2;
+              pn = pn2;
+              idn = idn2;
+              load_recs(gn, pn, idn, An0, An1, Bn0, Bn1);
+              if (k + 2 < nb) {
+                entry(k + 2, gn2, pn2, cn2);
+                idn2 = pn2 ? load_ids(gn2, cn2) : 0u;
+              }
+            }
+            const GroupDet gA = shfl_gd_fast(gdA_l, k);
+            const unsigned word = __shfl_sync(0xffffffffu, word_l, k);
+            const int blo = (int)(word & 0xFFFFu) << kBinShift;
+            const int ghi = blo + (int)((word >> 16) & 0x7FFFu);
+            PROF_T(t_s);
+            if (!pair) {   // single group: one ball per lane
+              const PairSetup p = pair_setup<DIR>(acq, gA, dd, A0, B0, my_ops, blo);
+              const bool empty_u = p.jlo > p.jhi;
+              const float Ak = empty_u ? 0.0f : p.Ak;
+              const float sg = Ak < 0.0f ? -1.0f : 1.0f;
+              const float nla = -__log2f(fabsf(Ak));   // +inf for Ak = 0
+#ifdef PAB_FWD_PROF
+              pp_setup += clock64() - t_s;
+#endif
+              publish(i0 + k, 0, p.L, blo, ghi, 0,
+                      make_float4(__int_as_float(p.J0), __int_as_float(empty_u ? -1 : p.jhi),
+                                  (float)(p.J0 * acq.f - p.kc), -p.sc * sg),
+                      make_float4(p.phi * p.sc * sg, nla, p.qmax + nla, 0.0f), make_float4(0.f, 0.f, 0.f, 0.f));
+              continue;
+            }
+            const GroupDet gB = shfl_gd_fast(gdB_l, k);
+            const PairSetup pa = pair_setup<DIR, false>(acq, (ids & 0xE0u) ? gB : gA, dd, A0, B0, my_ops, blo);
+            const PairSetup pb = pair_setup<DIR, false>(acq, (ids & 0xE000u) ? gB : gA, dd, A1, B1, my_ops, blo);
+            // walk parameters per ball (sgn(Ak) folded into y; empty balls: y = 0, G = 0)
+            auto params = [&](const PairSetup& p, bool e, int& J0, int& jh, float& mf, float& nsc, float& pss,
+                              float& nla) {
+              J0 = e ? blo : p.J0;
+              jh = e ? -1 : p.jhi;
+              mf = (float)(J0 * acq.f - p.kc);
+              const float sg = p.Ak < 0.0f ? -1.0f : 1.0f;
+              nsc = e ? 0.0f : -p.sc * sg;
+              pss = e ? 0.0f : p.phi * p.sc * sg;
+              nla = e ? __int_as_float(0x7f800000) : -__log2f(fabsf(p.Ak));
+            };
+            const bool ea = pa.jlo > pa.jhi, eb = pb.jlo > pb.jhi;
+            int J0a, jha, J0b, jhb;
+            float mfa, nsca, pssa, nlaa, mfb, nscb, pssb, nlab;
+            params(pa, ea, J0a, jha, mfa, nsca, pssa, nlaa);
+            params(pb, eb, J0b, jhb, mfb, nscb, pssb, nlab);
+            const int J0u = ea ? J0b : (eb ? J0a : min(J0a, J0b));
+            const int lim = max(jha, jhb);
+            // the recurrence's range guard: |y| <= kDualMaxY on every live
+            // walked sample, |dl| <= kDualMaxDl (y is linear: check the ends)
+            auto yok = [&](bool e, float mf, int J0, float nsc, float pss) {
+              if (e) return true;
+              const float m_lo = mf + (float)((J0u - J0) * acq.f), m_hi = mf + (float)((lim + 7 - J0) * acq.f);
+              return fabsf(fmaf(m_lo, nsc, pss)) <= kDualMaxY && fabsf(fmaf(m_hi, nsc, pss)) <= kDualMaxY &&
+                     fabsf(fs * nsc) <= kDualMaxDl;
+            };
+            const bool ok = __all_sync(0xffffffffu, yok(ea, mfa, J0a, nsca, pssa) && yok(eb, mfb, J0b, nscb, pssb));
+            const int Lu = __reduce_max_sync(0xffffffffu, (ea && eb) ? 0 : lim - J0u + 1);
+            const int La = ok ? 0 : __reduce_max_sync(0xffffffffu, ea ? 0 : jha - J0a + 1);
+            const int Lb = ok ? 0 : __reduce_max_sync(0xffffffffu, eb ? 0 : jhb - J0b + 1);
+#ifdef PAB_FWD_PROF
+            pp_setup += clock64() - t_s;
+#endif
+            publish(i0 + k, ok ? 1 : 2, ok ? Lu : La, blo, ghi, ok ? 0 : Lb,
+                    make_float4(__int_as_float(J0a), __int_as_float(jha), mfa, nsca),
+                    make_float4(pssa, nlaa, __int_as_float(J0b), __int_as_float(jhb)),
+                    make_float4(mfb, nscb, pssb, nlab));
+          }
+        }
+      } else
       for (int i0 = s_begin; i0 < s_end; i0 += kWarp) {
         const int nb = min(kWarp, s_end - i0);
         GroupDet gd_l;
@@ -757,8 +1128,8 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
     PROF_T(t_f);
     // ---- F: groups wider than the tile (rare): warp 0, linear passes ----
     if (warp == 0) {
-      for (int idx = n_reg; idx < n_all; ++idx) {
-        const int64_t g = cg0 + sorted[idx];
+      for (int idx = n_reg; idx < n_all; ++idx) {   // single groups only (a dual entry always fits)
+        const int64_t g = cg0 + (sorted[idx] & 0x7FFF);
         const GroupMeta gm = gmeta[g];
         const GroupDet gd = group_det(gm, det.px, det.py, det.pz, acq);
         int lo, hi;
@@ -850,12 +1221,14 @@ __global__ void decimate_kernel(const float* __restrict__ src, int n_rows, int n
 #endif
 constexpr bool kWS = PAB_FWD_WS != 0;
 
-size_t forward_smem(int n_out, int warps, bool srow) {
+size_t forward_smem(int n_out, int warps, bool srow, bool dual) {
   const size_t n_bins = (size_t)((n_out + (1 << kBinShift) - 1) >> kBinShift);
   const size_t row_bytes = srow ? (size_t)((n_out + 3) & ~3) * 4 : 0;
-  const size_t ring = kWS ? 16 + (size_t)warps * kRing * (2 * kWarp * 16 + 16 + 2 * 8) : 0;
+  const size_t slot_vecs = dual ? 3 : 2;   // float4 records per lane and ring slot
+  const size_t ring = kWS ? 16 + (size_t)warps * kRing * (slot_vecs * kWarp * 16 + 16 + 2 * 8) : 0;
+  const size_t units = kChunk;
   return row_bytes + (size_t)warps * kTileAlloc * kWarp * 4 + (size_t)warps * kTile * 4 + (n_bins + 1) * 4 +
-         (size_t)(warps + 1) * 4 + 16 + 2 * kChunk * 2 + 16 + ring;
+         (size_t)(warps + 1) * 4 + 16 + 2 * units * 2 + 16 + ring;
 }
 
 }  // namespace pab
@@ -866,14 +1239,18 @@ extern "C" {
 
 // The row stays in shared memory while two CTAs still fit on an SM
 // (2 x (smem + 1 KB reserve) <= 228 KB); longer records keep it in L2.
-static bool row_in_smem(int n_out, int warps) { return forward_smem(n_out, warps, true) <= 113 * 1024; }
+static size_t smem_both(int n_out, int warps, bool srow) {   // the larger of the single / dual layouts
+  return std::max(forward_smem(n_out, warps, srow, false), forward_smem(n_out, warps, srow, kWS && kDual));
+}
+static bool row_in_smem(int n_out, int warps) { return smem_both(n_out, warps, true) <= 113 * 1024; }
 
 size_t pab_forward_smem_bytes(int n_out, int warps, int tile_rows) {
   (void)tile_rows;
-  return forward_smem(n_out, warps, row_in_smem(n_out, warps));
+  return smem_both(n_out, warps, row_in_smem(n_out, warps));
 }
 
-int pab_forward(const void* rec_a, const void* rec_b, const void* group_meta, int64_t n_groups,
+int pab_forward(const void* rec_a, const void* rec_b, const void* group_meta, const unsigned char* pair_table,
+                int64_t n_groups,
                 const double* det_pos, const double* det_aux, int n_det, double v, double t0, double dt,
                 int f, int n_out, double cutoff, int dir_kind, double dir_param, int groups_per_cell,
                 int partitions, int warps, int tile_rows, float* partial_rows,
@@ -886,9 +1263,13 @@ int pab_forward(const void* rec_a, const void* rec_b, const void* group_meta, in
     return 1;
   if ((int64_t)n_out * f > (1 << 24)) return 1;
   const Acq acq = make_acq(v, t0, dt, f, n_out, cutoff, dir_kind, dir_param);
-  const int64_t per_part = (n_groups + partitions - 1) / partitions;
+  // per-sample truncation test only where the walk's overrun could matter
+  const bool mask = cutoff < kUnmaskedCutoff;
+  const bool dual = kWS && kDual && !mask && pair_table != nullptr;
+  int64_t per_part = (n_groups + partitions - 1) / partitions;
+  if (dual) per_part += per_part & 1;   // dual sort units (group pairs) never straddle partitions
   const bool srow = row_in_smem(n_out, warps);
-  const size_t smem = forward_smem(n_out, warps, srow);
+  const size_t smem = forward_smem(n_out, warps, srow, dual);
   if (smem > 227 * 1024) return 1;
   if (dir_kind < 0 || dir_kind > 2) return 1;
   dim3 grid((unsigned)n_det, (unsigned)partitions);
@@ -896,16 +1277,17 @@ int pab_forward(const void* rec_a, const void* rec_b, const void* group_meta, in
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     kernel<<<grid, warps * kWarp * (kWS ? 2 : 1), smem, (cudaStream_t)stream>>>(
-        (const BallA*)rec_a, (const BallB*)rec_b, (const GroupMeta*)group_meta, n_groups, det_pos, det_aux,
+        (const BallA*)rec_a, (const BallB*)rec_b, (const GroupMeta*)group_meta, pair_table, n_groups, det_pos, det_aux,
         n_det, acq, per_part, partial_rows, ops_total, status);
   };
-  // per-sample truncation test only where the walk's overrun could matter
-  const bool mask = cutoff < kUnmaskedCutoff;
   auto by_row = [&](auto k_srow, auto k_grow) { srow ? launch(k_srow) : launch(k_grow); };
-  auto by_mask = [&](auto km_s, auto km_g, auto ku_s, auto ku_g) { mask ? by_row(km_s, km_g) : by_row(ku_s, ku_g); };
+  auto by_mask = [&](auto km_s, auto km_g, auto ku_s, auto ku_g, auto kd_s, auto kd_g) {
+    mask ? by_row(km_s, km_g) : (dual ? by_row(kd_s, kd_g) : by_row(ku_s, ku_g));
+  };
 #define PAB_FWD_VARIANTS(D) \
-  by_mask(forward_kernel<D, true, true, kWS>, forward_kernel<D, true, false, kWS>,                 \
-          forward_kernel<D, false, true, kWS>, forward_kernel<D, false, false, kWS>)
+  by_mask(forward_kernel<D, true, true, kWS, false>, forward_kernel<D, true, false, kWS, false>,   \
+          forward_kernel<D, false, true, kWS, false>, forward_kernel<D, false, false, kWS, false>, \
+          forward_kernel<D, false, true, kWS, kWS && kDual>, forward_kernel<D, false, false, kWS, kWS && kDual>)
   if (dir_kind == kDirNone) PAB_FWD_VARIANTS(kDirNone);
   else if (dir_kind == kDirCosPower && dir_param == 2.0) PAB_FWD_VARIANTS(kDirCos2);
   else if (dir_kind == kDirCosPower) PAB_FWD_VARIANTS(kDirCosPower);
@@ -1006,6 +1388,23 @@ __global__ void __launch_bounds__(128, 2) walk_bench_dual_kernel(int reps, int L
   }
   out[blockIdx.x * blockDim.x + threadIdx.x] = tile[lane * 4];
 }
+// The production dual walk (two balls per lane, ratio recurrence).
+__global__ void __launch_bounds__(128, 2) walk_bench_dualrec_kernel(int reps, int L, float* out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* tile = reinterpret_cast<float*>(smem_raw) + (threadIdx.x >> 5) * kTileAlloc * kWarp;
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < kTileAlloc * kWarp; i += 32) tile[i] = 0.0f;
+  __syncwarp();
+  const float sc = 0.3f + 0.001f * lane, ps = 0.1f * lane;
+  for (int r = 0; r < reps; ++r) {
+    const int J0 = ((r * 8 + lane * 8) % kTile) & ~7;
+    const DWalk wa = make_dwalk(-sc, ps, 1.0f, -__log2f(1.0f + 0.01f * lane), (float)(-L / 2));
+    const DWalk wb = make_dwalk(-sc * 1.02f, ps + 0.05f, 1.0f, -__log2f(1.0f + 0.02f * lane), (float)(-L / 2 + 2));
+    rmw_walk_dual(tile, lane, J0, L, 1 << 30, 1.0f, wa, wb);
+    __syncwarp();
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = tile[lane * 4];
+}
 }  // namespace pab
 extern "C" int pab_bench_walk_dual(int blocks, int reps, int L, float* out, float* ms) {
   const size_t smem = 4 * kTileAlloc * kWarp * sizeof(float);
@@ -1016,6 +1415,20 @@ extern "C" int pab_bench_walk_dual(int blocks, int reps, int L, float* out, floa
   walk_bench_dual_kernel<<<blocks, 128, smem>>>(reps, L, out);
   cudaEventRecord(a);
   walk_bench_dual_kernel<<<blocks, 128, smem>>>(reps, L, out);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  cudaEventElapsedTime(ms, a, b);
+  return cudaGetLastError() == cudaSuccess ? 0 : 4;
+}
+extern "C" int pab_bench_walk_dualrec(int blocks, int reps, int L, float* out, float* ms) {
+  const size_t smem = 4 * kTileAlloc * kWarp * sizeof(float);
+  cudaFuncSetAttribute(walk_bench_dualrec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  walk_bench_dualrec_kernel<<<blocks, 128, smem>>>(reps, L, out);
+  cudaEventRecord(a);
+  walk_bench_dualrec_kernel<<<blocks, 128, smem>>>(reps, L, out);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   cudaEventElapsedTime(ms, a, b);

@@ -138,6 +138,68 @@ __global__ void pack_kernel(const double* __restrict__ pos, const double* __rest
   }
 }
 
+// Pairing table of the forward's dual walk (see pair_dir): one warp per unit
+// (lane groups 2u, 2u+1); lane l holds balls l and 32 + l of the unit.  For
+// each direction the 64 projections are bitonic-sorted (key = order-preserving
+// float bits with the ball id in the low 6 bits: deterministic, ties by id)
+// and written as 64 ball ids.  Performance only: any table gives the same
+// sums up to FP32 summation order.
+__device__ __forceinline__ unsigned orderable(float f) {
+  const unsigned u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__device__ __forceinline__ void bitonic64(unsigned& x0, unsigned& x1, int lane) {
+#pragma unroll
+  for (int k = 2; k <= 64; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j == 32) {   // partner in the other register (k = 64: ascending)
+        const unsigned a = min(x0, x1), b = max(x0, x1);
+        x0 = a;
+        x1 = b;
+      } else {
+        const bool up0 = k == 64 ? true : (k == 32 ? true : (lane & k) == 0);
+        const bool up1 = k == 64 ? true : (k == 32 ? false : (lane & k) == 0);
+        const bool lower = (lane & j) == 0;
+        const unsigned o0 = __shfl_xor_sync(0xffffffffu, x0, j);
+        const unsigned o1 = __shfl_xor_sync(0xffffffffu, x1, j);
+        x0 = (lower == up0) ? min(x0, o0) : max(x0, o0);
+        x1 = (lower == up1) ? min(x1, o1) : max(x1, o1);
+      }
+    }
+  }
+}
+
+__global__ void pair_table_kernel(const BallA* __restrict__ ra, const GroupMeta* __restrict__ gm, int64_t n_units,
+                                  int64_t n_groups, unsigned char* __restrict__ table) {
+  const int lane = threadIdx.x & 31;
+  const int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (u >= n_units) return;
+  const int64_t g0 = 2 * u;
+  const bool hasB = g0 + 1 < n_groups;
+  const GroupMeta ma = gm[g0];
+  const BallA a = ra[g0 * kWarp + lane];
+  float bx = 0.f, by = 0.f, bz = 0.f;
+  if (hasB) {   // second group's balls relative to the first group's centre
+    const GroupMeta mb = gm[g0 + 1];
+    const BallA b = ra[(g0 + 1) * kWarp + lane];
+    bx = (float)(mb.cx - ma.cx) + b.dx;
+    by = (float)(mb.cy - ma.cy) + b.dy;
+    bz = (float)(mb.cz - ma.cz) + b.dz;
+  }
+  unsigned char* out = table + (size_t)u * kPairDirs * 64;
+  for (int k = 0; k < kPairDirs; ++k) {
+    float ux, uy, uz;
+    pair_dir(k, &ux, &uy, &uz);
+    unsigned x0 = (orderable(a.dx * ux + a.dy * uy + a.dz * uz) & ~63u) | (unsigned)lane;
+    unsigned x1 = (orderable(bx * ux + by * uy + bz * uz) & ~63u) | (unsigned)(32 + lane);
+    bitonic64(x0, x1, lane);
+    out[k * 64 + lane] = (unsigned char)(x0 & 63u);
+    out[k * 64 + 32 + lane] = (unsigned char)(x1 & 63u);
+  }
+}
+
 }  // namespace pab
 
 using namespace pab;
@@ -166,6 +228,19 @@ int pab_pack(const double* pos, const double* p0, const double* a0, const int32_
       pos, p0, a0, perm, n, n_groups, (BallA*)rec_a, (BallB*)rec_b, (GroupMeta*)group_meta);
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
+
+int pab_pair_table(const void* rec_a, const void* group_meta, int64_t n_groups, unsigned char* table,
+                   void* stream) {
+  if (n_groups <= 0) return 0;
+  if (!rec_a || !group_meta || !table) return 1;
+  const int64_t n_units = (n_groups + 1) / 2;
+  const int warps = 8;
+  pair_table_kernel<<<(unsigned)((n_units + warps - 1) / warps), warps * kWarp, 0, (cudaStream_t)stream>>>(
+      (const BallA*)rec_a, (const GroupMeta*)group_meta, n_units, n_groups, table);
+  return cudaGetLastError() == cudaSuccess ? 0 : 4;
+}
+
+size_t pab_pair_table_bytes(int64_t n_groups) { return (size_t)((n_groups + 1) / 2) * kPairDirs * 64; }
 
 int pab_record_sizes(int* ball_a, int* ball_b, int* group_meta) {
   *ball_a = (int)sizeof(BallA);

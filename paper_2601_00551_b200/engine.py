@@ -150,6 +150,7 @@ class DeviceCloud:
         """Parameters changed: repack before the next pass (and resort)."""
         self._packed = False
         self._stats = None
+        self._ptable_ok = False
         if resort:
             self.perm = None
 
@@ -186,6 +187,19 @@ class DeviceCloud:
                  ptr(self.rec_a), ptr(self.rec_b), ptr(self.gmeta), _stream())
         self._packed = True
         self._stats = None
+        self._ptable_ok = False
+
+    def pair_table(self) -> torch.Tensor:
+        """Dual-walk pairing table of the packed cloud (built on first use
+        after each pack; the forward's performance aid, not its numerics)."""
+        if not getattr(self, "_ptable_ok", False):
+            nbytes = int(_lib.load().pab_pair_table_bytes(self.n_groups))
+            if not hasattr(self, "ptable") or self.ptable.numel() < max(nbytes, 1):
+                self.ptable = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=self.dev)
+            if self.n:
+                call("pab_pair_table", ptr(self.rec_a), ptr(self.gmeta), self.n_groups, ptr(self.ptable), _stream())
+            self._ptable_ok = True
+        return self.ptable
 
     def stats(self) -> tuple[float, float]:
         """(median lane-group radius, max a0) for launch planning."""
@@ -308,7 +322,8 @@ def forward_rows(cloud: DeviceCloud, det: DeviceDetectors, acq: Acq, counters: P
     partial = ws.get("partial_rows", plan.partitions * J * n_out, torch.float32)
     loss_rows = ws.get("loss_rows", J, torch.float64) if real_local is not None else None
     if cloud.n_groups > 0:
-        call("pab_forward", ptr(cloud.rec_a), ptr(cloud.rec_b), ptr(cloud.gmeta), cloud.n_groups,
+        call("pab_forward", ptr(cloud.rec_a), ptr(cloud.rec_b), ptr(cloud.gmeta), ptr(cloud.pair_table()),
+             cloud.n_groups,
              ptr(det.pos), ptr(det.aux), J, det.sound_speed, acq.t0, acq.dt, acq.f, n_out, acq.cutoff,
              acq.dir_kind, acq.dir_param, plan.groups_per_cell, plan.partitions, plan.warps,
              plan.tile_rows, ptr(partial), ptr(counters.ops), ptr(counters.status), _stream())

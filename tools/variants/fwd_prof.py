@@ -31,6 +31,7 @@ for it in range(2):
 lib.pab_fwd_prof(buf, 0)
 v = list(buf)
 ops = int(c.ops.item())
+print(f"dual units {v[15]}, single-fallback units {v[14]} (walked lane-samples count ball-slots once per lane)")
 print(f"walked lane-samples {v[11]:.4e} (regular groups {v[12]}), in-window samples {ops:.4e}: walked/useful {v[11] / ops:.3f}")
 names_w = {0: "A bin", 1: "A sync", 2: "B sort+sync", 3: "D sweep", 4: "D end sync", 5: "E merge", 7: "F oversize+sync",
            6: "  D: final flush", 13: "  D: ring loop total", 8: "  D: wait full", 9: "  D: make_room flush", 10: "  D: walk"}

@@ -27,3 +27,9 @@ for L in (48,):
     rc = lib.pab_bench_walk_dual(sms * 2, reps, L, ctypes.c_void_p(out.data_ptr()), ctypes.byref(ms))
     samples = 2 * sms * 2 * 128 * reps * L   # two balls per lane
     print(f"dual L={L}: rc={rc} {ms.value:.2f} ms, {samples / (ms.value * 1e-3) / 1e12:.2f} T ball-samples/s")
+for L in (48, 96):
+    reps = 4000
+    ms = ctypes.c_float()
+    rc = lib.pab_bench_walk_dualrec(sms * 2, reps, L, ctypes.c_void_p(out.data_ptr()), ctypes.byref(ms))
+    samples = 2 * sms * 2 * 128 * reps * L   # two balls per lane
+    print(f"dual-recurrence L={L}: rc={rc} {ms.value:.2f} ms, {samples / (ms.value * 1e-3) / 1e12:.2f} T ball-samples/s")
