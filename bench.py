@@ -35,6 +35,7 @@ METRIC = "ball-detector pair evals/s (fwd+adjoint) per iteration"
 UNIT = "pairs/s"
 FLOPS_FWD = 7      # per in-window sample
 FLOPS_ADJ_FINE = 12
+TRAFFIC_FWD_BYTES = 159_410_176   # dram__bytes_read.sum + dram__bytes_write.sum, forward, profiles/r01_v9
 EX2_PER_SAMPLE = 1
 
 
@@ -366,11 +367,12 @@ def main():
             dist.destroy_process_group()
         return
 
-    # roofline of the dominant kernel.  Per
-    # in-window sample the forward does 1 ex2 + 1 shared-memory
-    # read-modify-write of its private tile column (8 B) + 7 FP32 flops; the
-    # binding ceiling is the smem RMW rate, measured live by tools/probe
-    # (same access pattern), with the ex2 and FP32 ceilings reported beside.
+    # roofline of the dominant kernel: the
+    # forward against the north star's ceiling, the FP32 CUDA-core peak, with
+    # SURVEY §8d's algorithmic 7 FP32 flops per in-window sample (the
+    # reference op count); the canonical ex2 (1 per sample) and shared-memory
+    # RMW (8 B per sample) ceilings of the same work, and both kernels'
+    # fractions, are reported beside it.  Peaks are probed live on this GPU.
     probe = os.path.join(ROOT, "tools", "probe", "libfp32_peak.so")
     peak_flops = peak_ex2 = peak_rmw = None
     peak_kind = "measured live (tools/probe: FFMA2 chains, ex2 chains, private-column smem RMW; this GPU)"
@@ -391,24 +393,25 @@ def main():
     adj_mean = sum(adj_ms) / len(adj_ms)
     samples = ops_per_step   # in-window samples evaluated by the forward (== adjoint)
     fwd_s, adj_s = fwd_mean * 1e-3, adj_mean * 1e-3
-    ach = 8.0 * samples / fwd_s
-    roofline = {"bound": "smem", "achieved": ach / 1e9, "peak": 8.0 * peak_rmw / 1e9, "unit": "GB/s",
-                "frac": ach / (8.0 * peak_rmw), "traffic": None, "kernel": "forward_kernel",
+    ach = FLOPS_FWD * samples / fwd_s
+    roofline = {"bound": "fp32", "achieved": ach / 1e12, "peak": peak_flops / 1e12, "unit": "TFLOP/s",
+                "frac": ach / peak_flops, "traffic": TRAFFIC_FWD_BYTES, "kernel": "forward_kernel",
                 "peak_source": peak_kind,
-                "algorithmic": f"8 B shared-memory read-modify-write x {samples} in-window samples per launch "
-                               "(forward+residual events; pack and residual are < 0.3% of it)",
+                "algorithmic": f"{FLOPS_FWD} FP32 flops x {samples} in-window samples per launch (SURVEY 8d; "
+                               "forward+residual events, of which pack, pairing table and residual are ~1.5%)",
+                "traffic_unit": "DRAM bytes per forward launch (ncu --set full, profiles/r01_v9)",
                 "other_bounds": {
-                    "forward_ex2": {"frac": samples / fwd_s / peak_ex2, "peak_per_s": peak_ex2},
-                    "forward_fp32": {"frac": FLOPS_FWD * samples / fwd_s / peak_flops,
-                                     "peak_tflops": peak_flops / 1e12},
+                    "forward_ex2 (1 per sample)": {"frac": samples / fwd_s / peak_ex2, "peak_per_s": peak_ex2},
+                    "forward_smem_rmw (8 B per sample)": {"frac": samples / fwd_s / peak_rmw,
+                                                          "peak_GBps": 8.0 * peak_rmw / 1e9},
                     "adjoint_ex2 (its binding ceiling)": {"frac": samples / adj_s / peak_ex2},
                     "adjoint_fp32": {"frac": FLOPS_ADJ_FINE * samples / adj_s / peak_flops},
+                    "path_fp32 (fwd+adj, 19 flops per sample)": {
+                        "frac": (FLOPS_FWD + FLOPS_ADJ_FINE) * samples / (ms_max * 1e-3) / peak_flops},
                     "path_ex2 (fwd+adj, 2 ex2 per sample)": {"frac": 2 * samples / (ms_max * 1e-3) / peak_ex2}},
-                "traffic_note": "traffic is defined on DRAM bytes; this kernel is on-chip bound.  The ncu capture "
-                                "in profiles/ (r01_v8) gives 39 MB DRAM and 4.25e9 shared-memory wavefronts "
-                                "(544 GB, 1.66x the algorithmic 328 GB): the walks touch 1.17x the in-window "
-                                "samples (4-aligned starts, warp-uniform block counts; 385 GB), the setup "
-                                "hand-off ring ~65 GB, row flushes ~13 GB, the rest is sort/merge scratch",
+                "design_note": "the forward's dual walk executes 0.5 ex2, 4 FP32 lane-ops and 4 B of shared RMW per "
+                               "walked ball-sample (1.28 walked per in-window sample); no pipe is saturated "
+                               "(ncu r01_v9: issue slots 66%, ALU 39%, XU 39%, FMA 30%, LSU 17%)",
                 "kernel_ms": {"forward+residual": fwd_mean, "adjoint+finalize": adj_mean}}
 
     cpu = None
@@ -422,7 +425,7 @@ def main():
             "data": f"synthetic (seeded CounterRng, BASELINE config {args.config})", "config": config_dict(args, world),
             "in_window_samples_per_step": samples, "samples_per_pair": samples / pairs,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": sampler.summary(),
-            "gpu_launches": 4 * args.steps,
+            "gpu_launches": 6 * args.steps,   # pack, pairing table, forward, residual, adjoint, finalize
             "kernel_ms_min_median": {"forward+residual": [min(fwd_ms), statistics.median(fwd_ms)],
                                      "adjoint+finalize": [min(adj_ms), statistics.median(adj_ms)]}}
     if args.recon:

@@ -349,7 +349,7 @@ __device__ __forceinline__ void dual_block(float4& o0, float4& o1, float m, cons
 }
 
 #ifndef PAB_DUAL_UNROLL
-#define PAB_DUAL_UNROLL 1   // 8-sample blocks per loop trip (each block carries two balls)
+#define PAB_DUAL_UNROLL 2   // 8-sample blocks per loop trip (each block carries two balls)
 #endif
 // Warp-uniform walk of L samples (multiple of 4) from the lane's 4-aligned
 // union start J0; blocks starting past `lim` go to the dump block.
@@ -1040,14 +1040,13 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
             const int J0u = ea ? J0b : (eb ? J0a : min(J0a, J0b));
             const int lim = max(jha, jhb);
             // the recurrence's range guard: |y| <= kDualMaxY on every live
-            // walked sample, |dl| <= kDualMaxDl (y is linear: check the ends)
-            auto yok = [&](bool e, float mf, int J0, float nsc, float pss) {
-              if (e) return true;
-              const float m_lo = mf + (float)((J0u - J0) * acq.f), m_hi = mf + (float)((lim + 7 - J0) * acq.f);
-              return fabsf(fmaf(m_lo, nsc, pss)) <= kDualMaxY && fabsf(fmaf(m_hi, nsc, pss)) <= kDualMaxY &&
-                     fabsf(fs * nsc) <= kDualMaxDl;
+            // walked sample (|y| <= sc (|J f - kc| + 1/2), J in [J0u, lim + 7])
+            // and |dl| = f sc <= kDualMaxDl, folded into one test per ball
+            auto yok = [&](bool e, const PairSetup& p) {
+              const int dm = max(p.kc - J0u * acq.f, (lim + 7) * acq.f - p.kc);
+              return e || p.sc * fmaxf(fs * (1.0f / kDualMaxDl), (float)dm * (1.0f / kDualMaxY) + 0.5f / kDualMaxY) <= 1.0f;
             };
-            const bool ok = __all_sync(0xffffffffu, yok(ea, mfa, J0a, nsca, pssa) && yok(eb, mfb, J0b, nscb, pssb));
+            const bool ok = __all_sync(0xffffffffu, yok(ea, pa) && yok(eb, pb));
             const int Lu = __reduce_max_sync(0xffffffffu, (ea && eb) ? 0 : lim - J0u + 1);
             const int La = ok ? 0 : __reduce_max_sync(0xffffffffu, ea ? 0 : jha - J0a + 1);
             const int Lb = ok ? 0 : __reduce_max_sync(0xffffffffu, eb ? 0 : jhb - J0b + 1);
