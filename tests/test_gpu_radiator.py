@@ -518,3 +518,51 @@ def test_unaligned_and_long_records_match_oracle(P, n_samples, f):
     assert rel_l2(gr.d_p0, gp0) < GRAD_TOL
     assert rel_l2(gr.d_a0, ga0) < GRAD_TOL
     assert rel_l2(gr.d_position, gpos) < GRAD_TOL
+
+
+# ------------------------------------------------------------- dual walk
+
+def test_dual_walk_equals_single_walk(P, monkeypatch):
+    """The forward's dual walk (two balls per lane, ratio recurrence, pairing
+    table) against the single walk (PAB_FORWARD_DUAL=0) and the oracle on a
+    config-2 slice: the two agree to FP32 summation order."""
+    from paper_2601_00551_b200 import scenes
+    sc = scenes.microbench_config(n_balls=20000, n_det=1024)
+    sens, nrm = sc.array.positions[::32], sc.array.normals[::32]
+    ctx = P.ForwardContext(P.SensorArray(sens, 1500.0, normals=nrm), sc.grid,
+                           directivity=P.Directivity("cos_power", power=2.0))
+    t = sc.truth
+    real, _, _, ops = OR.run_model(t.positions, t.p0, t.a0, sens, nrm, 1500.0, 0.0, sc.grid.dt, 4096, 1,
+                                   kind=("cos_power", 2.0), threads=8)
+    P.reset_op_count()
+    dual = P.simulate_signals(t, ctx).data
+    ops_dual = P.op_count()
+    monkeypatch.setenv("PAB_FORWARD_DUAL", "0")
+    P.reset_op_count()
+    single = P.simulate_signals(t, ctx).data
+    assert P.op_count() == ops_dual
+    assert abs(ops_dual - ops) <= 1e-4 * ops
+    assert rel_l2(dual, single) < 5e-6
+    assert rel_l2(dual, real) < SIG_TOL
+    assert rel_l2(single, real) < SIG_TOL
+
+
+@pytest.mark.parametrize("a0_mm,f,n", [(0.02, 1, 32 * 124 + 17), (0.1, 2, 32 * 124 + 17), (0.1, 1, 32 * 61 + 5)])
+def test_dual_walk_guards_match_oracle(P, a0_mm, f, n):
+    """Dual-walk edge cases: steps |dl| = f v dt sqrt(log2(e)/2) / a0 above
+    the recurrence bound (a0 = 0.02 mm at f = 1: the pair falls back to two
+    single walks), a decimated level (f = 2), and group counts whose last
+    pair of lane groups is incomplete (odd group count, ragged last group)."""
+    rng = np.random.default_rng(53)
+    pos = rng.uniform(-3e-3, 3e-3, (n, 3))
+    p0 = rng.uniform(0.2, 1.0, n)
+    a0 = np.full(n, a0_mm * 1e-3) * rng.uniform(0.9, 1.1, n)
+    ang = rng.uniform(0, 2 * np.pi, 12)
+    sens = np.column_stack([0.03 * np.cos(ang), 0.03 * np.sin(ang), rng.uniform(-0.01, 0.01, 12)])
+    grid = P.TimeGrid(0.0, 2.5e-8, 2048)
+    ctx = P.ForwardContext(P.SensorArray(sens, 1500.0), grid)
+    rows, _, _, ops = OR.run_model(pos, p0, a0, sens, None, 1500.0, 0.0, grid.dt, grid.n_samples, f)
+    P.reset_op_count()
+    got = P.simulate_at_rate(P.PointCloud(pos, p0, a0), ctx, f).data
+    assert rel_l2(got, rows) < SIG_TOL
+    assert abs(P.op_count() - ops) <= 2
