@@ -35,7 +35,7 @@ METRIC = "ball-detector pair evals/s (fwd+adjoint) per iteration"
 UNIT = "pairs/s"
 FLOPS_FWD = 7      # per in-window sample
 FLOPS_ADJ_FINE = 12
-TRAFFIC_FWD_BYTES = 159_410_176   # dram__bytes_read.sum + dram__bytes_write.sum, forward, profiles/r01_v9
+TRAFFIC_FWD_BYTES = 138_801_920   # dram__bytes_read.sum + dram__bytes_write.sum, forward, profiles/r01_v9
 EX2_PER_SAMPLE = 1
 
 
