@@ -60,7 +60,8 @@ int pab_pack(const double* pos, const double* p0, const double* a0, const int32_
 
 /* Dual-walk pairing table of a packed cloud (performance only): for each pair
  * of consecutive lane groups and each of 64 fixed directions, the 64 balls in
- * projection order (pab_pair_table_bytes(n_groups) bytes).  Rebuild after
+ * projection order, laid out [cell][unit][64] (pab_pair_table_bytes(n_groups)
+ * bytes).  Rebuild after
  * every pab_pack.
  * Replaces: nothing (the reference evaluates balls one by one). */
 size_t pab_pair_table_bytes(int64_t n_groups);

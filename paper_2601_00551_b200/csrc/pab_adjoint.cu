@@ -270,7 +270,11 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   // the uniform walk must stay inside the staged samples + zero padding
   // (cover window <= 2 rho / f + 3 samples, + 3 alignment + 3 rounding)
   const bool fits = 2.0f * (acq.cutoff * gm.a0max * acq.inv_vdt_f) * acq.inv_f + 12.0f <= (float)kPad;
-  double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  // per-ball FP64 sums across the chunk, in shared memory (registers stay
+  // with the moment walk: measured 0.6% faster than register accumulators)
+  __shared__ double acc_s[kAdjWarps][5][kWarp];
+#pragma unroll
+  for (int c = 0; c < 5; ++c) acc_s[warp][c][lane] = 0.0;
   unsigned long long my_ops = 0;
   int coinc = 0;
 #ifdef PAB_ADJ_PROF
@@ -491,7 +495,7 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
     }
     __syncwarp();
 #pragma unroll
-    for (int c = 0; c < 5; ++c) acc[c] += (double)gb[c];
+    for (int c = 0; c < 5; ++c) acc_s[warp][c][lane] += (double)gb[c];
   }
 #ifdef PAB_ADJ_PROF
   APROF_ACC(7, t_all);
@@ -500,7 +504,7 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
 #endif
   double* out = gpart + (size_t)q * 5 * n_pad;
 #pragma unroll
-  for (int c = 0; c < 5; ++c) out[c * n_pad + bi] = acc[c];
+  for (int c = 0; c < 5; ++c) out[c * n_pad + bi] = acc_s[warp][c][lane];
   for (int o = 16; o > 0; o >>= 1) {
     my_ops += __shfl_xor_sync(0xffffffffu, my_ops, o);
     coinc |= __shfl_xor_sync(0xffffffffu, coinc, o);

@@ -73,6 +73,13 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
 // issue slots to the walker sharing its scheduler.
 __device__ __forceinline__ void mbar_wait_backoff(unsigned long long* b, unsigned parity) {
   const unsigned a = (unsigned)__cvta_generic_to_shared(b);
+#ifdef PAB_FWD_SUSPEND_NS   // hardware-suspended wait (time-limit hint) instead of polling
+  asm volatile(
+      "{\n .reg .pred p;\n WAITS_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n @!p bra WAITS_%=;\n}" ::"r"(a),
+      "r"(parity), "r"((unsigned)PAB_FWD_SUSPEND_NS)
+      : "memory");
+  return;
+#endif
   unsigned ok;
   for (;;) {
     asm volatile(
@@ -571,8 +578,9 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   const size_t ring_off = (reinterpret_cast<unsigned char*>(gbin + kCU) - smem_raw + 15) & ~(size_t)15;
   float4* slot_a = reinterpret_cast<float4*>(smem_raw + ring_off);
   float4* slot_b = slot_a + W * kRing * kWarp;
-  float4* slot_c = slot_b + W * kRing * kWarp;   // DUAL only
-  int4* slot_h = reinterpret_cast<int4*>(slot_b + (DUAL ? 2 : 1) * W * kRing * kWarp);
+  float2* slot_c = reinterpret_cast<float2*>(slot_b + W * kRing * kWarp);   // DUAL only
+  int4* slot_h = DUAL ? reinterpret_cast<int4*>(slot_c + W * kRing * kWarp)
+                      : reinterpret_cast<int4*>(slot_b + W * kRing * kWarp);
   unsigned long long* mb_full = reinterpret_cast<unsigned long long*>(slot_h + W * kRing);
   unsigned long long* mb_empty = mb_full + W * kRing;
 
@@ -773,12 +781,13 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
           const float4 ra4 = slot_a[(warp * kRing + sl) * kWarp + lane];
           const float4 rb4 = slot_b[(warp * kRing + sl) * kWarp + lane];
           const int mode = h.w & 3;
-          float4 rc4;
-          if (DUAL && mode != 0) rc4 = slot_c[(warp * kRing + sl) * kWarp + lane];
+          float2 rc2;
+          if (DUAL && mode != 0) rc2 = slot_c[(warp * kRing + sl) * kWarp + lane];
           mbar_arrive(&mb_empty[warp * kRing + sl]);
           if (DUAL && mode != 0) {
-            // record: a = (J0a, jhia, mfa, nsca), b = (pssa, nlaa, J0b, jhib),
-            // c = (mfb, nscb, pssb, nlab); header (Lu | La, blo, ghi, mode | Lb << 16)
+            // record (40 B per lane): a = (J0a | jha << 16, J0b | jhb << 16, mfa, nsca),
+            // b = (pssa, nlaa, mfb, nscb), c = (pssb, nlab), jh = 0xFFFF: empty;
+            // header (Lu | La, blo, ghi, mode | Lb << 16)
             PROF_T(t_r2);
             make_room(h.y, h.z);
             PROF_ACC(pw_room, t_r2);
@@ -788,21 +797,22 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
             if (lane == 0) atomicAdd(&g_fwd_prof[mode == 2 ? 14 : 15], 1ull);
 #endif
             PROF_T(t_k2);
-            const int J0a = __float_as_int(ra4.x), jha = __float_as_int(ra4.y);
-            const int J0b = __float_as_int(rb4.z), jhb = __float_as_int(rb4.w);
+            const unsigned wa_ = __float_as_uint(ra4.x), wb_ = __float_as_uint(ra4.y);
+            const int J0a = (int)(wa_ & 0xFFFFu), jha = (wa_ >> 16) == 0xFFFFu ? -1 : (int)(wa_ >> 16);
+            const int J0b = (int)(wb_ & 0xFFFFu), jhb = (wb_ >> 16) == 0xFFFFu ? -1 : (int)(wb_ >> 16);
             if (mode == 1) {   // dual walk over the lane's union window
               if (h.x > 0) {
                 const int J0u = jha < 0 ? J0b : (jhb < 0 ? J0a : min(J0a, J0b));
                 const DWalk wa = make_dwalk(ra4.w, rb4.x, fs, rb4.y, ra4.z + (float)((J0u - J0a) * acq.f));
-                const DWalk wb = make_dwalk(rc4.y, rc4.z, fs, rc4.w, rc4.x + (float)((J0u - J0b) * acq.f));
+                const DWalk wb = make_dwalk(rb4.w, rc2.x, fs, rc2.y, rb4.z + (float)((J0u - J0b) * acq.f));
                 rmw_walk_dual(tile, lane, J0u, (h.x + 3) & ~3, max(jha, jhb), fs, wa, wb);
               }
             } else {           // the pair's windows lie far apart: two single walks
               const int La = h.x, Lb = h.w >> 16;
               if (La > 0) rmw_walk<false>(tile, lane, J0a, (La + 3) & ~3, jha, ra4.z, fs,
                                          make_walk(ra4.w, rb4.x, fs, rb4.y, 0.0f));
-              if (Lb > 0) rmw_walk<false>(tile, lane, J0b, (Lb + 3) & ~3, jhb, rc4.x, fs,
-                                         make_walk(rc4.y, rc4.z, fs, rc4.w, 0.0f));
+              if (Lb > 0) rmw_walk<false>(tile, lane, J0b, (Lb + 3) & ~3, jhb, rb4.z, fs,
+                                         make_walk(rb4.w, rc2.x, fs, rc2.y, 0.0f));
             }
             __syncwarp();
             PROF_ACC(pw_walk, t_k2);
@@ -912,8 +922,9 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
         // dual entry: lane l walks the balls at positions 2l, 2l+1 of the
         // unit's projection order for the detector direction's cell (ball
         // ids 0-31 first group, 32-63 second: record g0 * 32 + id)
+        const int64_t n_units = (n_groups + 1) / 2;
         auto load_ids = [&](int64_t g0, int cell) -> unsigned {
-          return reinterpret_cast<const unsigned short*>(ptab + ((size_t)(g0 >> 1) * kPairDirs + cell) * 64)[lane];
+          return reinterpret_cast<const unsigned short*>(ptab + ((size_t)cell * n_units + (g0 >> 1)) * 64)[lane];
         };
         auto load_recs = [&](int64_t g0, bool pair, unsigned ids, BallA& A0, BallA& A1, BallB& B0, BallB& B1) {
           const int64_t bi = pair ? g0 * kWarp + (ids & 0xFFu) : g0 * kWarp + lane;
@@ -924,7 +935,7 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
             B1 = rb[g0 * kWarp + (ids >> 8)];
           }
         };
-        auto publish = [&](int i, int mode, int x, int blo, int ghi, int hw, float4 va, float4 vb, float4 vc) {
+        auto publish = [&](int i, int mode, int x, int blo, int ghi, int hw, float4 va, float4 vb, float2 vc) {
           const int sl = i % kRing;
           PROF_T(t_pw);
           mbar_wait_backoff(&mb_empty[w * kRing + sl], (ring_par >> sl) & 1u);
@@ -962,7 +973,11 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
               ghi = max(ghi, hi);
             }
             word_l = (unsigned)bin | ((unsigned)(ghi - (bin << kBinShift)) << 16) | (pair ? 0x80000000u : 0u);
+#ifdef PAB_FWD_CELL0   // tuning builds: one pairing cell for every detector (table locality test)
+            cell_l = 36;
+#else
             cell_l = pair ? pair_cell(gdA_l.Sx, gdA_l.Sy, gdA_l.Sz) : 0;
+#endif
           }
           PROF_ACC(pp_geo, t_g);
           // two-stage prefetch: pairing ids two entries ahead, records one ahead
@@ -1015,7 +1030,7 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
               publish(i0 + k, 0, p.L, blo, ghi, 0,
                       make_float4(__int_as_float(p.J0), __int_as_float(empty_u ? -1 : p.jhi),
                                   (float)(p.J0 * acq.f - p.kc), -p.sc * sg),
-                      make_float4(p.phi * p.sc * sg, nla, p.qmax + nla, 0.0f), make_float4(0.f, 0.f, 0.f, 0.f));
+                      make_float4(p.phi * p.sc * sg, nla, p.qmax + nla, 0.0f), make_float2(0.f, 0.f));
               continue;
             }
             const GroupDet gB = shfl_gd_fast(gdB_l, k);
@@ -1054,9 +1069,9 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
             pp_setup += clock64() - t_s;
 #endif
             publish(i0 + k, ok ? 1 : 2, ok ? Lu : La, blo, ghi, ok ? 0 : Lb,
-                    make_float4(__int_as_float(J0a), __int_as_float(jha), mfa, nsca),
-                    make_float4(pssa, nlaa, __int_as_float(J0b), __int_as_float(jhb)),
-                    make_float4(mfb, nscb, pssb, nlab));
+                    make_float4(__uint_as_float((unsigned)J0a | ((unsigned)jha << 16)),
+                                __uint_as_float((unsigned)J0b | ((unsigned)jhb << 16)), mfa, nsca),
+                    make_float4(pssa, nlaa, mfb, nscb), make_float2(pssb, nlab));
           }
         }
       } else
@@ -1223,8 +1238,8 @@ constexpr bool kWS = PAB_FWD_WS != 0;
 size_t forward_smem(int n_out, int warps, bool srow, bool dual) {
   const size_t n_bins = (size_t)((n_out + (1 << kBinShift) - 1) >> kBinShift);
   const size_t row_bytes = srow ? (size_t)((n_out + 3) & ~3) * 4 : 0;
-  const size_t slot_vecs = dual ? 3 : 2;   // float4 records per lane and ring slot
-  const size_t ring = kWS ? 16 + (size_t)warps * kRing * (slot_vecs * kWarp * 16 + 16 + 2 * 8) : 0;
+  const size_t rec_bytes = dual ? 40 : 32;   // hand-off record per lane and ring slot
+  const size_t ring = kWS ? 16 + (size_t)warps * kRing * (rec_bytes * kWarp + 16 + 2 * 8) : 0;
   const size_t units = kChunk;
   return row_bytes + (size_t)warps * kTileAlloc * kWarp * 4 + (size_t)warps * kTile * 4 + (n_bins + 1) * 4 +
          (size_t)(warps + 1) * 4 + 16 + 2 * units * 2 + 16 + ring;
@@ -1264,7 +1279,9 @@ int pab_forward(const void* rec_a, const void* rec_b, const void* group_meta, co
   const Acq acq = make_acq(v, t0, dt, f, n_out, cutoff, dir_kind, dir_param);
   // per-sample truncation test only where the walk's overrun could matter
   const bool mask = cutoff < kUnmaskedCutoff;
-  const bool dual = kWS && kDual && !mask && pair_table != nullptr;
+  // dual walk: needs the pairing table, 16-bit row fields and two CTAs per SM
+  const bool dual = kWS && kDual && !mask && pair_table != nullptr && n_out < 65535 &&
+                    2 * (forward_smem(n_out, warps, row_in_smem(n_out, warps), true) + 1024) <= 228 * 1024;
   int64_t per_part = (n_groups + partitions - 1) / partitions;
   if (dual) per_part += per_part & 1;   // dual sort units (group pairs) never straddle partitions
   const bool srow = row_in_smem(n_out, warps);

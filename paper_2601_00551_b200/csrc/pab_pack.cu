@@ -188,15 +188,17 @@ __global__ void pair_table_kernel(const BallA* __restrict__ ra, const GroupMeta*
     by = (float)(mb.cy - ma.cy) + b.dy;
     bz = (float)(mb.cz - ma.cz) + b.dz;
   }
-  unsigned char* out = table + (size_t)u * kPairDirs * 64;
+  // layout [cell][unit][64]: a detector's CTAs read one cell's rows, whose
+  // working set (64 B per unit) stays in L2 even when the whole table does not
   for (int k = 0; k < kPairDirs; ++k) {
+    unsigned char* out = table + ((size_t)k * n_units + u) * 64;
     float ux, uy, uz;
     pair_dir(k, &ux, &uy, &uz);
     unsigned x0 = (orderable(a.dx * ux + a.dy * uy + a.dz * uz) & ~63u) | (unsigned)lane;
     unsigned x1 = (orderable(bx * ux + by * uy + bz * uz) & ~63u) | (unsigned)(32 + lane);
     bitonic64(x0, x1, lane);
-    out[k * 64 + lane] = (unsigned char)(x0 & 63u);
-    out[k * 64 + 32 + lane] = (unsigned char)(x1 & 63u);
+    out[lane] = (unsigned char)(x0 & 63u);
+    out[32 + lane] = (unsigned char)(x1 & 63u);
   }
 }
 

@@ -16,8 +16,13 @@ from paper_2601_00551_b200 import engine as E  # noqa: E402
 from paper_2601_00551_b200 import radiator as R  # noqa: E402
 from paper_2601_00551_b200 import scenes  # noqa: E402
 
-sc = scenes.microbench_config()
-ctx = P.ForwardContext(sc.array, sc.grid, directivity=P.Directivity("cos_power", power=2.0))
+if os.environ.get("CONFIG") == "4":
+    sc = scenes.planar_config(n_balls=int(os.environ.get("N", "4000000")))
+    ctx = P.ForwardContext(sc.array, sc.grid, directivity=P.Directivity(
+        "none") if os.environ.get("DIR") == "none" else P.Directivity("element", width=0.5e-3))
+else:
+    sc = scenes.microbench_config()
+    ctx = P.ForwardContext(sc.array, sc.grid, directivity=P.Directivity("cos_power", power=2.0))
 det = R.device_detectors(ctx)
 acq = R._acq(ctx, 1)
 dc = E.DeviceCloud.from_host(sc.init.positions, sc.init.p0, sc.init.a0, torch.device("cuda", 0))
