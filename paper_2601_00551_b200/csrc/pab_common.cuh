@@ -228,11 +228,19 @@ __device__ __forceinline__ float dir_weight(const DetDir& dd, float hx, float hy
   const float s2 = dd.e2x * hx + dd.e2y * hy + dd.e2z * hz;
   const float sc = 0.5f * width * inv_a0;
   const float x1 = sc * s1, x2 = sc * s2;
-  float f1, g1, f2, g2;
-  if (fabsf(x1) < 1e-3f) { f1 = 1.0f - x1 * x1 * (1.0f / 6.0f); g1 = -x1 * (1.0f / 3.0f); }
-  else { float sn, cs; __sincosf(x1, &sn, &cs); f1 = sn / x1; g1 = (cs - f1) / x1; }
-  if (fabsf(x2) < 1e-3f) { f2 = 1.0f - x2 * x2 * (1.0f / 6.0f); g2 = -x2 * (1.0f / 3.0f); }
-  else { float sn, cs; __sincosf(x2, &sn, &cs); f2 = sn / x2; g2 = (cs - f2) / x2; }
+  // sinc and its derivative, branch-free: MUFU sin/cos and reciprocal (no
+  // IEEE division), Taylor terms below |x| = 1e-3
+  auto sinc = [&](float x, float* f, float* g) {
+    float sn, cs;
+    __sincosf(x, &sn, &cs);
+    const bool small = fabsf(x) < 1e-3f;
+    const float r = rcp_ftz(small ? 1.0f : x);
+    *f = small ? fmaf(x * x, -1.0f / 6.0f, 1.0f) : sn * r;
+    if (GRAD) *g = small ? x * (-1.0f / 3.0f) : (cs - *f) * r;
+  };
+  float f1, g1 = 0.0f, f2, g2 = 0.0f;
+  sinc(x1, &f1, &g1);
+  sinc(x2, &f2, &g2);
   if (GRAD) {
     const float a1 = g1 * f2 * sc, a2 = f1 * g2 * sc;
     dDdr[0] = (a1 * (dd.e1x - s1 * hx) + a2 * (dd.e2x - s2 * hx)) * id;
