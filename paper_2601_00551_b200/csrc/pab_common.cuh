@@ -73,6 +73,25 @@ struct GroupDet {
   int slow;           // detector close to the group: exact FP64 per-pair path
 };
 
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// MUFU reciprocal / reciprocal square root without the denormal-range
+// rescaling rsqrtf/__fdividef emit (operands here are normal numbers; the
+// results are identical to theirs for normal inputs)
+__device__ __forceinline__ float rcp_ftz(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 struct Detector {
   double px, py, pz;
   float fx, fy, fz;   // receive direction (unit; = -outward normal)
@@ -99,7 +118,7 @@ __device__ __forceinline__ GroupDet group_det(const GroupMeta& g, double px, dou
   const double kf = floor(tau);
   r.Sx = (float)Sx; r.Sy = (float)Sy; r.Sz = (float)Sz;
   r.Sn = (float)Sn;
-  r.isn = (float)(1.0 / Sn);
+  r.isn = (float)(1.0 / Sn);   // correctly rounded: the pair distances depend on it
   r.phg = (float)(tau - kf);
   r.kg = (int)kf;
   r.slow = (Sn <= 2.0 * (double)g.radius + 1e-9) ? 1 : 0;
@@ -146,25 +165,6 @@ __device__ __forceinline__ int floor_div_f(int a, int f, float inv_f) {
 }
 template <bool BF = false>
 __device__ __forceinline__ int ceil_div_f(int a, int f, float inv_f) { return -floor_div_f<BF>(-a, f, inv_f); }
-
-__device__ __forceinline__ float ex2(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-// MUFU reciprocal / reciprocal square root without the denormal-range
-// rescaling rsqrtf/__fdividef emit (operands here are normal numbers; the
-// results are identical to theirs for normal inputs)
-__device__ __forceinline__ float rcp_ftz(float x) {
-  float y;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-__device__ __forceinline__ float rsqrt_ftz(float x) {
-  float y;
-  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
 
 // ---------------------------------------------------------------------------
 // Lean per-pair pieces used by the hot loops (per-ball constants hoisted by
@@ -375,8 +375,8 @@ __device__ __forceinline__ void group_range(const Acq& a, const GroupDet& gd, co
     klo = min(klo, (int)floorf(-(gd.Sn + gm.radius + a.vt0_f) * a.inv_vdt_f - rho - 2.0f));
     khi = max(khi, (int)ceilf(taup_max + rho + 2.0f));
   }
-  *lo = max(floor_div(klo, a.f), 0);
-  *hi = min(ceil_div(khi, a.f), a.n_out - 1);
+  *lo = max(floor_div_f<true>(klo, a.f, a.inv_f), 0);   // |k| < 2^24 (host-checked): no integer division
+  *hi = min(ceil_div_f<true>(khi, a.f, a.inv_f), a.n_out - 1);
 }
 
 // Dual-walk pairing directions (forward kernel): the 8 x 8 cells of a
