@@ -45,8 +45,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, choices=[2, 4], default=2,
-                    help="BASELINE config: 2 microbench (default, the headline), 4 planar tilted / element")
+    ap.add_argument("--config", type=int, choices=[2, 4, 5], default=2,
+                    help="BASELINE config: 2 microbench (default, the headline), 4 planar tilted / element, "
+                         "5 mouse-scale (one fwd+fine-adjoint iteration of the 256^3-in-ellipsoid grid cloud)")
     ap.add_argument("--n-balls", type=int, default=None, help="default: 1M (config 2), 4M (config 4)")
     ap.add_argument("--n-det", type=int, default=1024)
     ap.add_argument("--n-samples", type=int, default=4096, help="config 2 only (config 4: 6144)")
@@ -62,6 +63,11 @@ def make_scene(args):
     """(scene, directivity kwargs for P.Directivity, oracle kind) of the
     selected BASELINE config."""
     from paper_2601_00551_b200 import scenes
+    if args.config == 5:
+        sc = scenes.mouse_config()
+        args.n_balls = len(sc.init)
+        args.n_det, args.n_samples = sc.array.positions.shape[0], sc.grid.n_samples
+        return sc, dict(kind="cos_power", power=2.0), ("cos_power", 2.0)
     if args.config == 4:
         args.n_balls = args.n_balls or 4_000_000
         args.n_det, args.n_samples = 1024, 6144
@@ -72,6 +78,11 @@ def make_scene(args):
 
 
 def config_dict(args, world):
+    if args.config == 5:
+        return {"workload": "config5-mouse-scale: one fwd+fine-adjoint iteration of the initial grid cloud",
+                "n_balls": args.n_balls, "n_detectors": args.n_det, "n_samples": args.n_samples,
+                "sampling_hz": 40e6, "a0_mm": 0.1, "directivity": "cos^2", "parallelism": f"detector-shard x{world}",
+                "l2": "inputs larger than L2", "inputs": "device-resident"}
     if args.config == 4:
         return {"workload": "config4-planar-tilted: fwd+fine-adjoint", "n_balls": args.n_balls,
                 "n_detectors": 1024, "n_samples": 6144, "sampling_hz": 40e6, "a0_mm": [0.05, 0.2],

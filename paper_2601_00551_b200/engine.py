@@ -323,7 +323,8 @@ def forward_rows(cloud: DeviceCloud, det: DeviceDetectors, acq: Acq, counters: P
     loss_rows = ws.get("loss_rows", J, torch.float64) if real_local is not None else None
     if cloud.n_groups > 0:
         # the dual walk (pairing table) unless PAB_FORWARD_DUAL=0 (single walks: A/B tests)
-        ptab = ptr(cloud.pair_table()) if os.environ.get("PAB_FORWARD_DUAL", "1") != "0" else None
+        dual = os.environ.get("PAB_FORWARD_DUAL", "1") != "0" and acq.f <= int(os.environ.get("PAB_FORWARD_DUAL_MAXF", "64"))
+        ptab = ptr(cloud.pair_table()) if dual else None
         call("pab_forward", ptr(cloud.rec_a), ptr(cloud.rec_b), ptr(cloud.gmeta), ptab,
              cloud.n_groups,
              ptr(det.pos), ptr(det.aux), J, det.sound_speed, acq.t0, acq.dt, acq.f, n_out, acq.cutoff,
