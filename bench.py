@@ -35,7 +35,7 @@ METRIC = "ball-detector pair evals/s (fwd+adjoint) per iteration"
 UNIT = "pairs/s"
 FLOPS_FWD = 7      # per in-window sample
 FLOPS_ADJ_FINE = 12
-TRAFFIC_FWD_BYTES = 138_801_920   # dram__bytes_read.sum + dram__bytes_write.sum, forward, profiles/r01_v9
+TRAFFIC_FWD_BYTES = 152_493_568   # dram__bytes_read.sum + dram__bytes_write.sum, forward, profiles/r01_v10
 EX2_PER_SAMPLE = 1
 
 
@@ -410,7 +410,7 @@ def main():
                 "peak_source": peak_kind,
                 "algorithmic": f"{FLOPS_FWD} FP32 flops x {samples} in-window samples per launch (SURVEY 8d; "
                                "forward+residual events, of which pack, pairing table and residual are ~1.5%)",
-                "traffic_unit": "DRAM bytes per forward launch (ncu --set full, profiles/r01_v9)",
+                "traffic_unit": "DRAM bytes per forward launch (ncu --set full, profiles/r01_v10)",
                 "other_bounds": {
                     "forward_ex2 (1 per sample)": {"frac": samples / fwd_s / peak_ex2, "peak_per_s": peak_ex2},
                     "forward_smem_rmw (8 B per sample)": {"frac": samples / fwd_s / peak_rmw,
@@ -422,7 +422,7 @@ def main():
                     "path_ex2 (fwd+adj, 2 ex2 per sample)": {"frac": 2 * samples / (ms_max * 1e-3) / peak_ex2}},
                 "design_note": "the forward's dual walk executes 0.5 ex2, 4 FP32 lane-ops and 4 B of shared RMW per "
                                "walked ball-sample (1.28 walked per in-window sample); no pipe is saturated "
-                               "(ncu r01_v9: issue slots 66%, ALU 39%, XU 39%, FMA 30%, LSU 17%)",
+                               "(ncu r01_v10: issue slots 67%, ALU 40%, XU 39%, FMA 31%, LSU 17%)",
                 "kernel_ms": {"forward+residual": fwd_mean, "adjoint+finalize": adj_mean}}
 
     cpu = None
