@@ -160,16 +160,6 @@ __device__ __forceinline__ void moment_block8(const float4* s4, float mf, const 
                                               float2& A3) {
   const float4 ra = s4[0], rb = s4[1];
   const float2 m2 = make_float2(mf, mf);
-#ifdef PAB_ADJ_YCHAIN   // pairs 1-3 of a block by FADD2 from pair 0 (two register pairs per op instead of three)
-  (void)c1; (void)c2; (void)c3;
-  const float2 y0 = __ffma2_rn(m2, W.nsc2, c0);
-  const float2 d2 = make_float2(W.dl2, W.dl2);
-  const float2 y1 = __fadd2_rn(y0, d2), y2 = __fadd2_rn(y1, d2), y3 = __fadd2_rn(y2, d2);
-  moment_pair_masked<STAGE, MASK>(make_float2(ra.x, ra.y), y0, qmax, A0, A1, A2, A3);
-  moment_pair_masked<STAGE, MASK>(make_float2(ra.z, ra.w), y1, qmax, A0, A1, A2, A3);
-  moment_pair_masked<STAGE, MASK>(make_float2(rb.x, rb.y), y2, qmax, A0, A1, A2, A3);
-  moment_pair_masked<STAGE, MASK>(make_float2(rb.z, rb.w), y3, qmax, A0, A1, A2, A3);
-#else
   moment_pair_masked<STAGE, MASK>(make_float2(ra.x, ra.y), __ffma2_rn(m2, W.nsc2, c0), qmax,
                                                         A0, A1, A2, A3);
   moment_pair_masked<STAGE, MASK>(make_float2(ra.z, ra.w), __ffma2_rn(m2, W.nsc2, c1), qmax,
@@ -178,7 +168,6 @@ __device__ __forceinline__ void moment_block8(const float4* s4, float mf, const 
                                                         A0, A1, A2, A3);
   moment_pair_masked<STAGE, MASK>(make_float2(rb.z, rb.w), __ffma2_rn(m2, W.nsc2, c3), qmax,
                                                         A0, A1, A2, A3);
-#endif
 }
 
 template <int STAGE, bool MASK>

@@ -73,13 +73,6 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
 // issue slots to the walker sharing its scheduler.
 __device__ __forceinline__ void mbar_wait_backoff(unsigned long long* b, unsigned parity) {
   const unsigned a = (unsigned)__cvta_generic_to_shared(b);
-#ifdef PAB_FWD_SUSPEND_NS   // hardware-suspended wait (time-limit hint) instead of polling
-  asm volatile(
-      "{\n .reg .pred p;\n WAITS_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n @!p bra WAITS_%=;\n}" ::"r"(a),
-      "r"(parity), "r"((unsigned)PAB_FWD_SUSPEND_NS)
-      : "memory");
-  return;
-#endif
   unsigned ok;
   for (;;) {
     asm volatile(
@@ -973,11 +966,7 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
               ghi = max(ghi, hi);
             }
             word_l = (unsigned)bin | ((unsigned)(ghi - (bin << kBinShift)) << 16) | (pair ? 0x80000000u : 0u);
-#ifdef PAB_FWD_CELL0   // tuning builds: one pairing cell for every detector (table locality test)
-            cell_l = 36;
-#else
             cell_l = pair ? pair_cell(gdA_l.Sx, gdA_l.Sy, gdA_l.Sz) : 0;
-#endif
           }
           PROF_ACC(pp_geo, t_g);
           // two-stage prefetch: pairing ids two entries ahead, records one ahead
