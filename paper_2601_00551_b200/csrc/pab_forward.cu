@@ -1184,10 +1184,33 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
 // res = -real for the zero-pressure filter probe), per-row FP64 loss.
 __global__ void residual_kernel(const float* __restrict__ partial_rows, int parts, int n_det, int n_out,
                                 const float* __restrict__ real, float* __restrict__ out,
-                                double* __restrict__ loss_rows) {
+                                double* __restrict__ loss_rows, bool vec) {
   const int j = blockIdx.x;
   double acc = 0.0;
-  for (int k = threadIdx.x; k < n_out; k += blockDim.x) {
+  int k0 = 0;
+  if (vec) {   // 16-byte rows: float4 streams, all loads of a step in flight together
+    const int n4 = n_out >> 2;
+    const size_t row4 = (size_t)j * n4, plane4 = (size_t)n_det * n4;
+    const float4* pr = reinterpret_cast<const float4*>(partial_rows);
+    const float4* re = reinterpret_cast<const float4*>(real);
+    float4* o4 = reinterpret_cast<float4*>(out);
+    for (int k = threadIdx.x; k < n4; k += blockDim.x) {
+      float4 v = pr[row4 + k];
+      for (int p = 1; p < parts; ++p) {
+        const float4 w = pr[p * plane4 + row4 + k];
+        v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
+      }
+      if (real != nullptr) {
+        const float4 t = re[row4 + k];
+        v.x -= t.x; v.y -= t.y; v.z -= t.z; v.w -= t.w;
+        acc += (double)v.x * (double)v.x + (double)v.y * (double)v.y + (double)v.z * (double)v.z +
+               (double)v.w * (double)v.w;
+      }
+      o4[row4 + k] = v;
+    }
+    k0 = n_out;
+  }
+  for (int k = k0 + threadIdx.x; k < n_out; k += blockDim.x) {
     float s = 0.0f;
     for (int p = 0; p < parts; ++p) s += partial_rows[((size_t)p * n_det + j) * n_out + k];
     if (real != nullptr) {
@@ -1305,8 +1328,10 @@ int pab_residual(const float* partial_rows, int partitions, int n_det, int n_out
                  float* out, double* loss_rows, void* stream) {
   if (n_det <= 0 || n_out <= 0) return 0;
   if (!partial_rows || !out || partitions < 1) return 1;
+  auto a16 = [](const void* q) { return ((uintptr_t)q & 15) == 0; };
+  const bool vec = (n_out & 3) == 0 && a16(partial_rows) && a16(out) && (real == nullptr || a16(real));
   residual_kernel<<<n_det, 256, 0, (cudaStream_t)stream>>>(partial_rows, partitions, n_det, n_out, real,
-                                                           out, loss_rows);
+                                                           out, loss_rows, vec);
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 
