@@ -325,11 +325,15 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    hbm_evs = []
     with sampler:
         for k in range(args.steps):
             flush.fill_(float(k))
+            E.TIMING = {n: [torch.cuda.Event(enable_timing=True) for _ in range(2)] for n in ("residual", "finalize")}
+            hbm_evs.append(E.TIMING)
             one_step(evs[k])
         torch.cuda.synchronize()
+    E.TIMING = None
     if world > 1:
         dist.barrier()
     fwd_ms = [e[0].elapsed_time(e[1]) for e in evs]
@@ -424,6 +428,26 @@ def main():
                                "walked ball-sample (1.28 walked per in-window sample); no pipe is saturated "
                                "(ncu r01_v10: issue slots 67%, ALU 40%, XU 39%, FMA 31%, LSU 17%)",
                 "kernel_ms": {"forward+residual": fwd_mean, "adjoint+finalize": adj_mean}}
+
+    # the HBM-bound kernels of the step (signal and gradient traffic) against
+    # the measured copy bandwidth; algorithmic bytes: residual = partition
+    # planes + supervision read, residual written; finalize = chunk partials
+    # + ball records read, caller-order gradients written
+    peak_hbm, hbm_src = 6650.0, "fallback (B200_PROFILING.md)"
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peak_hbm, hbm_src = float(json.load(fh)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, KeyError, ValueError):
+        pass
+    parts = E.plan_forward(cloud, det, acq).partitions
+    res_bytes = (parts + 2) * det.n_local * acq.n_out * 4
+    hbm = {"peak_GBps": peak_hbm, "peak_source": hbm_src}
+    for name, nbytes in (("residual", res_bytes), ("grad_finalize", hbm_evs[0].get("finalize_bytes", 0))):
+        key = "finalize" if name == "grad_finalize" else name
+        ms_k = statistics.median(t[key][0].elapsed_time(t[key][1]) for t in hbm_evs)
+        gbs = nbytes / (ms_k * 1e-3) / 1e9
+        hbm[name] = {"ms": ms_k, "algorithmic_bytes": int(nbytes), "GBps": gbs, "frac": gbs / peak_hbm}
+    roofline["hbm_kernels"] = hbm
 
     cpu = None
     if world == 1 and not args.no_cpu:

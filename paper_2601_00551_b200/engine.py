@@ -302,6 +302,16 @@ class PassCounters:
         return int(self.ops.item())
 
 
+# bench hook: {"residual" | "finalize": [start, end] CUDA events} recorded on the
+# launching stream around those HBM-bound kernels (None: no events)
+TIMING = None
+
+
+def _mark(name: str, i: int) -> None:
+    if TIMING is not None and name in TIMING:
+        TIMING[name][i].record(torch.cuda.current_stream())
+
+
 def forward_rows(cloud: DeviceCloud, det: DeviceDetectors, acq: Acq, counters: PassCounters,
                  real_local: torch.Tensor | None = None, out: torch.Tensor | None = None,
                  real_ready: torch.cuda.Event | None = None):
@@ -334,8 +344,10 @@ def forward_rows(cloud: DeviceCloud, det: DeviceDetectors, acq: Acq, counters: P
         partial.zero_()
     if real_ready is not None:
         torch.cuda.current_stream(cloud.dev).wait_event(real_ready)
+    _mark("residual", 0)
     call("pab_residual", ptr(partial), plan.partitions, J, n_out, ptr(real_local), ptr(out),
          ptr(loss_rows), _stream())
+    _mark("residual", 1)
     return out, loss_rows
 
 
@@ -368,8 +380,12 @@ def adjoint_grads(cloud: DeviceCloud, det: DeviceDetectors, acq: Acq, res: torch
              acq.cutoff, acq.dir_kind, acq.dir_param, ptr(res), float(res_sign), int(stage), chunks,
              ADJOINT_WARPS, ptr(gpart), ptr(counters.ops) if count_ops else None, ptr(counters.status),
              _stream())
+        _mark("finalize", 0)
         call("pab_grad_finalize", ptr(gpart), chunks, cloud.n_groups, ptr(cloud.rec_b), float(scale), int(stage),
              ptr(d_p0), ptr(d_a0), ptr(d_pos), ptr(counters.status), _stream())
+        _mark("finalize", 1)
+        if TIMING is not None:
+            TIMING["finalize_bytes"] = chunks * 5 * npad * 8 + npad * 16 + 5 * n * 8
     if det.shard.world > 1:
         allreduce_sum_(flat)
     return d_p0, d_a0, d_pos
