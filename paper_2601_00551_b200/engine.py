@@ -31,7 +31,7 @@ FORWARD_WARPS = int(os.environ.get("PAB_FWD_WARPS", "4"))   # 2 CTAs per SM: one
 FORWARD_TILE_ROWS = 160   # reserved ABI argument (the library's tile height is a build constant)
 ADJOINT_WARPS = int(os.environ.get("PAB_ADJ_WARPS", "1"))   # = PAB_ADJ_WARPS of the library build
 GROUP = 32
-A0_BUCKETS = int(os.environ.get("PAB_A0_BUCKETS", "8"))   # lane groups hold balls of similar radius (equal window lengths)
+A0_BUCKETS = int(os.environ.get("PAB_A0_BUCKETS", "6"))   # lane groups hold balls of similar radius (equal window lengths)
 GROUP_META_BYTES = 48
 
 
