@@ -59,7 +59,7 @@ def test_integration_stub_matches_package():
     rows, _, _, ops = run(cloud, ctx, 1)
     P.reset_op_count()
     ref = P.simulate_signals(cloud, ctx).data
-    assert rel_l2(rows, ref) < 1e-6
+    assert rel_l2(rows, ref) < 1e-5   # FP32 summation order differs (partitions, bucket count)
     assert ops == P.op_count()
     real = P.SignalSet(ctx.grid, 0.9 * ref + 0.01 * np.abs(ref).max())
     cand = P.PointCloud(pos + rng.normal(scale=2e-5, size=pos.shape), cloud.p0 * 1.1, cloud.a0 * 0.97)
