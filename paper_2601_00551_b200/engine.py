@@ -253,17 +253,20 @@ class ForwardPlan:
 
 
 def plan_forward(cloud: DeviceCloud, det: DeviceDetectors, acq: Acq) -> ForwardPlan:
-    """Two CTAs (4 warps, ~100-110 KB smem each) per SM: detectors x
-    partitions should cover >= 6 waves (tail < 3%); each partition keeps >= 4
-    lane groups per warp."""
+    """Two CTAs (4 walker + 4 producer warps, ~110-115 KB smem each) per SM:
+    detectors x partitions should cover >= 20 waves (measured with the dual
+    walk: 2 / 4 / 6 / 12 partitions at config 2 give 21.16 / 21.00 / 20.81 /
+    20.76 ms of forward + residual; finer partitions cost residual traffic
+    and partial-row memory); each partition keeps >= 4 lane groups per warp."""
     dev = cloud.dev
     tile = FORWARD_TILE_ROWS
     warps = FORWARD_WARPS
     while warps > 1 and _lib.load().pab_forward_smem_bytes(acq.n_out, warps, tile) > 227 * 1024:
         warps -= 1
-    target_ctas = 12 * sm_count(dev)   # >= 6 waves of 2 resident CTAs per SM
+    target_ctas = 40 * sm_count(dev)   # >= 20 waves of 2 resident CTAs per SM
     parts = max(1, -(-target_ctas // max(det.n_local, 1)))
     parts = int(max(1, min(parts, cloud.n_groups // (4 * warps))))
+    parts = int(os.environ.get("PAB_FWD_PARTS", parts))   # tuning override
     return ForwardPlan(0, parts, warps, tile)
 
 
