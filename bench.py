@@ -302,7 +302,8 @@ def main():
 
     def one_step(ev=None):
         c = E.PassCounters(dev)
-        cloud.invalidate()   # parameters change every iteration: repack (the optimizer's per-step cost)
+        cloud.invalidate()   # parameters change every iteration: repack (the optimizer's per-step cost;
+        #                      the sort order and the dual-walk pairing table persist until a resort)
         if ev:
             ev[0].record(stream)
         cloud.pack()
@@ -413,7 +414,7 @@ def main():
                 "frac": ach / peak_flops, "traffic": TRAFFIC_FWD_BYTES, "kernel": "forward_kernel",
                 "peak_source": peak_kind,
                 "algorithmic": f"{FLOPS_FWD} FP32 flops x {samples} in-window samples per launch (SURVEY 8d; "
-                               "forward+residual events, of which pack, pairing table and residual are ~1.5%)",
+                               "forward+residual events, of which pack and residual are ~0.3%)",
                 "traffic_unit": "DRAM bytes per forward launch (ncu --set full, profiles/r01_v10)",
                 "other_bounds": {
                     "forward_ex2 (1 per sample)": {"frac": samples / fwd_s / peak_ex2, "peak_per_s": peak_ex2},
@@ -460,7 +461,7 @@ def main():
             "data": f"synthetic (seeded CounterRng, BASELINE config {args.config})", "config": config_dict(args, world),
             "in_window_samples_per_step": samples, "samples_per_pair": samples / pairs,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": sampler.summary(),
-            "gpu_launches": 6 * args.steps,   # pack, pairing table, forward, residual, adjoint, finalize
+            "gpu_launches": 5 * args.steps,   # pack, forward, residual, adjoint, finalize (pairing table: per sort)
             "kernel_ms_min_median": {"forward+residual": [min(fwd_ms), statistics.median(fwd_ms)],
                                      "adjoint+finalize": [min(adj_ms), statistics.median(adj_ms)]}}
     if args.recon:

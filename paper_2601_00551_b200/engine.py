@@ -150,7 +150,6 @@ class DeviceCloud:
         """Parameters changed: repack before the next pass (and resort)."""
         self._packed = False
         self._stats = None
-        self._ptable_ok = False
         if resort:
             self.perm = None
 
@@ -158,6 +157,7 @@ class DeviceCloud:
         n = self.n
         if n == 0:
             self.perm = torch.empty(0, dtype=torch.int32, device=self.dev)
+            self._ptable_ok = False
             return
         lo = torch.amin(self.pos, dim=0)
         hi = torch.amax(self.pos, dim=0)
@@ -170,6 +170,7 @@ class DeviceCloud:
              ext, a0lo, a0hi, A0_BUCKETS, ptr(keys), _stream())
         skeys, _ = torch.sort(keys)
         self.perm = (skeys & 0xFFFFFFF).to(torch.int32)
+        self._ptable_ok = False   # new units: rebuild the pairing table
 
     def pack(self) -> None:
         if self._packed:
@@ -187,11 +188,14 @@ class DeviceCloud:
                  ptr(self.rec_a), ptr(self.rec_b), ptr(self.gmeta), _stream())
         self._packed = True
         self._stats = None
-        self._ptable_ok = False
 
     def pair_table(self) -> torch.Tensor:
-        """Dual-walk pairing table of the packed cloud (built on first use
-        after each pack; the forward's performance aid, not its numerics)."""
+        """Dual-walk pairing table: which two balls of a 64-ball unit a lane
+        walks together, per direction cell.  Built on first use after each
+        sort (unit membership follows the processing order); repacks with
+        moved balls keep it, like the sort order itself: any pairing gives
+        the same sums up to FP32 rounding, a slightly stale one only walks a
+        little more."""
         if not getattr(self, "_ptable_ok", False):
             nbytes = int(_lib.load().pab_pair_table_bytes(self.n_groups))
             if not hasattr(self, "ptable") or self.ptable.numel() < max(nbytes, 1):
