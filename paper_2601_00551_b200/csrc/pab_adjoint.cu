@@ -625,3 +625,39 @@ extern "C" int pab_adj_prof(unsigned long long* out /*[16]*/, int reset) {
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 #endif
+
+#ifdef PAB_ADJ_BENCH
+// Tuning builds only: the fine adjoint's moment walk in isolation (16 warps
+// per SM, one per CTA, like the kernel), `reps` walks of L samples per lane
+// over a staged segment -- lane-samples per second vs the ex2 / FMA ceilings.
+namespace pab {
+__global__ void __launch_bounds__(32, 16) adj_walk_bench_kernel(int reps, int L, float* out) {
+  __shared__ __align__(16) float seg[kSeg + kPad + 4];
+  const int lane = threadIdx.x;
+  for (int i = lane; i < kSeg + kPad + 4; i += 32) seg[i] = 0.001f * (float)((i * 7) % 13);
+  __syncwarp();
+  const float sc = 0.3f + 0.001f * lane, ps = 0.1f * lane;
+  const WalkConst W = walk_const(sc, 1);
+  Moments acc = {0.f, 0.f, 0.f, 0.f};
+  for (int r = 0; r < reps; ++r) {
+    const int J0 = ((r * 4 + lane * 4) % 64);
+    Moments M;
+    moments_uniform<kStageFine, false>(seg + J0, L, (float)(-L / 2), W, ps, 30.0f, M);
+    acc.T0 += M.T0; acc.T1 += M.T1; acc.T2 += M.T2; acc.T3 += M.T3;
+  }
+  out[blockIdx.x * 32 + lane] = acc.T0 + acc.T1 + acc.T2 + acc.T3;
+}
+}  // namespace pab
+extern "C" int pab_bench_adj_walk(int blocks, int reps, int L, float* out, float* ms) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  pab::adj_walk_bench_kernel<<<blocks, 32>>>(reps, L, out);
+  cudaEventRecord(a);
+  pab::adj_walk_bench_kernel<<<blocks, 32>>>(reps, L, out);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  cudaEventElapsedTime(ms, a, b);
+  return cudaGetLastError() == cudaSuccess ? 0 : 4;
+}
+#endif
