@@ -274,9 +274,12 @@ def _run_model(cloud, ctx, f, real=None, stage="fine"):
     det = device_detectors(ctx)
     dev = det.pos.device
     acq = _acq(ctx, f)
-    if need_grad:   # supervision upload first: it overlaps the cloud upload, packing and forward kernel
-        real_local, real_ready = device_supervision(real.data, det, defer=True)
+    # the cloud first (sorting and packing wait for it), then the supervision
+    # on a side stream: it overlaps the sort, pack and forward kernel instead
+    # of sharing the link with the cloud upload
     dc = E.DeviceCloud.from_host(cloud.positions, cloud.p0, a0, dev)
+    if need_grad:
+        real_local, real_ready = device_supervision(real.data, det, defer=True)
     counters = E.PassCounters(dev)
     if not need_grad:
         local, _ = E.forward_rows(dc, det, acq, counters)
