@@ -566,3 +566,36 @@ def test_dual_walk_guards_match_oracle(P, a0_mm, f, n):
     got = P.simulate_at_rate(P.PointCloud(pos, p0, a0), ctx, f).data
     assert rel_l2(got, rows) < SIG_TOL
     assert abs(P.op_count() - ops) <= 2
+
+
+def test_stale_pairing_table_after_repack(P):
+    """The pairing table survives repacks until the next sort (engine
+    DeviceCloud.invalidate without resort): moved balls walked with the old
+    pairing give the same rows as a fresh cloud, to FP32 summation order."""
+    import torch
+
+    from paper_2601_00551_b200 import engine as E
+    from paper_2601_00551_b200 import radiator as R
+    rng = np.random.default_rng(61)
+    n = 5000
+    pos = rng.uniform(-3e-3, 3e-3, (n, 3))
+    p0 = rng.uniform(0.2, 1.0, n)
+    a0 = rng.uniform(0.05e-3, 0.2e-3, n)
+    ang = rng.uniform(0, 2 * np.pi, 8)
+    sens = np.column_stack([0.03 * np.cos(ang), 0.03 * np.sin(ang), rng.uniform(-0.01, 0.01, 8)])
+    ctx = P.ForwardContext(P.SensorArray(sens, 1500.0), P.TimeGrid(0.0, 2.5e-8, 2048))
+    det, acq = R.device_detectors(ctx), R._acq(ctx, 1)
+    dev = det.pos.device
+    dc = E.DeviceCloud.from_host(pos, p0, a0, dev)
+    E.forward_rows(dc, det, acq, E.PassCounters(dev))
+    table = dc.pair_table()
+    moved = pos + rng.normal(scale=5e-5, size=pos.shape)
+    dc.pos.copy_(torch.from_numpy(moved).to(dev))
+    dc.invalidate()
+    stale, _ = E.forward_rows(dc, det, acq, E.PassCounters(dev))
+    assert dc.pair_table() is table   # not rebuilt
+    fresh_dc = E.DeviceCloud.from_host(moved, p0, a0, dev)
+    fresh, _ = E.forward_rows(fresh_dc, det, acq, E.PassCounters(dev))
+    rows = OR.run_model(moved, p0, a0, sens, None, 1500.0, 0.0, 2.5e-8, 2048, 1)[0]
+    assert rel_l2(stale.double().cpu().numpy(), rows) < SIG_TOL
+    assert rel_l2(stale.double().cpu().numpy(), fresh.double().cpu().numpy()) < 1e-5
