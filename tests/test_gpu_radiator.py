@@ -599,3 +599,41 @@ def test_stale_pairing_table_after_repack(P):
     rows = OR.run_model(moved, p0, a0, sens, None, 1500.0, 0.0, 2.5e-8, 2048, 1)[0]
     assert rel_l2(stale.double().cpu().numpy(), rows) < SIG_TOL
     assert rel_l2(stale.double().cpu().numpy(), fresh.double().cpu().numpy()) < 1e-5
+
+
+@pytest.mark.parametrize("config", [4, 5])
+def test_config_slices_match_oracle(P, config):
+    """BASELINE config 4 (planar tilted array, element directivity, 6144
+    samples) and config 5 (ring-cylinder array, cos^2, 8192 samples, grid
+    cloud) geometries on slices the oracle finishes in seconds: forward
+    and fine gradients through the dual-walk forward and the adjoint."""
+    from paper_2601_00551_b200 import scenes
+    if config == 4:
+        sc = scenes.planar_config(n_balls=200_000)
+        kind, dkw = ("element", 0.5e-3), dict(kind="element", width=0.5e-3)
+        sel = slice(0, 1024, 64)
+        balls = slice(0, 200_000, 10)
+    else:
+        sc = scenes.mouse_config(grid_n=64, n_truth=20_000)
+        kind, dkw = ("cos_power", 2.0), dict(kind="cos_power", power=2.0)
+        sel = slice(0, 2048, 128)
+        balls = slice(0, None, 4)
+    sens, nrm = sc.array.positions[sel], sc.array.normals[sel]
+    ctx = P.ForwardContext(P.SensorArray(sens, 1500.0, normals=nrm), sc.grid, directivity=P.Directivity(**dkw))
+    t = sc.truth
+    tp, tp0, ta0 = t.positions[balls], t.p0[balls], t.a0[balls]
+    real, _, _, ops = OR.run_model(tp, tp0, ta0, sens, nrm, 1500.0, 0.0, sc.grid.dt, sc.grid.n_samples, 1,
+                                   kind=kind, threads=8)
+    P.reset_op_count()
+    got = P.simulate_signals(P.PointCloud(tp, tp0, ta0), ctx).data
+    assert rel_l2(got, real) < SIG_TOL
+    assert abs(P.op_count() - ops) <= 1e-4 * ops
+    c = sc.init
+    cp, cp0, ca0 = c.positions[balls], c.p0[balls], c.a0[balls]
+    _, L, (gp0, ga0, gpos), _ = OR.run_model(cp, cp0, ca0, sens, nrm, 1500.0, 0.0, sc.grid.dt, sc.grid.n_samples,
+                                             1, real=real, stage="fine", kind=kind, threads=8)
+    Lg, gr = P.backward(P.PointCloud(cp, cp0, ca0), ctx, P.SignalSet(sc.grid, real), stage="fine")
+    assert abs(Lg - L) <= 1e-4 * L
+    assert rel_l2(gr.d_p0, gp0) < GRAD_TOL
+    assert rel_l2(gr.d_a0, ga0) < GRAD_TOL
+    assert rel_l2(gr.d_position, gpos) < GRAD_TOL
