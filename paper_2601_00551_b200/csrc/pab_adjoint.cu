@@ -290,6 +290,9 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
     // stage res[j][lo .. hi] (lo a multiple of 4) + kPad zeros into buffer
     // `buf`: 16-B cp.async (16-B aligned rows) or 4-B cp.async
     auto stage_seg = [&](int jj, int lo, int hi, int fl, int buf) {
+#ifdef PAB_ADJ_NOSTAGE   // tuning builds only: no residual staging (wrong gradients)
+      return;
+#endif
       if (!(fl & kFlagUniform)) return;
       const float* src = res + (size_t)(jb + jj) * n_out + lo;
       float* dst = seg_all[warp][buf];
@@ -315,6 +318,10 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
 
     // per-pair gradient terms (reference radiator.py:275-286 in y units)
     auto epilogue = [&](const PairGeom& pg, const Moments& M, const DetDir& dd) {
+#ifdef PAB_ADJ_NOEPI   // tuning builds only: no gradient epilogue (wrong gradients)
+      gb[0] += M.T0 + M.T1 + M.T2 + M.T3 + pg.id + pg.rx;
+      return;
+#endif
       float dDdr[3] = {0.f, 0.f, 0.f}, dDda0 = 0.f;
       const float id = pg.id;
       const float D = dir_weight<DIR, STAGE == kStageFine || DIR == kDirElement>(
@@ -365,6 +372,10 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
     // uniform path, part 2: the moment walk over the staged segment
     auto uwalk = [&](const USetup& u, int lo, int buf) {
       Moments M;
+#ifdef PAB_ADJ_NOWALK   // tuning builds only: everything but the moment walk (wrong gradients)
+      M = {(float)(u.J0 - lo + buf), (float)u.L, 0.f, 0.f};
+      return M;
+#endif
       moments_uniform<STAGE, MASK>(seg_all[warp][buf] + (u.J0 - lo), (u.L + 3) & ~3, (float)(u.J0 * f - u.pg.kc),
                                    W, u.pg.phi * sc, u.empty ? -1.0f : qmax, M);
       if (!MASK && u.empty) M = {0.f, 0.f, 0.f, 0.f};
