@@ -301,7 +301,7 @@ __device__ __forceinline__ void rmw_walk(float* tile, int lane, int J0, int L, i
 // at |y| <= kDualMaxY (else the pair walks singly), so R < 2^127 there;
 // blocks past a lane's window go to the dump block and never reach the row.
 // ---------------------------------------------------------------------------
-constexpr float kDualMaxDl = 0.75f;   // max |y| step per sample for the recurrence (host-checked)
+constexpr float kDualMaxDl = 0.75f;   // max |y| step per sample for the recurrence (producer-checked)
 constexpr float kDualMaxY = 30.0f;    // max |y| over a dual walk's live samples (producer-checked)
 
 struct DWalk {
