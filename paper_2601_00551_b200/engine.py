@@ -32,6 +32,11 @@ FORWARD_TILE_ROWS = 160   # reserved ABI argument (the library's tile height is 
 ADJOINT_WARPS = int(os.environ.get("PAB_ADJ_WARPS", "1"))   # = PAB_ADJ_WARPS of the library build
 GROUP = 32
 A0_BUCKETS = int(os.environ.get("PAB_A0_BUCKETS", "6"))   # lane groups hold balls of similar radius (equal window lengths)
+# the adjoint walks each ball's own window (no tile, no pairing): it prefers
+# narrower radius buckets than the forward, so it runs on its own packing of
+# the same cloud (measured adjoint at config 2: 6 / 8 / 10 / 16 buckets ->
+# 20.19 / 20.02 / 19.87 / 19.75 ms)
+ADJ_A0_BUCKETS = int(os.environ.get("PAB_ADJ_A0_BUCKETS", "16"))
 GROUP_META_BYTES = 48
 
 
@@ -124,14 +129,27 @@ class DeviceDetectors:
 class DeviceCloud:
     """FP64 SoA cloud in caller order plus packed processing-order records."""
 
-    def __init__(self, pos: torch.Tensor, p0: torch.Tensor, a0: torch.Tensor):
+    def __init__(self, pos: torch.Tensor, p0: torch.Tensor, a0: torch.Tensor, buckets: int | None = None):
         self.dev = pos.device
         self.pos = pos.contiguous()
         self.p0 = p0.contiguous()
         self.a0 = a0.contiguous()
+        self.buckets = A0_BUCKETS if buckets is None else buckets
         self.perm = None
         self._packed = False
         self._stats = None
+        self._adj = None
+
+    def adjoint_cloud(self) -> "DeviceCloud":
+        """The same balls (shared parameter tensors) packed for the adjoint
+        with ADJ_A0_BUCKETS radius buckets; follows this cloud's
+        invalidations.  With equal bucket counts it is this cloud."""
+        if ADJ_A0_BUCKETS == self.buckets:
+            return self
+        if self._adj is None or self._adj.pos is not self.pos or self._adj.p0 is not self.p0 \
+                or self._adj.a0 is not self.a0:
+            self._adj = DeviceCloud(self.pos, self.p0, self.a0, buckets=ADJ_A0_BUCKETS)
+        return self._adj
 
     @classmethod
     def from_host(cls, positions, p0, a0, dev) -> "DeviceCloud":
@@ -150,6 +168,8 @@ class DeviceCloud:
         """Parameters changed: repack before the next pass (and resort)."""
         self._packed = False
         self._stats = None
+        if self._adj is not None:
+            self._adj.invalidate(resort)
         if resort:
             self.perm = None
 
@@ -167,7 +187,7 @@ class DeviceCloud:
         a0lo, a0hi = (float(x) for x in torch.aminmax(self.a0))
         keys = torch.empty(n, dtype=torch.int64, device=self.dev)
         call("pab_morton_keys", ptr(self.pos), ptr(self.a0), n, float(lo_h[0]), float(lo_h[1]), float(lo_h[2]),
-             ext, a0lo, a0hi, A0_BUCKETS, ptr(keys), _stream())
+             ext, a0lo, a0hi, self.buckets, ptr(keys), _stream())
         skeys, _ = torch.sort(keys)
         self.perm = (skeys & 0xFFFFFFF).to(torch.int32)
         self._ptable_ok = False   # new units: rebuild the pairing table
@@ -383,6 +403,7 @@ def adjoint_grads(cloud: DeviceCloud, det: DeviceDetectors, acq: Acq, res: torch
     d_a0 = flat[n:2 * n] if stage >= 1 else None
     d_pos = flat[2 * n:].view(n, 3) if stage >= 1 else None
     if n > 0 and det.n_local > 0:
+        cloud = cloud.adjoint_cloud()   # the adjoint's own packing (radius buckets)
         cloud.pack()
         chunks = plan_adjoint(cloud, det)
         ws = workspace(dev)
