@@ -35,7 +35,7 @@ METRIC = "ball-detector pair evals/s (fwd+adjoint) per iteration"
 UNIT = "pairs/s"
 FLOPS_FWD = 7      # per in-window sample
 FLOPS_ADJ_FINE = 12
-TRAFFIC_FWD_BYTES = 173_823_488   # dram__bytes_read.sum + dram__bytes_write.sum, forward, profiles/r01_v11
+TRAFFIC_FWD_BYTES = 172_755_456   # dram__bytes_read.sum + dram__bytes_write.sum, forward, profiles/r01_v12
 EX2_PER_SAMPLE = 1
 
 
@@ -415,7 +415,7 @@ def main():
                 "peak_source": peak_kind,
                 "algorithmic": f"{FLOPS_FWD} FP32 flops x {samples} in-window samples per launch (SURVEY 8d; "
                                "forward+residual events, of which pack and residual are ~0.3%)",
-                "traffic_unit": "DRAM bytes per forward launch (ncu --set full, profiles/r01_v11; 6 partition planes written)",
+                "traffic_unit": "DRAM bytes per forward launch (ncu --set full, profiles/r01_v12; 6 partition planes written)",
                 "other_bounds": {
                     "forward_ex2 (1 per sample)": {"frac": samples / fwd_s / peak_ex2, "peak_per_s": peak_ex2},
                     "forward_smem_rmw (8 B per sample)": {"frac": samples / fwd_s / peak_rmw,
@@ -427,7 +427,7 @@ def main():
                     "path_ex2 (fwd+adj, 2 ex2 per sample)": {"frac": 2 * samples / (ms_max * 1e-3) / peak_ex2}},
                 "design_note": "the forward's dual walk executes 0.5 ex2, 4 FP32 lane-ops and 4 B of shared RMW per "
                                "walked ball-sample (1.28 walked per in-window sample); no pipe is saturated "
-                               "(ncu r01_v11: issue slots 69%, ALU 42%, XU 40%, FMA 32%, LSU 17%)",
+                               "(ncu r01_v12: issue slots 69%, ALU 42%, XU 40%, FMA 32%, LSU 17%)",
                 "kernel_ms": {"forward+residual": fwd_mean, "adjoint+finalize": adj_mean}}
 
     # the HBM-bound kernels of the step (signal and gradient traffic) against
