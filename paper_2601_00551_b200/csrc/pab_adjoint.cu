@@ -372,6 +372,7 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
     // uniform path, part 2: the moment walk over the staged segment
     auto uwalk = [&](const USetup& u, int lo, int buf) {
       Moments M;
+      PAB_CHECK(u.J0 - lo >= 0 && u.J0 - lo + ((u.L + 3) & ~3) <= kSeg + kPad);
 #ifdef PAB_ADJ_NOWALK   // tuning builds only: everything but the moment walk (wrong gradients)
       M = {(float)(u.J0 - lo + buf), (float)u.L, 0.f, 0.f};
       return M;

@@ -18,6 +18,14 @@
 
 namespace pab {
 
+// Bounds checks of the debug build (-DPAB_DEBUG_CHECKS, tools/variants):
+// a failed check traps the kernel, so the GPU tests fail loudly on it.
+#ifdef PAB_DEBUG_CHECKS
+#define PAB_CHECK(cond) do { if (!(cond)) __trap(); } while (0)
+#else
+#define PAB_CHECK(cond) do { } while (0)
+#endif
+
 constexpr int kWarp = 32;
 constexpr float kSqrtHalfLog2e = 0.84932180028801907f;   // sqrt(log2(e) / 2)
 constexpr float kSqrt2Ln2 = 1.17741002251547469f;        // sqrt(2 ln 2) = kappa / a0

@@ -379,6 +379,7 @@ __device__ __forceinline__ void rmw_walk_dual(float* tile, int lane, int J0, int
     float4 o[K][2];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
+      PAB_CHECK(qq[k] >= 0 && qq[k] <= dump && qn[k] >= 0 && qn[k] <= dump + 1);
       o[k][0] = T[qq[k] * kWarp];
       o[k][1] = T[qn[k] * kWarp];
     }
@@ -744,6 +745,7 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       const int zone_end = zs[warp + 1];
       float* my_stage = stage + warp * kTile;
       auto sink = [&](int r, float v) {
+        PAB_CHECK(r >= 0 && r < n_out && (r < zone_end || r - zone_end < kTile));
         if (r < zone_end) row[r] += v;
         else my_stage[r - zone_end] = v;
       };
@@ -917,10 +919,13 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
         // ids 0-31 first group, 32-63 second: record g0 * 32 + id)
         const int64_t n_units = (n_groups + 1) / 2;
         auto load_ids = [&](int64_t g0, int cell) -> unsigned {
+          PAB_CHECK(cell >= 0 && cell < kPairDirs && (g0 >> 1) < n_units && (g0 & 1) == 0);
           return reinterpret_cast<const unsigned short*>(ptab + ((size_t)cell * n_units + (g0 >> 1)) * 64)[lane];
         };
         auto load_recs = [&](int64_t g0, bool pair, unsigned ids, BallA& A0, BallA& A1, BallB& B0, BallB& B1) {
           const int64_t bi = pair ? g0 * kWarp + (ids & 0xFFu) : g0 * kWarp + lane;
+          PAB_CHECK(bi < n_groups * kWarp && (!pair || (ids & 0xFFu) < 64u && (ids >> 8) < 64u &&
+                                              g0 + 1 < n_groups));
           A0 = ra[bi];
           B0 = rb[bi];
           if (pair) {
