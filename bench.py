@@ -323,11 +323,15 @@ def main():
     # kernel-level events: pack+forward+residual, adjoint+finalize(+allreduce)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     sampler = ClockSampler(local, dev)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
     hbm_evs = []
+    # the sampler thread is running (steady state) before the timed region
+    # opens, so its start-up never delays a kernel launch inside it; its
+    # samples span the timed region
     with sampler:
+        time.sleep(0.2)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
         for k in range(args.steps):
             flush.fill_(float(k))
             E.TIMING = {n: [torch.cuda.Event(enable_timing=True) for _ in range(2)] for n in ("residual", "finalize")}
