@@ -10,8 +10,18 @@ per second, pairs = N_balls x N_detectors per step.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Under torchrun each rank owns a contiguous detector block (strong scaling:
-the configuration is fixed, the per-GPU work shrinks as 1/N).
+Each rank owns a contiguous detector block (strong scaling: the
+configuration is fixed, the per-GPU work shrinks as 1/N); the step's one
+collective is the NCCL all-reduce of the per-ball gradient buffer, whose
+tail carries the loss, error flags and op count.  ``--gpus N`` without a
+torchrun environment re-launches itself under ``torch.distributed.run``
+with N ranks (NCCL, one GPU per rank).  With fewer GPUs than ranks the
+ranks share the GPUs over a gloo group ("oversubscribed": the multi-rank
+code path runs, the number is not a scaling measurement).
+
+The default line also carries BASELINE's second metric (``recon``: the
+config-3 reconstruction wall time, with the CPU reference's extrapolated
+time beside it) and the launch-bound config-1 toy (``config1``).
 """
 
 from __future__ import annotations
@@ -35,8 +45,10 @@ METRIC = "ball-detector pair evals/s (fwd+adjoint) per iteration"
 UNIT = "pairs/s"
 FLOPS_FWD = 7      # per in-window sample
 FLOPS_ADJ_FINE = 12
-TRAFFIC_FWD_BYTES = 172_755_456   # dram__bytes_read.sum + dram__bytes_write.sum, forward, profiles/r01_v12
-EX2_PER_SAMPLE = 1
+# dram__bytes_read.sum + dram__bytes_write.sum per launch from the latest
+# ncu --set full capture of each kernel (profiles/)
+TRAFFIC_BYTES = {"forward_kernel": 172_755_456, "adjoint_kernel": 183_812_352}
+TRAFFIC_SRC = "profiles/r01_v12_ncu_summary.txt"
 
 
 def parse():
@@ -52,10 +64,15 @@ def parse():
     ap.add_argument("--n-det", type=int, default=1024)
     ap.add_argument("--n-samples", type=int, default=4096, help="config 2 only (config 4: 6144)")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-balls", type=int, default=20000, help="oracle sample: balls x 64 detectors")
+    ap.add_argument("--cpu-balls", type=int, default=50000,
+                    help="CPU reference sample: balls (strided subset) x --cpu-det detectors")
+    ap.add_argument("--cpu-det", type=int, default=0,
+                    help="detectors of the CPU sample (0: 8 per host thread, >= 128: every thread gets a block)")
+    ap.add_argument("--cpu-reps", type=int, default=3, help="CPU sample: best of this many runs")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--recon", action="store_true",
-                    help="also time the full config-3 reconstruction (filter + 300 iterations)")
+    ap.add_argument("--no-recon", action="store_true",
+                    help="skip the config-3 reconstruction wall time (BASELINE's second metric)")
+    ap.add_argument("--no-config1", action="store_true", help="skip the config-1 (launch-bound toy) timing")
     return ap.parse_args()
 
 
@@ -181,63 +198,168 @@ def torch_props(dev):
     return torch.cuda.get_device_properties(dev)
 
 
+
+
 # ---------------------------------------------------------------------------
-# CPU reference (oracle port of the reference algorithm) on a bounded sample
+# CPU reference (the oracle's restatement of the reference algorithm) on a
+# bounded sample, with a thread sweep
 # ---------------------------------------------------------------------------
 
-def cpu_reference_pairs_per_s(scene, n_sample: int, steps: int = 1, threads: int | None = None,
-                              n_det: int = 64, kind=("cos_power", 2.0)):
-    """SURVEY.md §6 microbench slice: a strided ball subset x a strided
-    detector subset of config 2 (pairs/s is linear in N*J*W)."""
-    from oracle import radiator as OR   # the reference's CPU algorithm (restated); baseline only
-    threads = threads or os.cpu_count() or 1
-    c, t = scene.init, scene.truth
-    stride = max(1, scene.array.positions.shape[0] // n_det)
-    sens, nrm = scene.array.positions[::stride], scene.array.normals[::stride]
-    sel = np.linspace(0, len(c) - 1, n_sample).astype(np.int64)
-    real, _, _, _ = OR.run_model(t.positions[sel], t.p0[sel], t.a0[sel], sens, nrm, 1500.0, 0.0, scene.grid.dt,
-                                 scene.grid.n_samples, 1, kind=kind, threads=threads)
-    times = []
-    for _ in range(steps):
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def host_ram_bytes() -> int:
+    try:
+        with open("/proc/meminfo") as fh:
+            for line in fh:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 16 << 30
+
+
+class CpuReference:
+    """The reference's CPU algorithm (oracle/radiator.py: FP64 numpy, sensor
+    blocks of 8 over a thread pool, radiator.py:316-332) on a strided ball
+    subset x a strided detector subset of the workload (cost is linear in
+    N * J * W, so pairs/s carries over).  The thread count is swept on a
+    small sample first; the timed sample then runs with the best count, and
+    every thread has a sensor block (>= 8 detectors per thread)."""
+
+    SWEEP = (1, 2, 4, 8, 16, 32, 64)
+
+    def __init__(self, scene, kind, n_balls: int, n_det: int = 0):
+        from oracle import radiator as OR   # the reference's CPU algorithm (restated); baseline only
+        self.OR = OR
+        self.kind = kind
+        self.scene = scene
+        ncpu = os.cpu_count() or 1
+        J = scene.array.positions.shape[0]
+        n_det = n_det or min(J, max(128, 8 * ncpu))
+        stride = max(1, J // n_det)
+        self.sens = scene.array.positions[::stride][:n_det]
+        self.nrm = scene.array.normals[::stride][:n_det]
+        self.threads_avail = ncpu
+        # the oracle caches ~14 KB per ball per busy thread (BASELINE.md): stay within half the RAM
+        cap = int(0.5 * host_ram_bytes() / (14e3 * max(1, min(ncpu, -(-self.sens.shape[0] // 8)))))
+        self.n_balls = int(max(1000, min(n_balls, cap, len(scene.init))))
+        self.sel = self._subset(self.n_balls)
+        t = scene.truth
+        tsel = np.linspace(0, len(t) - 1, min(len(t), self.n_balls)).astype(np.int64)
+        self.real, _, _, _ = OR.run_model(t.positions[tsel], t.p0[tsel], t.a0[tsel], self.sens, self.nrm,
+                                          float(scene.array.sound_speed), 0.0, scene.grid.dt,
+                                          scene.grid.n_samples, 1, kind=kind, threads=ncpu)
+        self.threads = None
+        self.sweep = {}
+
+    def _subset(self, m):
+        return np.linspace(0, len(self.scene.init) - 1, m).astype(np.int64)
+
+    def _run(self, sel, threads) -> float:
+        c, sc = self.scene.init, self.scene
         t0 = time.perf_counter()
-        OR.run_model(c.positions[sel], c.p0[sel], c.a0[sel], sens, nrm, 1500.0, 0.0, scene.grid.dt,
-                     scene.grid.n_samples, 1, real=real, stage="fine", kind=kind, threads=threads)
-        times.append(time.perf_counter() - t0)
-    pairs = n_sample * sens.shape[0]
-    return pairs / min(times), threads, f"{n_sample} balls (strided subset) x {sens.shape[0]} detectors, " \
-                                        f"fine backward (fwd+adj), best of {steps}"
+        self.OR.run_model(c.positions[sel], c.p0[sel], c.a0[sel], self.sens, self.nrm, float(sc.array.sound_speed),
+                          0.0, sc.grid.dt, sc.grid.n_samples, 1, real=self.real, stage="fine", kind=self.kind,
+                          threads=threads)
+        return time.perf_counter() - t0
+
+    def pick_threads(self, sweep_balls: int = 6000) -> int:
+        sel = self._subset(min(sweep_balls, self.n_balls))
+        blocks = -(-self.sens.shape[0] // 8)
+        cands = [t for t in self.SWEEP if t <= min(self.threads_avail, blocks)]
+        if min(self.threads_avail, blocks) not in cands:
+            cands.append(min(self.threads_avail, blocks))
+        for t in cands:
+            self.sweep[t] = len(sel) * self.sens.shape[0] / self._run(sel, t)
+        self.threads = max(self.sweep, key=self.sweep.get)
+        return self.threads
+
+    def pairs_per_s(self, reps: int) -> float:
+        if self.threads is None:
+            self.pick_threads()
+        best = min(self._run(self.sel, self.threads) for _ in range(max(1, reps)))
+        return self.n_balls * self.sens.shape[0] / best
+
+    def describe(self, value: float, reps: int) -> dict:
+        return {"value": value, "unit": UNIT, "cores": self.threads, "kind": "port",
+                "sample": f"{self.n_balls} balls (strided subset) x {self.sens.shape[0]} detectors of the workload, "
+                          f"fine backward (fwd+adj), FP64 numpy, best of {reps} at the best thread count",
+                "thread_sweep_pairs_per_s": {str(k): v for k, v in sorted(self.sweep.items())},
+                "host_threads": self.threads_avail, "cpu_model": cpu_model()}
 
 
 def run_reference(args, rank, world):
+    """The reference arm: the reference's CPU algorithm on the host cores
+    (rank 0 only; other ranks exit without work)."""
     if rank != 0:
         return
     scene, _, kind = make_scene(args)
-    vals = []
-    for _ in range(args.warmup + args.steps):
-        v, cores, sample = cpu_reference_pairs_per_s(scene, args.cpu_balls, steps=1, kind=kind)
-        vals.append(v)
+    ref = CpuReference(scene, kind, args.cpu_balls, args.cpu_det)
+    ref.pick_threads()
+    vals = [ref.pairs_per_s(1) for _ in range(args.warmup + args.steps)]
     v = statistics.median(vals[args.warmup:]) if args.steps else vals[-1]
     ms = args.n_balls * args.n_det / v * 1e3
+    cpu = ref.describe(v, 1)
+    cpu["sample"] = cpu["sample"].replace("best of 1", f"median of {args.steps} steps after {args.warmup} warm-up")
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": f"synthetic (seeded CounterRng, BASELINE config {args.config})",
-            "config": config_dict(args, world), "impl": "reference",
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+            "config": config_dict(args, world), "impl": "reference", "cpu_baseline": cpu,
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "note": "reference CPU algorithm = oracle/radiator.py (FP64 numpy port of paball radiator, "
-                    "key-fixed); ms_per_step extrapolated linearly to the full N*J"}
+            "note": "reference CPU algorithm = oracle/radiator.py (FP64 numpy restatement of paball radiator, "
+                    "key-fixed); each step = one fine backward of the sample; ms_per_step extrapolated linearly "
+                    "to the full N*J"}
     print(json.dumps(line), flush=True)
 
 
 # ---------------------------------------------------------------------------
-# Our arm
+# BASELINE's second metric and the launch-bound toy
 # ---------------------------------------------------------------------------
 
-def run_recon():
+def recon_cpu_estimate(sc, kept, sched, trace, n_sub: int = 3000, threads: int | None = None):
+    """Extrapolated wall time of the same reconstruction on the reference's
+    CPU algorithm: one backward (the iteration's whole cost; Adam and density
+    control are O(N) numpy) timed per level on a strided n_sub-ball subset
+    of the filtered cloud with all detectors, scaled linearly by every
+    iteration's ball count (plus the initial filter on the 96^3 grid)."""
+    from oracle import radiator as OR
+    threads = threads or os.cpu_count() or 1
+    ctx_dt, n_samples = sc.grid.dt, sc.grid.n_samples
+    sens, v = sc.array.positions, float(sc.array.sound_speed)
+    sel = np.linspace(0, len(kept) - 1, min(n_sub, len(kept))).astype(np.int64)
+    truth = sc.truth
+    per_level = []
+    for lv in sched.levels:
+        n_out = -(-n_samples // lv.f)
+        real = np.zeros((sens.shape[0], n_out))
+        t0 = time.perf_counter()
+        OR.run_model(kept.positions[sel], kept.p0[sel], kept.a0[sel], sens, None, v, 0.0, ctx_dt, n_samples, lv.f,
+                     real=real, stage=lv.stage, threads=threads)
+        per_level.append((time.perf_counter() - t0) / len(sel))   # s per ball per iteration
+    total = per_level[0] * len(sc.init)   # the initial filter pass at f = 4 (same kernel sums, p0 = 0)
+    for r in trace.records:
+        total += per_level[r.level] * r.ball_count
+    del truth
+    return {"value_s": total, "kind": "port", "cores": threads,
+            "sample": f"one backward per level on {len(sel)} balls (strided subset of the filtered cloud) x "
+                      f"{sens.shape[0]} detectors, scaled by each iteration's ball count",
+            "s_per_ball_iteration": per_level}
+
+
+def run_recon(world: int):
     """BASELINE config 3 end to end through the public API: zero-gradient
     filter of the 96^3 grid at f = 4, then the (4,100,coarse), (2,100,fine),
     (1,100,fine) schedule with the filter re-applied every 10 iterations and
-    the reference density-control cadence; host wall clock."""
+    the reference density-control cadence; host wall clock (max over ranks)."""
     import torch
 
     import paper_2601_00551_b200 as P
@@ -255,14 +377,111 @@ def run_recon():
     kept, rep = P.zero_gradient_filter(sc.init, ctx, real, f=4)
     final, trace = P.run_hierarchical(kept, ctx, real, sched, th, lr=lr, seed=103, filter_every=10, plateau=False)
     torch.cuda.synchronize()
-    wall = time.perf_counter() - t0
-    return {"workload": "config3: 512 det, 96^3 init, 50k-ball truth, 40 MHz x 4096, schedule 4/2/1 x 100",
-            "wall_s": wall, "iterations": len(trace.records), "n_init": len(sc.init), "n_after_filter": len(kept),
-            "n_final": len(final), "loss_first": trace.records[0].loss, "loss_last": trace.records[-1].loss}
+    wall = max_over_ranks(time.perf_counter() - t0, world)
+    out = {"workload": "config3: 512 det, 96^3 init, 50k-ball truth, 40 MHz x 4096, filter at f=4 then schedule "
+                       "4/2/1 x 100 (filter every 10, density control every 100), fp32 kernels",
+           "wall_s": wall, "unit": "s", "higher_is_better": False, "iterations": len(trace.records),
+           "n_init": len(sc.init), "n_after_filter": len(kept), "n_final": len(final),
+           "loss_first": trace.records[0].loss, "loss_last": trace.records[-1].loss,
+           "path": "paper_2601_00551_b200.zero_gradient_filter + run_hierarchical (public API, host wall clock)"}
+    return out, (sc, kept, sched, trace)
+
+
+def run_config1(world: int):
+    """BASELINE config 1 (launch-bound toy) through the public API: forward of
+    the truth, zero-gradient filter of the 32^3 grid at f = 1, five fine Adam
+    steps; host wall clock of filter + steps (max over ranks)."""
+    import torch
+
+    import paper_2601_00551_b200 as P
+    from paper_2601_00551_b200 import scenes
+    sc = scenes.toy_config()
+    ctx = P.ForwardContext(sc.array, sc.grid)
+    real = P.simulate_signals(sc.truth, ctx)
+    lr = P.LearningRates.from_spacing(10e-3 / 32)
+
+    def once():
+        kept, _ = P.zero_gradient_filter(sc.init, ctx, real, f=1)
+        state = P.create_state(kept, lr=lr, seed=103)
+        for _ in range(5):
+            state, _ = P.step(state, ctx, real, 1, "fine")
+        return state
+
+    once()
+    times = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        state = once()
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    return {"workload": "config1 toy: 256 det, 32^3 init, filter at f=1 + 5 fine Adam steps (public API)",
+            "wall_ms": 1e3 * max_over_ranks(min(times), world), "unit": "ms", "higher_is_better": False,
+            "n_after_filter": state.n, "best_of": 3}
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world <= 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64,
+                     device="cuda" if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# Our arm
+# ---------------------------------------------------------------------------
+
+def relaunch_under_torchrun(args) -> int:
+    """``--gpus N`` outside torchrun: run this script as N ranks."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
+def nominal_fp32_peak(sms: int) -> tuple[float, float, str]:
+    """Fixed roofline denominators: the FFMA2 rate (256 FP32 flop/clk/SM)
+    and MUFU ex2 rate (16/clk/SM) at the measured maximum SM clock."""
+    mhz, src = 1965.0, "1965 MHz (B200 clocks.max.sm)"
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            mhz = float(json.load(fh)["sm_max_mhz"])
+            src = f"{mhz:.0f} MHz (MEASURED_PEAKS.json sm_max_mhz)"
+    except (OSError, KeyError, ValueError):
+        pass
+    return sms * 256 * mhz * 1e6, sms * 16 * mhz * 1e6, \
+        f"nominal: {sms} SMs x 256 FP32 flop/clk (FFMA2) and 16 ex2/clk at {src}"
+
+
+def probe_peaks():
+    """Live FP32 / ex2 / shared-memory RMW probes (tools/probe), reported
+    beside the fixed denominators."""
+    probe = os.path.join(ROOT, "tools", "probe", "libfp32_peak.so")
+    try:
+        lib = ctypes.CDLL(probe)
+        fl, ex, rm = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        out = {}
+        if lib.probe_fp32_peak(3, ctypes.byref(fl), ctypes.byref(ex)) == 0:
+            out["fp32_tflops"], out["ex2_per_s"] = fl.value / 1e12, ex.value
+        if lib.probe_smem_rmw(3, ctypes.byref(rm)) == 0:
+            out["smem_rmw_per_s"] = rm.value
+        return out
+    except (OSError, AttributeError):
+        return {}
 
 
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch_under_torchrun(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -273,15 +492,22 @@ def main():
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local)
+    ndev = max(1, torch.cuda.device_count())
+    oversubscribed = world > ndev
+    dev = torch.device("cuda", local % ndev)
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
+        if oversubscribed:   # ranks share GPUs: gloo over host memory, no rank waits inside a kernel
+            dist.init_process_group("gloo")
+        else:
+            os.environ.setdefault("NCCL_DEBUG", "INFO")          # init log: the driver can check nranks
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            dist.init_process_group("nccl", device_id=dev)
 
     import paper_2601_00551_b200 as P
+    from paper_2601_00551_b200 import _lib
     from paper_2601_00551_b200 import engine as E
     from paper_2601_00551_b200 import radiator as R
-    from paper_2601_00551_b200 import scenes
 
     scene, dirkw, kind = make_scene(args)
     ctx = P.ForwardContext(scene.array, scene.grid, directivity=P.Directivity(**dirkw))
@@ -294,13 +520,17 @@ def main():
     counters = E.PassCounters(dev)
     real_local, _ = E.forward_rows(truth, det, acq, counters)
     real_local = real_local.clone()
+    del truth
     cloud = E.DeviceCloud.from_host(scene.init.positions, scene.init.p0, scene.init.a0, dev)
     cloud.pack()
     res_buf = torch.empty_like(real_local)
+    flat_buf = torch.empty(5 * cloud.n + E.TAIL, dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
 
     def one_step(ev=None):
+        """forward + residual/loss + adjoint + finalize (+ the one all-reduce
+        of gradients and pass tail for N > 1), inputs resident."""
         c = E.PassCounters(dev)
         cloud.invalidate()   # parameters change every iteration: repack (the optimizer's per-step cost;
         #                      the sort order and the dual-walk pairing table persist until a resort)
@@ -310,22 +540,22 @@ def main():
         res, loss_rows = E.forward_rows(cloud, det, acq, c, real_local=real_local, out=res_buf)
         if ev:
             ev[1].record(stream)
-        g = E.adjoint_grads(cloud, det, acq, res, 1.0, 2, 2.0 / n_total, c)
+        E.adjoint_grads(cloud, det, acq, res, 1.0, 2, 2.0 / n_total, c, flat=flat_buf, loss_rows=loss_rows)
         if ev:
             ev[2].record(stream)
-        return c, loss_rows, g
+        return c
 
     for k in range(args.warmup):   # exactly the timed loop's launches (flush, events), untimed
         flush.fill_(float(k))
         E.TIMING = {n: [torch.cuda.Event(enable_timing=True) for _ in range(2)] for n in ("residual", "finalize")}
-        c, _, _ = one_step([torch.cuda.Event(enable_timing=True) for _ in range(3)])
+        c = one_step([torch.cuda.Event(enable_timing=True) for _ in range(3)])
     E.TIMING = None
     torch.cuda.synchronize()
-    ops_per_step = c.read()
+    _, ops_per_step = c.result()
 
-    # kernel-level events: pack+forward+residual, adjoint+finalize(+allreduce)
+    # kernel-level events: pack+forward+residual, adjoint+finalize(+all-reduce)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    sampler = ClockSampler(local, dev, period=float(os.environ.get("PAB_BENCH_CLOCK_PERIOD", "0.05")))
+    sampler = ClockSampler(dev.index, dev, period=float(os.environ.get("PAB_BENCH_CLOCK_PERIOD", "0.05")))
     hbm_evs = []
     # the sampler thread is running (steady state) before the timed region
     # opens, so its start-up never delays a kernel launch inside it; its
@@ -335,11 +565,13 @@ def main():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+        launches0 = _lib.LAUNCHES["kernels"]
         for k in range(args.steps):
             flush.fill_(float(k))
             E.TIMING = {n: [torch.cuda.Event(enable_timing=True) for _ in range(2)] for n in ("residual", "finalize")}
             hbm_evs.append(E.TIMING)
             one_step(evs[k])
+        launches = _lib.LAUNCHES["kernels"] - launches0
         torch.cuda.synchronize()
     E.TIMING = None
     if world > 1:
@@ -348,93 +580,88 @@ def main():
     adj_ms = [e[1].elapsed_time(e[2]) for e in evs]
     step_ms = [e[0].elapsed_time(e[2]) for e in evs]
     mean_step = sum(step_ms) / len(step_ms)
-    print("step_ms " + " ".join(f"{x:.2f}" for x in step_ms) + " | fwd " + " ".join(f"{x:.2f}" for x in fwd_ms)
-          + " | adj " + " ".join(f"{x:.2f}" for x in adj_ms), file=sys.stderr)
-    t = torch.tensor([mean_step], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    print(f"rank {rank} step_ms " + " ".join(f"{x:.2f}" for x in step_ms) + " | fwd "
+          + " ".join(f"{x:.2f}" for x in fwd_ms) + " | adj " + " ".join(f"{x:.2f}" for x in adj_ms), file=sys.stderr)
+    ms_max = max_over_ranks(mean_step, world)
     pairs = args.n_balls * det.n_total
     value = pairs / (ms_max * 1e-3)
 
-    # end to end through the public API: host (pinned) cloud + supervision in,
-    # loss + gradients out, every step
+    # end to end through the public API: host cloud + supervision in, loss +
+    # gradients out, every step; pageable numpy arrays (what a caller of the
+    # reference API holds) and, beside it, the same with page-locked arrays
     e2e = None
     if args.e2e_steps > 0:
-        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
-        host_cloud = P.PointCloud(pin(scene.init.positions), pin(scene.init.p0), pin(scene.init.a0))
-        real_full = E.full_rows(real_local, det).double().cpu()
-        host_real = P.SignalSet(scene.grid, real_full.pin_memory().numpy())
-        P.backward(host_cloud, ctx, host_real, stage="fine")
-        e2e_ms = []
-        for _ in range(args.e2e_steps):
-            R._sup_cache.clear()
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
+        real_full = E.full_rows(real_local, det).double().cpu().numpy()
+
+        def time_e2e(host_cloud, host_real):
             P.backward(host_cloud, ctx, host_real, stage="fine")
-            torch.cuda.synchronize()
-            e2e_ms.append((time.perf_counter() - t0) * 1e3)
-        tt = torch.tensor([statistics.median(e2e_ms)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = []
+            for _ in range(args.e2e_steps):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                P.backward(host_cloud, ctx, host_real, stage="fine")
+                torch.cuda.synchronize()
+                ms.append((time.perf_counter() - t0) * 1e3)
+            return max_over_ranks(statistics.median(ms), world)
+
+        pageable_ms = time_e2e(P.PointCloud(scene.init.positions.copy(), scene.init.p0.copy(),
+                                            scene.init.a0.copy()), P.SignalSet(scene.grid, real_full))
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+        pinned_ms = time_e2e(P.PointCloud(pin(scene.init.positions), pin(scene.init.p0), pin(scene.init.a0)),
+                             P.SignalSet(scene.grid, pin(real_full)))
         n = args.n_balls
-        h2d = n * 5 * 8 + det.n_total * acq.n_out * 8 // world * world
-        d2h = n * 5 * 8 + 8
-        e2e = {"value": pairs / (float(tt.item()) * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": float(tt.item()),
-               "path": "paper_2601_00551_b200.backward(PointCloud, ForwardContext, SignalSet, 'fine') "
-                       "with pinned host numpy inputs; supervision re-uploaded every step"}
+        h2d = n * 5 * 8 + det.n_total * acq.n_out * 8
+        d2h = (5 * n + E.TAIL) * 8
+        e2e = {"value": pairs / (pageable_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": pageable_ms,
+               "path": "paper_2601_00551_b200.backward(PointCloud, ForwardContext, SignalSet, 'fine') with pageable "
+                       "host numpy inputs (as a reference caller holds them); cloud and supervision uploaded and "
+                       "loss + gradients downloaded every step",
+               "pinned": {"value": pairs / (pinned_ms * 1e-3), "ms_per_step": pinned_ms,
+                          "path": "same call with page-locked host arrays"}}
+
+    recon = recon_state = None
+    if not args.no_recon and args.config == 2:
+        recon, recon_state = run_recon(world)
+    config1 = None
+    if not args.no_config1 and args.config == 2:
+        config1 = run_config1(world)
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
 
-    # roofline of the dominant kernel: the
-    # forward against the north star's ceiling, the FP32 CUDA-core peak, with
-    # SURVEY §8d's algorithmic 7 FP32 flops per in-window sample (the
-    # reference op count); the canonical ex2 (1 per sample) and shared-memory
-    # RMW (8 B per sample) ceilings of the same work, and both kernels'
-    # fractions, are reported beside it.  Peaks are probed live on this GPU.
-    probe = os.path.join(ROOT, "tools", "probe", "libfp32_peak.so")
-    peak_flops = peak_ex2 = peak_rmw = None
-    peak_kind = "measured live (tools/probe: FFMA2 chains, ex2 chains, private-column smem RMW; this GPU)"
-    try:
-        lib = ctypes.CDLL(probe)
-        fl, ex, rm = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
-        if lib.probe_fp32_peak(3, ctypes.byref(fl), ctypes.byref(ex)) == 0:
-            peak_flops, peak_ex2 = fl.value, ex.value
-        if lib.probe_smem_rmw(3, ctypes.byref(rm)) == 0:
-            peak_rmw = rm.value
-    except (OSError, AttributeError):
-        pass
+    # roofline of the dominant kernel against
+    # the north star's ceiling, the FP32 CUDA-core peak (fixed nominal
+    # denominator; the live probes are printed beside it), with SURVEY §8d's
+    # algorithmic flops per in-window sample (the reference op count): 7 for
+    # the forward, 12 for the fine adjoint
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    if peak_flops is None or peak_rmw is None:
-        peak_flops, peak_ex2, peak_rmw = sms * 256 * 1.965e9, sms * 16 * 1.965e9, sms * 14.4 * 1.965e9
-        peak_kind = "nominal at 1965 MHz (FFMA2 256 flop/clk/SM, ex2 16/clk/SM, smem RMW 14.4/clk/SM)"
+    peak_flops, peak_ex2, peak_src = nominal_fp32_peak(sms)
     fwd_mean = sum(fwd_ms) / len(fwd_ms)
     adj_mean = sum(adj_ms) / len(adj_ms)
-    samples = ops_per_step   # in-window samples evaluated by the forward (== adjoint)
+    samples = ops_per_step   # in-window samples of the pass over all ranks (== the adjoint's)
+    local_samples = samples / world
     fwd_s, adj_s = fwd_mean * 1e-3, adj_mean * 1e-3
-    ach = FLOPS_FWD * samples / fwd_s
+    kernels = {"forward_kernel": (FLOPS_FWD, fwd_s, "forward+residual events; pack and residual are ~0.3%"),
+               "adjoint_kernel": (FLOPS_ADJ_FINE, adj_s, "adjoint+finalize events; finalize is ~0.4%")}
+    dom = max(kernels, key=lambda k: kernels[k][1])
+    fl, secs, note = kernels[dom]
+    ach = fl * local_samples / secs
     roofline = {"bound": "fp32", "achieved": ach / 1e12, "peak": peak_flops / 1e12, "unit": "TFLOP/s",
-                "frac": ach / peak_flops, "traffic": TRAFFIC_FWD_BYTES, "kernel": "forward_kernel",
-                "peak_source": peak_kind,
-                "algorithmic": f"{FLOPS_FWD} FP32 flops x {samples} in-window samples per launch (SURVEY 8d; "
-                               "forward+residual events, of which pack and residual are ~0.3%)",
-                "traffic_unit": "DRAM bytes per forward launch (ncu --set full, profiles/r01_v12; 6 partition planes written)",
+                "frac": ach / peak_flops, "traffic": TRAFFIC_BYTES.get(dom), "kernel": dom,
+                "peak_source": peak_src, "peak_probe_live": probe_peaks(),
+                "algorithmic": f"{fl} FP32 flops x {int(local_samples)} in-window samples per launch (SURVEY 8d; {note})",
+                "traffic_unit": f"DRAM bytes per launch (ncu --set full, {TRAFFIC_SRC})",
                 "other_bounds": {
-                    "forward_ex2 (1 per sample)": {"frac": samples / fwd_s / peak_ex2, "peak_per_s": peak_ex2},
-                    "forward_smem_rmw (8 B per sample)": {"frac": samples / fwd_s / peak_rmw,
-                                                          "peak_GBps": 8.0 * peak_rmw / 1e9},
-                    "adjoint_ex2 (its binding ceiling)": {"frac": samples / adj_s / peak_ex2},
-                    "adjoint_fp32": {"frac": FLOPS_ADJ_FINE * samples / adj_s / peak_flops},
+                    "forward_fp32 (7 flops per sample)": {"frac": FLOPS_FWD * local_samples / fwd_s / peak_flops},
+                    "adjoint_fp32 (12 flops per sample)": {"frac": FLOPS_ADJ_FINE * local_samples / adj_s / peak_flops},
+                    "forward_ex2 (1 per sample)": {"frac": local_samples / fwd_s / peak_ex2},
+                    "adjoint_ex2 (1 per sample)": {"frac": local_samples / adj_s / peak_ex2},
                     "path_fp32 (fwd+adj, 19 flops per sample)": {
-                        "frac": (FLOPS_FWD + FLOPS_ADJ_FINE) * samples / (ms_max * 1e-3) / peak_flops},
-                    "path_ex2 (fwd+adj, 2 ex2 per sample)": {"frac": 2 * samples / (ms_max * 1e-3) / peak_ex2}},
-                "design_note": "the forward's dual walk executes 0.5 ex2, 4 FP32 lane-ops and 4 B of shared RMW per "
-                               "walked ball-sample (1.28 walked per in-window sample); no pipe is saturated "
-                               "(ncu r01_v12: issue slots 69%, ALU 42%, XU 40%, FMA 32%, LSU 17%)",
+                        "frac": (FLOPS_FWD + FLOPS_ADJ_FINE) * local_samples / (ms_max * 1e-3) / peak_flops},
+                    "path_ex2 (fwd+adj, 2 ex2 per sample)": {"frac": 2 * local_samples / (ms_max * 1e-3) / peak_ex2}},
                 "kernel_ms": {"forward+residual": fwd_mean, "adjoint+finalize": adj_mean}}
 
     # the HBM-bound kernels of the step (signal and gradient traffic) against
@@ -459,8 +686,12 @@ def main():
 
     cpu = None
     if world == 1 and not args.no_cpu:
-        v, cores, sample = cpu_reference_pairs_per_s(scene, args.cpu_balls, steps=1, kind=kind)
-        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+        ref = CpuReference(scene, kind, args.cpu_balls, args.cpu_det)
+        ref.pick_threads()
+        cpu = ref.describe(ref.pairs_per_s(args.cpu_reps), args.cpu_reps)
+        if recon is not None:
+            sc3, kept3, sched3, trace3 = recon_state
+            recon["cpu_reference"] = recon_cpu_estimate(sc3, kept3, sched3, trace3, threads=ref.threads)
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
@@ -468,11 +699,22 @@ def main():
             "data": f"synthetic (seeded CounterRng, BASELINE config {args.config})", "config": config_dict(args, world),
             "in_window_samples_per_step": samples, "samples_per_pair": samples / pairs,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": sampler.summary(),
-            "gpu_launches": 5 * args.steps,   # pack, forward, residual, adjoint, finalize (pairing table: per sort)
+            "gpu_launches": int(launches),
+            "gpu_launches_note": "library kernels issued inside the timed region (counted by _lib.call): per step "
+                                 "pack x2 (forward and adjoint packings), forward, residual, adjoint, finalize, "
+                                 "pass tail",
             "kernel_ms_min_median": {"forward+residual": [min(fwd_ms), statistics.median(fwd_ms)],
                                      "adjoint+finalize": [min(adj_ms), statistics.median(adj_ms)]}}
-    if args.recon:
-        line["recon"] = run_recon()
+    if world > 1:
+        line["collective"] = {"backend": dist.get_backend(), "per_step": "one all-reduce of (5 n + 4) FP64",
+                              "oversubscribed": oversubscribed, "gpus_visible": ndev}
+        if oversubscribed:
+            line["note"] = (f"{world} ranks on {ndev} GPU(s): the multi-rank path runs (gloo all-reduce), "
+                            "the number is not a scaling measurement")
+    if recon is not None:
+        line["recon"] = recon
+    if config1 is not None:
+        line["config1"] = config1
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -106,6 +106,18 @@ int pab_adjoint(const void* rec_a, const void* rec_b, const void* group_meta, in
 int pab_grad_finalize(const double* grad_partial, int chunks, int64_t n_groups, const void* rec_b, double scale,
                       int stage, double* d_p0, double* d_a0, double* d_pos, int* status, void* stream);
 
+/* Pass tail (4 doubles) appended to the per-ball gradient buffer, so that
+ * one all-reduce per iteration carries gradients, loss, error flags and op
+ * count across detector shards: tail[0] = sum of loss_rows[0..n_rows) in row
+ * order (loss_rows nullable: 0), tail[1] = 1 if *status has the coincident
+ * bit (SimulationError), tail[2] = 1 if it has the non-finite bit
+ * (OptimizationError), tail[3] = *ops (nullable: 0).  After the sum over
+ * ranks every rank raises the same error at the same step.
+ * Replaces: the merge of block losses and op counts, radiator.py:336-344,
+ * and the finite check of optimizer.py:284-294. */
+int pab_pass_tail(const double* loss_rows, int n_rows, const unsigned long long* ops, const int* status,
+                  double* tail, void* stream);
+
 /* Pure decimation of FP32 rows: dst[r][k] = src[r][k*f], k < ceil(n_in/f).
  * Replaces: radiator.downsample (radiator.py:382-390). */
 int pab_decimate(const float* src, int n_rows, int n_in, int f, float* dst, void* stream);

@@ -30,6 +30,7 @@ _SIGS = {
     "pab_adjoint": ([_vp, _vp, _vp, _i64, _vp, _vp, _i, _d, _d, _d, _i, _i, _d, _i, _d, _vp, _f, _i, _i, _i,
                      _vp, _vp, _vp, _vp], _i),
     "pab_grad_finalize": ([_vp, _i, _i64, _vp, _d, _i, _vp, _vp, _vp, _vp, _vp], _i),
+    "pab_pass_tail": ([_vp, _i, _vp, _vp, _vp, _vp], _i),
     "pab_decimate": ([_vp, _i, _i, _i, _vp, _vp], _i),
     "pab_adam": ([_vp, _vp, _vp, _vp, _i64, _d, _d, _d, _d, _i, _vp], _i),
     "pab_compact_workspace_bytes": ([_i64], C.c_size_t),
@@ -81,10 +82,18 @@ def load(path: str = LIB_PATH):
     return lib
 
 
+# Kernel launches issued through call() (bench.py reports the count inside
+# its timed region as gpu_launches).  Every launching entry point issues one
+# kernel, except these.
+LAUNCHES = {"kernels": 0}
+_KERNELS_PER_CALL = {"pab_compact": 3, "pab_sumsq_diff_f64": 2}
+
+
 def call(name: str, *args) -> None:
     """Invoke an entry point and turn non-zero return codes into errors."""
     lib = load()
     rc = getattr(lib, name)(*args)
+    LAUNCHES["kernels"] += _KERNELS_PER_CALL.get(name, 1)
     if rc != 0:
         if rc == 1:
             raise ValueError(f"{name}: invalid argument (rc=1)")

@@ -172,6 +172,28 @@ __global__ void sum_ordered_kernel(const double* __restrict__ partial, int np, d
   }
 }
 
+// Per-pass tail of the gradient buffer (one all-reduce carries gradients,
+// loss, error flags and the op count across detector shards): the loss rows
+// summed in row order by one warp (fixed lane-strided partials, fixed
+// shuffle tree: bitwise reproducible), the status bits as 0/1 counts and the
+// op counter as a double (exact below 2^53).
+__global__ void pass_tail_kernel(const double* __restrict__ loss_rows, int n_rows,
+                                 const unsigned long long* __restrict__ ops, const int* __restrict__ status,
+                                 double* __restrict__ tail) {
+  const int lane = threadIdx.x;
+  double acc = 0.0;
+  if (loss_rows)
+    for (int i = lane; i < n_rows; i += 32) acc += loss_rows[i];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) {
+    const int st = status ? *status : 0;
+    tail[0] = acc;
+    tail[1] = (st & kStatusCoincident) ? 1.0 : 0.0;
+    tail[2] = (st & kStatusNonFinite) ? 1.0 : 0.0;
+    tail[3] = ops ? (double)*ops : 0.0;
+  }
+}
+
 }  // namespace pab
 
 using namespace pab;
@@ -242,6 +264,13 @@ int pab_sumsq_diff_f64(const double* a, const double* b, int64_t n, double* out,
   }
   ssd_partial_kernel<<<nb, kSsdBlock, 0, s>>>(a, b, n, (double*)workspace);
   sum_ordered_kernel<<<1, 32, 0, s>>>((const double*)workspace, nb, out);
+  return cudaGetLastError() == cudaSuccess ? 0 : 4;
+}
+
+int pab_pass_tail(const double* loss_rows, int n_rows, const unsigned long long* ops, const int* status,
+                  double* tail, void* stream) {
+  if (!tail || n_rows < 0) return 1;
+  pass_tail_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(loss_rows, n_rows, ops, status, tail);
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 

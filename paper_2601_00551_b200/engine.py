@@ -5,8 +5,9 @@ arithmetic on the path runs in the sm_100a library (``_lib``).
 
 Multi-GPU: one process per GPU, detectors sharded in
 contiguous blocks; the ball cloud, its Adam state and every per-ball decision
-are replicated.  The forward is detector-local; the two exchanges per
-iteration are the scalar loss and the per-ball gradient all-reduce (NCCL).
+are replicated.  The forward is detector-local; the one exchange per
+iteration is the all-reduce (NCCL) of the per-ball gradient buffer, whose
+tail carries the loss, the error flags and the op count.
 """
 
 from __future__ import annotations
@@ -22,10 +23,8 @@ import torch
 from . import _lib
 from ._lib import call, ptr
 from .model import OptimizationError, SimulationError
-from .parallel import Shard, allreduce_scalar, allreduce_sum_, current_shard, gather_rows  # noqa: F401
+from .parallel import TAIL, Shard, allreduce_sum_, current_shard, gather_rows, read_tail  # noqa: F401
 
-STATUS_COINCIDENT = 2
-STATUS_NONFINITE = 8
 
 FORWARD_WARPS = int(os.environ.get("PAB_FWD_WARPS", "4"))   # 2 CTAs per SM: one sorts while the other sweeps
 FORWARD_TILE_ROWS = 160   # reserved ABI argument (the library's tile height is a build constant)
@@ -312,27 +311,68 @@ def plan_adjoint(cloud: DeviceCloud, det: DeviceDetectors) -> int:
 # ---------------------------------------------------------------------------
 
 
-def _check_status(status: torch.Tensor) -> None:
-    s = int(status.item())
-    if s & STATUS_COINCIDENT:
-        raise SimulationError("ball coincident with a sensor (zero source-sensor distance)")
-    if s & STATUS_NONFINITE:
-        raise OptimizationError("non-finite gradient")
+# Every gradient buffer ends in the pass tail (parallel.TAIL doubles, written
+# by pab_pass_tail): loss sum, coincident flag, non-finite flag, op count.  It
+# rides in the same all-reduce as the per-ball gradients: one collective per
+# iteration, and every rank sees the same loss, error flags and op count (so
+# every rank raises the same error at the same step).
 
 
 class PassCounters:
-    """Device op counter + status word for one API call."""
+    """Device op counter + status word for one API call, reduced over ranks
+    through the pass tail."""
 
     def __init__(self, dev):
         ws = workspace(dev)
+        self.dev = dev
         self.ops = ws.get("ops", 1, torch.int64)
         self.status = ws.get("status", 1, torch.int32)
         self.ops.zero_()
         self.status.zero_()
+        self.tail = None   # device tail of this pass (after the all-reduce)
+        self._host_tail = None
+
+    def close(self, loss_rows: torch.Tensor | None = None, tail: torch.Tensor | None = None) -> torch.Tensor:
+        """Write this rank's pass tail (device) from its loss rows, status
+        word and op counter."""
+        if tail is None:
+            tail = workspace(self.dev).get("tail", TAIL, torch.float64)
+        n_rows = 0 if loss_rows is None else int(loss_rows.numel())
+        call("pab_pass_tail", ptr(loss_rows) if n_rows else None, n_rows, ptr(self.ops), ptr(self.status),
+             ptr(tail), _stream())
+        return tail
+
+    def result(self, host_tail=None, check_nonfinite: bool = True) -> tuple[float, int]:
+        """(loss sum, op count) of the pass summed over ranks; raises the
+        reference's error classes, identically on every rank.  A pass
+        without an adjoint (forward only) reduces its tail here."""
+        loss_sum, coincident, nonfinite, ops = read_tail(self._host(host_tail))
+        if coincident:
+            raise SimulationError("ball coincident with a sensor (zero source-sensor distance)")
+        if check_nonfinite and nonfinite:
+            raise OptimizationError("non-finite gradient")
+        return loss_sum, ops
+
+    def _host(self, host_tail=None):
+        if host_tail is None:
+            if self._host_tail is not None:
+                return self._host_tail
+            if self.tail is None:
+                t = self.close()
+                if current_shard().world > 1:
+                    allreduce_sum_(t)
+                self.tail = t
+            host_tail = self.tail.cpu().numpy()
+        self._host_tail = host_tail
+        return host_tail
+
+    def tail_flags(self) -> tuple[bool, bool]:
+        """(coincident, non-finite) of the reduced pass tail."""
+        _, coincident, nonfinite, _ = read_tail(self._host())
+        return coincident, nonfinite
 
     def read(self) -> int:
-        _check_status(self.status)
-        return int(self.ops.item())
+        return self.result()[1]
 
 
 # bench hook: {"residual" | "finalize": [start, end] CUDA events} recorded on the
@@ -386,22 +426,25 @@ def forward_rows(cloud: DeviceCloud, det: DeviceDetectors, acq: Acq, counters: P
 
 def adjoint_grads(cloud: DeviceCloud, det: DeviceDetectors, acq: Acq, res: torch.Tensor, res_sign: float,
                   stage: int, scale: float, counters: PassCounters, count_ops: bool = False,
-                  flat: torch.Tensor | None = None):
+                  flat: torch.Tensor | None = None, loss_rows: torch.Tensor | None = None):
     """Per-ball loss gradients in caller order (FP64), reduced over ranks.
     stage: 0 filter (d_p0 only), 1 coarse, 2 fine.  The three fields are
-    views of one contiguous buffer ``flat`` ([n] for stage 0, [5n] otherwise;
-    allocated when not given): one all-reduce, one host copy."""
+    views of one contiguous buffer ``flat`` ([n] for stage 0, [5n] otherwise,
+    then the TAIL-double pass tail with this pass's loss (``loss_rows``),
+    error flags and op count; allocated when not given): one all-reduce,
+    one host copy.  ``counters.tail`` is the reduced tail."""
     dev = cloud.dev
     n = cloud.n
     width = 1 if stage == 0 else 5
     if flat is None:
-        flat = torch.zeros(width * n, dtype=torch.float64, device=dev)
+        flat = torch.zeros(width * n + TAIL, dtype=torch.float64, device=dev)
     else:
-        flat = flat[: width * n]
+        flat = flat[: width * n + TAIL]
         flat.zero_()
     d_p0 = flat[:n]
     d_a0 = flat[n:2 * n] if stage >= 1 else None
-    d_pos = flat[2 * n:].view(n, 3) if stage >= 1 else None
+    d_pos = flat[2 * n:5 * n].view(n, 3) if stage >= 1 else None
+    tail = flat[width * n:]
     if n > 0 and det.n_local > 0:
         cloud = cloud.adjoint_cloud()   # the adjoint's own packing (radius buckets)
         cloud.pack()
@@ -420,8 +463,10 @@ def adjoint_grads(cloud: DeviceCloud, det: DeviceDetectors, acq: Acq, res: torch
         _mark("finalize", 1)
         if TIMING is not None:
             TIMING["finalize_bytes"] = chunks * 5 * npad * 8 + npad * 16 + 5 * n * 8
+    counters.close(loss_rows, tail)
     if det.shard.world > 1:
-        allreduce_sum_(flat)
+        allreduce_sum_(flat)   # gradients + loss + flags + ops: the iteration's one collective
+    counters.tail = tail
     return d_p0, d_a0, d_pos
 
 

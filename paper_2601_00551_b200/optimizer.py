@@ -330,20 +330,18 @@ def _device_step(state: OptimState, det: E.DeviceDetectors, acq: E.Acq, real_loc
     res, loss_rows = E.forward_rows(dc, det, acq, counters, real_local=real_local)
     n_total = det.n_total * acq.n_out
     stage_code = 2 if stage == "fine" else 1
-    d_p0, d_a0, d_pos = E.adjoint_grads(dc, det, acq, res, 1.0, stage_code, 2.0 / n_total, counters)
-    loss_sum = float(loss_rows.sum().item())
-    if det.shard.world > 1:
-        loss_sum = E.allreduce_scalar(loss_sum, dc.dev)
+    d_p0, d_a0, d_pos = E.adjoint_grads(dc, det, acq, res, 1.0, stage_code, 2.0 / n_total, counters,
+                                        loss_rows=loss_rows)
+    # the one host read of the iteration: the all-reduced pass tail (loss,
+    # error flags, op count), identical on every rank
+    loss_sum, ops = counters.result(check_nonfinite=False)
     loss_value = loss_sum / n_total
-    status = int(counters.status.item())
-    if status & E.STATUS_COINCIDENT:
-        raise SimulationError("ball coincident with a sensor (zero source-sensor distance)")
-    if not math.isfinite(loss_value) or status & E.STATUS_NONFINITE:
+    if not math.isfinite(loss_value) or counters.tail_flags()[1]:
         raise OptimizationError(
             f"non-finite loss or gradient at step {state.step_count}: loss={loss_value}, "
             f"balls={dc.n}, p0 range=({float(dc.p0.min())}, {float(dc.p0.max())}), "
             f"a0 range=({float(dc.a0.min())}, {float(dc.a0.max())})")
-    R._add_ops(int(counters.ops.item()))
+    R._add_ops(ops)
     state.step_count += 1
     t = state.step_count
     _adam_(dc.p0, d_p0, state._m["p0"], state._v["p0"], state.lr.p0, t)
@@ -681,16 +679,13 @@ def positivity_refine(state: OptimState, ctx, real, iters: int) -> PointCloud:
         dc.invalidate()
         counters = E.PassCounters(dc.dev)
         res, loss_rows = E.forward_rows(dc, det, acq, counters, real_local=real_local)
-        d_p0, d_a0, d_pos = E.adjoint_grads(dc, det, acq, res, 1.0, 2, 2.0 / n_total, counters)
-        loss_sum = float(loss_rows.sum().item())
-        if det.shard.world > 1:
-            loss_sum = E.allreduce_scalar(loss_sum, dc.dev)
+        d_p0, d_a0, d_pos = E.adjoint_grads(dc, det, acq, res, 1.0, 2, 2.0 / n_total, counters,
+                                            loss_rows=loss_rows)
+        loss_sum, ops = counters.result(check_nonfinite=False)
         loss_value = loss_sum / n_total
-        if int(counters.status.item()) & E.STATUS_COINCIDENT:
-            raise SimulationError("ball coincident with a sensor (zero source-sensor distance)")
         if not math.isfinite(loss_value):
             raise OptimizationError(f"non-finite loss during refinement: {loss_value}")
-        R._add_ops(int(counters.ops.item()))
+        R._add_ops(ops)
         refine.step_count += 1
         t = refine.step_count
         _adam_(dc.p0, d_p0, refine._m["p0"], refine._v["p0"], refine.lr.p0, t)

@@ -15,6 +15,7 @@ reference semantics).
 
 from __future__ import annotations
 
+import hashlib
 import os
 import threading
 from dataclasses import dataclass, field
@@ -179,7 +180,20 @@ def _directivity(ctx) -> Directivity:
 # ---------------------------------------------------------------------------
 
 _det_cache: dict = {}
-_sup_cache: list = []
+
+
+def _detector_key(arr, d, dev, shard) -> tuple:
+    """Content key of a sensor layout: the reference recomputes from the
+    arrays on every call (radiator.py:316-332), so an in-place edit of
+    ``positions`` / ``normals`` must reach the device; the digest of ~50 KB
+    costs microseconds."""
+    h = hashlib.blake2b(digest_size=16)
+    pos = np.ascontiguousarray(arr.positions, dtype=np.float64)
+    h.update(pos.tobytes())
+    nrm = getattr(arr, "normals", None)
+    if nrm is not None:
+        h.update(np.ascontiguousarray(nrm, dtype=np.float64).tobytes())
+    return (h.digest(), pos.shape, float(arr.sound_speed), dev.index, shard, d)
 
 
 def device_detectors(ctx) -> E.DeviceDetectors:
@@ -187,21 +201,15 @@ def device_detectors(ctx) -> E.DeviceDetectors:
     shard = E.current_shard_for(dev)
     d = _directivity(ctx)
     arr = ctx.array
-    key = (id(arr), dev.index, shard, d)
+    key = _detector_key(arr, d, dev, shard)
     hit = _det_cache.get(key)
-    if hit is not None and hit[0] is arr:
-        return hit[1]
+    if hit is not None:
+        return hit
     det = E.DeviceDetectors(arr.positions, getattr(arr, "normals", None), d, arr.sound_speed, dev, shard)
     if len(_det_cache) > 16:
         _det_cache.clear()
-    _det_cache[key] = (arr, det)
+    _det_cache[key] = det
     return det
-
-
-def _fingerprint(a: np.ndarray) -> tuple:
-    flat = a.reshape(-1)
-    step = max(1, flat.size // 61)
-    return (a.ctypes.data, a.shape, a.strides, flat[::step].tobytes())
 
 
 _side_streams: dict = {}
@@ -215,16 +223,16 @@ def _side_stream(dev) -> torch.cuda.Stream:
 
 
 def device_supervision(data: np.ndarray, det: E.DeviceDetectors, defer: bool = False):
-    """This rank's supervision rows as FP32 on device (cached per array).
+    """This rank's supervision rows as FP32 on device, uploaded on every
+    call: the reference reads ``real.data`` on every call, so an in-place
+    edit between calls must be seen (no content cache; the iteration
+    driver ``run_hierarchical`` keeps its own device copy of the array it
+    was given).
 
     The rows travel in their host dtype (no host-side conversion pass) on a
     side stream and are narrowed on the device.  ``defer=True`` returns
-    (tensor, event or None) without making the current stream wait, so the
-    copy overlaps whatever is enqueued before the caller waits on the event."""
-    key = (_fingerprint(data), det.lo, det.hi)
-    for k, t in _sup_cache:
-        if k == key:
-            return (t, None) if defer else t
+    (tensor, event) without making the current stream wait, so the copy
+    overlaps whatever is enqueued before the caller waits on the event."""
     dev = det.pos.device
     host = torch.from_numpy(np.ascontiguousarray(data[det.lo:det.hi]))
     main = torch.cuda.current_stream(dev)
@@ -235,9 +243,6 @@ def device_supervision(data: np.ndarray, det: E.DeviceDetectors, defer: bool = F
         ev = torch.cuda.Event()
         ev.record(side)
     t.record_stream(main)
-    _sup_cache.append((key, t))
-    if len(_sup_cache) > 4:
-        _sup_cache.pop(0)
     if defer:
         return t, ev
     main.wait_event(ev)
@@ -290,19 +295,18 @@ def _run_model(cloud, ctx, f, real=None, stage="fine"):
     res, loss_rows = E.forward_rows(dc, det, acq, counters, real_local=real_local, real_ready=real_ready)
     stage_code = 2 if stage == "fine" else 1
     n_total = det.n_total * n_out
-    flat = torch.empty(5 * n, dtype=torch.float64, device=dev)
-    E.adjoint_grads(dc, det, acq, res, 1.0, stage_code, 2.0 / n_total, counters, flat=flat)
-    # one copy into page-locked host memory; the returned arrays are views
-    # that keep it alive
-    host = torch.empty(5 * n, dtype=torch.float64, pin_memory=True)
+    flat = torch.empty(5 * n + E.TAIL, dtype=torch.float64, device=dev)
+    # gradients, loss, error flags and op count in one buffer: one
+    # all-reduce over detector shards, one copy into page-locked host memory
+    # (the returned arrays are views that keep it alive)
+    E.adjoint_grads(dc, det, acq, res, 1.0, stage_code, 2.0 / n_total, counters, flat=flat, loss_rows=loss_rows)
+    host = torch.empty(5 * n + E.TAIL, dtype=torch.float64, pin_memory=True)
     host.copy_(flat, non_blocking=True)
-    loss_sum = E.allreduce_scalar(float(loss_rows.sum().item()), dev) if det.shard.world > 1 \
-        else float(loss_rows.sum().item())
-    ops = counters.read()
-    _add_ops(ops)
     torch.cuda.current_stream(dev).synchronize()
     h = host.numpy()
-    grads = ParamGradients(h[:n], h[n:2 * n], h[2 * n:].reshape(n, 3))
+    loss_sum, ops = counters.result(host_tail=h[5 * n:], check_nonfinite=False)
+    _add_ops(ops)
+    grads = ParamGradients(h[:n], h[n:2 * n], h[2 * n:5 * n].reshape(n, 3))
     return None, loss_sum / n_total, grads, ops
 
 

@@ -87,3 +87,58 @@ def test_two_rank_sharded_path_matches_single_process():
     # every rank holds the same cloud
     np.testing.assert_array_equal(res[0]["p0"], res[1]["p0"])
     np.testing.assert_array_equal(res[0]["pos"], res[1]["pos"])
+
+
+def _coincident_worker(rank, world, port, q):
+    """A ball sits on the last detector (rank 1's shard): only rank 1's
+    kernels see it, the reduced pass tail makes BOTH ranks raise
+    SimulationError at the same call (neither hangs in a later collective).
+    The op count each rank adds is the global one."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        P, sc, ctx = _instance()
+        real = P.simulate_signals(sc.truth, ctx)
+        P.reset_op_count()
+        P.backward(sc.init, ctx, real, stage="fine")
+        ops = P.op_count()
+        bad = sc.init.copy()
+        bad.positions[0] = sc.array.positions[-1]
+        raised = []
+        for call in (lambda: P.backward(bad, ctx, real, stage="fine"),
+                     lambda: P.step(P.create_state(bad, lr=P.LearningRates.from_spacing(4e-4)), ctx, real, 1,
+                                    "fine")):
+            try:
+                call()
+                raised.append(False)
+            except P.SimulationError:
+                raised.append(True)
+        # both ranks are still in step: one more collective completes
+        L, _ = P.backward(sc.init, ctx, real, stage="fine")
+        q.put((rank, raised, ops, L))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(600)
+def test_error_on_one_rank_is_raised_on_every_rank():
+    ctx_mp = mp.get_context("spawn")
+    q = ctx_mp.Queue()
+    port = _free_port()
+    procs = [ctx_mp.Process(target=_coincident_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((r, (raised, ops, L)) for r, raised, ops, L in (q.get(timeout=500) for _ in range(2)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    P, sc, ctx = _instance()
+    real = P.simulate_signals(sc.truth, ctx)
+    P.reset_op_count()
+    L, _ = P.backward(sc.init, ctx, real, stage="fine")
+    for r in (0, 1):
+        raised, ops, Lr = res[r]
+        assert raised == [True, True]
+        assert ops == P.op_count()          # the global op count on every rank
+        assert abs(Lr - L) <= 1e-9 * L

