@@ -701,7 +701,7 @@ def main():
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": sampler.summary(),
             "gpu_launches": int(launches),
             "gpu_launches_note": "library kernels issued inside the timed region (counted by _lib.call): per step "
-                                 "pack x2 (forward and adjoint packings), forward, residual, adjoint, finalize, "
+                                 "pack x2 (forward and adjoint packings), coincidence test, forward, residual, adjoint, finalize, "
                                  "pass tail",
             "kernel_ms_min_median": {"forward+residual": [min(fwd_ms), statistics.median(fwd_ms)],
                                      "adjoint+finalize": [min(adj_ms), statistics.median(adj_ms)]}}

@@ -58,6 +58,13 @@ int pab_morton_keys(const double* pos /*[n][3]*/, const double* a0, int64_t n, d
 int pab_pack(const double* pos, const double* p0, const double* a0, const int32_t* perm, int64_t n,
              void* rec_a, void* rec_b, void* group_meta, void* stream);
 
+/* Exact FP64 ball-on-sensor test of a packed cloud: sets kStatusCoincident
+ * (2) in *status when any ball of `pos` (caller order, [n][3]) lies within
+ * 1e-12 of a detector (bounding-box prefilter per lane group).
+ * Replaces: the distance check of radiator.py:189-193. */
+int pab_coincident(const void* rec_b, const void* group_meta, int64_t n_groups, const double* pos,
+                   const double* det_pos, int n_det, int* status, void* stream);
+
 /* Dual-walk pairing table of a packed cloud (performance only): for each pair
  * of consecutive lane groups and each of 64 fixed directions, the 64 balls in
  * projection order, laid out [cell][unit][64] (pab_pair_table_bytes(n_groups)

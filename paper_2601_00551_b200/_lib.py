@@ -30,6 +30,7 @@ _SIGS = {
     "pab_adjoint": ([_vp, _vp, _vp, _i64, _vp, _vp, _i, _d, _d, _d, _i, _i, _d, _i, _d, _vp, _f, _i, _i, _i,
                      _vp, _vp, _vp, _vp], _i),
     "pab_grad_finalize": ([_vp, _i, _i64, _vp, _d, _i, _vp, _vp, _vp, _vp, _vp], _i),
+    "pab_coincident": ([_vp, _vp, _i64, _vp, _vp, _i, _vp, _vp], _i),
     "pab_pass_tail": ([_vp, _i, _vp, _vp, _vp, _vp], _i),
     "pab_decimate": ([_vp, _i, _i, _i, _vp, _vp], _i),
     "pab_adam": ([_vp, _vp, _vp, _vp, _i64, _d, _d, _d, _d, _i, _vp], _i),

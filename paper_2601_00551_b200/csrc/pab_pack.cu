@@ -202,6 +202,46 @@ __global__ void pair_table_kernel(const BallA* __restrict__ ra, const GroupMeta*
   }
 }
 
+// Exact coincidence test (reference radiator.py:189-193: SimulationError when
+// a ball lies within 1e-12 of a sensor), in FP64 on the caller-order master
+// positions: one warp per lane group tests every detector against the
+// group's bounding box (+1e-9 margin), and only a detector inside the box is
+// compared with the group's 32 balls.  The kernels' FP32 offsets from the
+// group centre cannot resolve 1e-12 for a ball far from its centre, so the
+// flag comes from here.  Cost: n_groups x n_det box tests per pass.
+__global__ void coincident_kernel(const BallB* __restrict__ rb, const GroupMeta* __restrict__ gm, int64_t n_groups,
+                                  const double* __restrict__ pos, const double* __restrict__ det, int n_det,
+                                  int* __restrict__ status) {
+  const int lane = threadIdx.x & 31;
+  const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (g >= n_groups) return;
+  const GroupMeta m = gm[g];
+  const int orig = rb[g * kWarp + lane].orig;
+  double bx = 0, by = 0, bz = 0;
+  if (orig >= 0) { bx = pos[3 * (int64_t)orig]; by = pos[3 * (int64_t)orig + 1]; bz = pos[3 * (int64_t)orig + 2]; }
+  bool hit = false;
+  for (int j0 = 0; j0 < n_det; j0 += kWarp) {
+    const int j = j0 + lane;
+    bool in = false;
+    double px = 0, py = 0, pz = 0;
+    if (j < n_det) {
+      px = det[3 * j]; py = det[3 * j + 1]; pz = det[3 * j + 2];
+      in = fabs(px - m.cx) <= (double)m.hx + 1e-9 && fabs(py - m.cy) <= (double)m.hy + 1e-9 &&
+           fabs(pz - m.cz) <= (double)m.hz + 1e-9;
+    }
+    unsigned cand = __ballot_sync(0xffffffffu, in);
+    while (cand) {   // rare: a detector inside the group's box
+      const int src = __ffs(cand) - 1;
+      cand &= cand - 1;
+      const double qx = __shfl_sync(0xffffffffu, px, src), qy = __shfl_sync(0xffffffffu, py, src),
+                   qz = __shfl_sync(0xffffffffu, pz, src);
+      const double dx = bx - qx, dy = by - qy, dz = bz - qz;
+      hit |= orig >= 0 && sqrt(dx * dx + dy * dy + dz * dz) < 1e-12;
+    }
+  }
+  if (__any_sync(0xffffffffu, hit) && lane == 0) atomicOr(status, kStatusCoincident);
+}
+
 }  // namespace pab
 
 using namespace pab;
@@ -249,6 +289,16 @@ int pab_record_sizes(int* ball_a, int* ball_b, int* group_meta) {
   *ball_b = (int)sizeof(BallB);
   *group_meta = (int)sizeof(GroupMeta);
   return 0;
+}
+
+int pab_coincident(const void* rec_b, const void* group_meta, int64_t n_groups, const double* pos,
+                   const double* det_pos, int n_det, int* status, void* stream) {
+  if (n_groups <= 0 || n_det <= 0) return 0;
+  if (!rec_b || !group_meta || !pos || !det_pos || !status) return 1;
+  const int warps = 8;
+  coincident_kernel<<<(unsigned)((n_groups + warps - 1) / warps), warps * kWarp, 0, (cudaStream_t)stream>>>(
+      (const BallB*)rec_b, (const GroupMeta*)group_meta, n_groups, pos, det_pos, n_det, status);
+  return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 
 }  // extern "C"

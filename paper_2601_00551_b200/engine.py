@@ -385,6 +385,14 @@ def _mark(name: str, i: int) -> None:
         TIMING[name][i].record(torch.cuda.current_stream())
 
 
+def check_coincident(cloud: DeviceCloud, det: DeviceDetectors, counters: PassCounters) -> None:
+    """Exact FP64 ball-on-sensor test (reference radiator.py:189-193) into
+    the pass's status word."""
+    if cloud.n_groups and det.n_local:
+        call("pab_coincident", ptr(cloud.rec_b), ptr(cloud.gmeta), cloud.n_groups, ptr(cloud.pos), ptr(det.pos),
+             det.n_local, ptr(counters.status), _stream())
+
+
 def forward_rows(cloud: DeviceCloud, det: DeviceDetectors, acq: Acq, counters: PassCounters,
                  real_local: torch.Tensor | None = None, out: torch.Tensor | None = None,
                  real_ready: torch.cuda.Event | None = None):
@@ -401,6 +409,7 @@ def forward_rows(cloud: DeviceCloud, det: DeviceDetectors, acq: Acq, counters: P
     if J == 0:
         return out, (torch.zeros(0, dtype=torch.float64, device=cloud.dev) if real_local is not None else None)
     cloud.pack()
+    check_coincident(cloud, det, counters)
     plan = plan_forward(cloud, det, acq)
     partial = ws.get("partial_rows", plan.partitions * J * n_out, torch.float32)
     loss_rows = ws.get("loss_rows", J, torch.float64) if real_local is not None else None
@@ -448,6 +457,8 @@ def adjoint_grads(cloud: DeviceCloud, det: DeviceDetectors, acq: Acq, res: torch
     if n > 0 and det.n_local > 0:
         cloud = cloud.adjoint_cloud()   # the adjoint's own packing (radius buckets)
         cloud.pack()
+        if stage == 0:   # the filter pass runs no forward
+            check_coincident(cloud, det, counters)
         chunks = plan_adjoint(cloud, det)
         ws = workspace(dev)
         npad = cloud.n_groups * GROUP

@@ -78,3 +78,20 @@ def test_in_place_edit_of_detector_positions_and_normals(P):
                                       sc.array.normals, 1500.0, 0.0, sc.grid.dt, sc.grid.n_samples, 1,
                                       kind=("cos_power", 2.0))
     assert rel_l2(rows, want_rows) < 1e-4
+
+
+def test_ball_exactly_on_a_sensor_far_from_its_group_centre(P):
+    """The coincidence test is exact in FP64 (reference radiator.py:189-193)
+    even when the ball sits far from its lane group's centre, where the
+    kernels' FP32 offsets cannot resolve 1e-12."""
+    sc, ctx = _instance(P)
+    real = P.simulate_signals(sc.truth, ctx)
+    bad = sc.init.copy()
+    bad.positions[1234] = sc.array.positions[7]
+    for call in (lambda: P.simulate_signals(bad, ctx), lambda: P.backward(bad, ctx, real, stage="fine"),
+                 lambda: P.zero_gradient_filter(bad, ctx, real, f=2)):
+        with pytest.raises(P.SimulationError):
+            call()
+    near = sc.init.copy()
+    near.positions[1234] = sc.array.positions[7] + np.array([1e-9, 0.0, 0.0])   # reference: no error
+    P.simulate_signals(near, ctx)
