@@ -533,8 +533,11 @@ class IterationTrace:
 
 
 def _filter_state_(state: OptimState, det, acq, real_local, strict: bool = True) -> None:
-    """Builder-defined periodic filter (config 3): reference predicate on the
-    current cloud at the current factor; survivors keep params and moments."""
+    """Builder-defined periodic filter (config 3): reference predicate
+    (optimizer.py:230-258) on the current cloud at the current factor;
+    survivors keep their parameters, Adam moments and last gradients.
+    Reference equivalent: the ``callback`` of run_hierarchical filtering
+    ``state`` in place (tests/golden/make_golden_config3.py)."""
     dc = state._dc
     probe = E.DeviceCloud(dc.pos, torch.zeros_like(dc.p0), dc.a0)
     probe.perm = dc.perm
@@ -556,7 +559,11 @@ def _filter_state_(state: OptimState, det, acq, real_local, strict: bool = True)
         d["position"] = ws_gather(d["position"], 3).view(m, 3)
     state._free = ws_gather(state._free, 1)
     state._host_cache = None
-    state._last = None
+    last = state._last   # survivors keep their last gradients: a density-control step right after the
+    #                      filter still ranks duplicates by |grad position|
+    if last is not None:
+        state._last = _DeviceGrads(ws_gather(last.d_p0_t, 1), ws_gather(last.d_a0_t, 1),
+                                   ws_gather(last.d_pos_t, 3).view(m, 3))
 
 
 def _gather(src: torch.Tensor, width: int, idx: torch.Tensor) -> torch.Tensor:

@@ -95,3 +95,32 @@ def test_ball_exactly_on_a_sensor_far_from_its_group_centre(P):
     near = sc.init.copy()
     near.positions[1234] = sc.array.positions[7] + np.array([1e-9, 0.0, 0.0])   # reference: no error
     P.simulate_signals(near, ctx)
+
+
+def test_adjoint_on_an_unaligned_residual_view(P):
+    """pab_adjoint stages 16-byte vectors only from a 16-byte aligned
+    residual; an offset view (a row slice of a larger buffer) takes the
+    4-byte path and gives the same gradients up to the few overrun samples
+    past a window end (finite residual in one staging, zero padding in the
+    other; their Gaussian weights are below 2^-24)."""
+    import torch
+
+    from paper_2601_00551_b200 import engine as E
+    from paper_2601_00551_b200 import radiator as R
+    sc, ctx = _instance(P)
+    det = R.device_detectors(ctx)
+    acq = R._acq(ctx, 1)
+    dev = det.pos.device
+    cloud = E.DeviceCloud.from_host(sc.init.positions, sc.init.p0, sc.init.a0, dev)
+    real = R.device_supervision(P.simulate_signals(sc.truth, ctx).data, det)
+    c = E.PassCounters(dev)
+    res, _ = E.forward_rows(cloud, det, acq, c, real_local=real)
+    buf = torch.empty(res.numel() + 1, dtype=torch.float32, device=dev)
+    buf[1:].copy_(res.reshape(-1))
+    shifted = buf[1:].view(res.shape)
+    assert shifted.data_ptr() % 16 != 0
+    n_total = det.n_total * acq.n_out
+    a = [t.clone() for t in E.adjoint_grads(cloud, det, acq, res, 1.0, 2, 2.0 / n_total, E.PassCounters(dev))]
+    b = E.adjoint_grads(cloud, det, acq, shifted, 1.0, 2, 2.0 / n_total, E.PassCounters(dev))
+    for x, y in zip(a, b):
+        assert rel_l2(x.cpu().numpy(), y.cpu().numpy()) < 1e-6

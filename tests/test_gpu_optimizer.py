@@ -219,9 +219,10 @@ class TestRunHierarchical:
         counts = np.array([r.ball_count for r in trace.records])
         losses = np.array([r.loss for r in trace.records])
         assert np.array_equal(counts, g["counts"])
-        assert np.allclose(losses, g["losses"], rtol=1e-2)
+        # measured on B200: losses within 1.1e-5, volume rel L2 8.8e-7 (north star: 1e-3)
+        assert np.allclose(losses, g["losses"], rtol=1e-4)
         vol = ORend.voxelize(final.positions, final.p0, final.a0, (31, 31, 31), 2e-4, (-3e-3,) * 3)
-        assert rel_l2(vol, g["volume"]) < 1e-3
+        assert rel_l2(vol, g["volume"]) < 1e-5
 
 
 def test_toy_five_adam_steps_match_reference(P):
@@ -238,11 +239,13 @@ def test_toy_five_adam_steps_match_reference(P):
     for _ in range(5):
         state, L = P.step(state, ctx, real, 1, "fine")
         losses.append(L)
-    assert np.allclose(losses, g["step_losses"], rtol=1e-4)
+    # measured on B200: losses 1.0e-7, displacements 2.7e-6, p0 1.6e-7, a0 1.9e-6 (rel)
+    assert np.allclose(losses, g["step_losses"], rtol=1e-6)
     c = state.cloud
     init = sc.init.subset(keep)
-    assert rel_l2(c.positions - init.positions, g["final_pos"] - init.positions) < 1e-2
-    assert rel_l2(c.p0, g["final_p0"]) < 1e-4
+    assert rel_l2(c.positions - init.positions, g["final_pos"] - init.positions) < 3e-5
+    assert rel_l2(c.p0, g["final_p0"]) < 2e-6
+    assert rel_l2(c.a0, g["final_a0"]) < 2e-5
 
 
 class TestPositivityRefine:
