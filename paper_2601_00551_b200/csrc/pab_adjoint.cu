@@ -142,9 +142,6 @@ struct WalkConst {
   float2 nsc2;
   float dl, dl2;   // f * (-sc), 2 f * (-sc)
   float step8;     // 8 f (m advance per block)
-#ifdef PAB_ADJ_REC
-  float2 kr2, br2, cc2;   // ratio recurrence: R0 = 2^(kr y0 + br), R <- R * cc per sample pair
-#endif
 };
 
 __device__ __forceinline__ WalkConst walk_const(float sc, int f) {
@@ -154,12 +151,6 @@ __device__ __forceinline__ WalkConst walk_const(float sc, int f) {
   w.dl = fs * nsc;
   w.dl2 = 2.0f * fs * nsc;
   w.step8 = 8.0f * fs;
-#ifdef PAB_ADJ_REC
-  w.kr2 = make_float2(-4.0f * w.dl, -4.0f * w.dl);
-  w.br2 = make_float2(-4.0f * w.dl * w.dl, -4.0f * w.dl * w.dl);
-  const float c = ex2(-8.0f * w.dl * w.dl);
-  w.cc2 = make_float2(c, c);
-#endif
   return w;
 }
 
@@ -179,52 +170,9 @@ __device__ __forceinline__ void moment_block8(const float4* s4, float mf, const 
                                                         A0, A1, A2, A3);
 }
 
-#ifdef PAB_ADJ_REC
-// Ratio recurrence (as the forward's dual walk): pair 0 of the block and its
-// step ratio R exactly (4 ex2), pairs 1-3 by G <- G R, R <- R C (FMUL2); no
-// state crosses blocks.  Used when every lane's |dl| <= kRecMaxDl (pair-0
-// underflow then only loses terms beyond cutoff sigmas) and the walked |y|
-// stays small enough that R < 2^127 (cutoff <= 12, host-checked).
-constexpr float kRecMaxDl = 0.75f;
-template <int STAGE>
-__device__ __forceinline__ void moment_pair_g(float2 res, float2 y, float2 G, float2& A0, float2& A1, float2& A2,
-                                              float2& A3) {
-  const float2 r = __fmul2_rn(res, G);
-  const float2 t = __fmul2_rn(r, y);
-  A1 = __fadd2_rn(A1, t);
-  if (STAGE >= kStageCoarse) A3 = __ffma2_rn(t, __fmul2_rn(y, y), A3);
-  if (STAGE == kStageFine) {
-    A0 = __fadd2_rn(A0, r);
-    A2 = __ffma2_rn(t, y, A2);
-  }
-}
-template <int STAGE>
-__device__ __forceinline__ void moment_block8_rec(const float4* s4, float mf, const WalkConst& W, float2 c0,
-                                                  float2 c1, float2 c2, float2 c3, float2& A0, float2& A1,
-                                                  float2& A2, float2& A3) {
-  const float4 ra = s4[0], rb = s4[1];
-  const float2 m2 = make_float2(mf, mf);
-  const float2 y0 = __ffma2_rn(m2, W.nsc2, c0), y1 = __ffma2_rn(m2, W.nsc2, c1);
-  const float2 y2 = __ffma2_rn(m2, W.nsc2, c2), y3 = __ffma2_rn(m2, W.nsc2, c3);
-  const float2 q0 = __fmul2_rn(y0, y0);
-  const float2 er = __ffma2_rn(y0, W.kr2, W.br2);
-  const float2 g0 = make_float2(ex2(-q0.x), ex2(-q0.y));
-  const float2 r0 = make_float2(ex2(er.x), ex2(er.y));
-  const float2 g1 = __fmul2_rn(g0, r0);
-  const float2 r1 = __fmul2_rn(r0, W.cc2);
-  const float2 g2 = __fmul2_rn(g1, r1);
-  const float2 r2 = __fmul2_rn(r1, W.cc2);
-  const float2 g3 = __fmul2_rn(g2, r2);
-  moment_pair_g<STAGE>(make_float2(ra.x, ra.y), y0, g0, A0, A1, A2, A3);
-  moment_pair_g<STAGE>(make_float2(ra.z, ra.w), y1, g1, A0, A1, A2, A3);
-  moment_pair_g<STAGE>(make_float2(rb.x, rb.y), y2, g2, A0, A1, A2, A3);
-  moment_pair_g<STAGE>(make_float2(rb.z, rb.w), y3, g3, A0, A1, A2, A3);
-}
-#endif
-
 template <int STAGE, bool MASK>
 __device__ __forceinline__ void moments_uniform(const float* seg, int L, float mf, const WalkConst& W, float ps,
-                                                float qmax, Moments& M, bool rec = false) {
+                                                float qmax, Moments& M) {
   const float4* s4 = reinterpret_cast<const float4*>(seg);
   float2 A0 = make_float2(0.f, 0.f), A1 = A0, A2 = A0, A3 = A0;
   const float2 c0 = make_float2(ps, ps + W.dl);
@@ -232,15 +180,6 @@ __device__ __forceinline__ void moments_uniform(const float* seg, int L, float m
   const float2 c2 = __fadd2_rn(c1, make_float2(W.dl2, W.dl2));
   const float2 c3 = __fadd2_rn(c2, make_float2(W.dl2, W.dl2));
   int nb = L >> 3;
-#ifdef PAB_ADJ_REC
-  if (!MASK && rec) {
-#pragma unroll 1
-    for (; nb >= 2; nb -= 2, s4 += 4, mf += 2.0f * W.step8) {
-      moment_block8_rec<STAGE>(s4, mf, W, c0, c1, c2, c3, A0, A1, A2, A3);
-      moment_block8_rec<STAGE>(s4 + 2, mf + W.step8, W, c0, c1, c2, c3, A0, A1, A2, A3);
-    }
-  }
-#endif
 #pragma unroll 1
   for (; nb >= 2; nb -= 2, s4 += 4, mf += 2.0f * W.step8) {   // two blocks per trip
     moment_block8<STAGE, MASK>(s4, mf, W, c0, c1, c2, c3, qmax, A0, A1, A2, A3);
@@ -285,40 +224,6 @@ __device__ unsigned long long g_adj_prof[16];
 #define APROF_T(v)
 #define APROF_ACC(i, t0)
 #endif
-
-__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
-
-// Two detectors' pair geometry side by side (A in .x, B in .y): the same
-// operations, in the same order, as pair_geom_fast, on FP32x2 pairs.
-struct PairGeom2 {
-  float2 phi, id, rx, ry, rz;
-  int kcA, kcB;
-};
-__device__ __forceinline__ PairGeom2 pair_geom_fast2(const GroupDet& ga, const GroupDet& gb, float2 dx2, float2 dy2,
-                                                     float2 dz2, float2 r2, const Acq& a) {
-  PairGeom2 g;
-  const float2 isn = f2(ga.isn, gb.isn);
-  float2 sd = __fmul2_rn(f2(ga.Sx, gb.Sx), dx2);
-  sd = __ffma2_rn(f2(ga.Sy, gb.Sy), dy2, sd);
-  sd = __ffma2_rn(f2(ga.Sz, gb.Sz), dz2, sd);
-  const float2 num = __ffma2_rn(sd, f2(-2.0f, -2.0f), r2);
-  const float2 ni = __fmul2_rn(num, isn);
-  const float2 e1 = __ffma2_rn(ni, isn, f2(1.0f, 1.0f));
-  const float2 den = __ffma2_rn(e1, f2(rsqrt_ftz(e1.x), rsqrt_ftz(e1.y)), f2(1.0f, 1.0f));
-  const float2 dd = __fmul2_rn(ni, f2(rcp_ftz(den.x), rcp_ftz(den.y)));
-  const float2 d = __fadd2_rn(f2(ga.Sn, gb.Sn), dd);
-  const float2 tr = __ffma2_rn(dd, f2(a.inv_vdt_f, a.inv_vdt_f), f2(ga.phg, gb.phg));
-  const float krA = rintf(tr.x), krB = rintf(tr.y);
-  g.kcA = ga.kg + (int)krA;
-  g.kcB = gb.kg + (int)krB;
-  g.phi = __fadd2_rn(tr, f2(-krA, -krB));
-  g.id = f2(rcp_ftz(d.x), rcp_ftz(d.y));
-  g.rx = __ffma2_rn(f2(ga.Sx, gb.Sx), f2(-1.0f, -1.0f), dx2);
-  g.ry = __ffma2_rn(f2(ga.Sy, gb.Sy), f2(-1.0f, -1.0f), dy2);
-  g.rz = __ffma2_rn(f2(ga.Sz, gb.Sz), f2(-1.0f, -1.0f), dz2);
-  return g;
-}
-
 template <int STAGE, int DIR, bool MASK>
 __global__ void __launch_bounds__(kAdjWarps * 32, PAB_ADJ_MINB)
 adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
@@ -350,11 +255,6 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   const bool live = B.orig >= 0;
   const float qmax = live ? (rho * sc) * (rho * sc) : -1.0f;
   const WalkConst W = walk_const(sc, f);
-#ifdef PAB_ADJ_REC
-  const bool rec = __all_sync(0xffffffffu, fabsf(W.dl) <= kRecMaxDl) && acq.cutoff <= 12.0f;
-#else
-  const bool rec = false;
-#endif
   const float kap_rs = A.a0 * kSqrt2Ln2 * res_sign;   // kappa * sign
   const float p0h = 0.5f * B.p0;
   // the uniform walk must stay inside the staged samples + zero padding
@@ -415,18 +315,12 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
     auto wait_seg = [&](int fl) {
       if (fl & kFlagUniform) cp_async_wait_all();
     };
-#ifdef PAB_ADJ_PACK2
-    float2 gb2[5] = {f2(0.f, 0.f), f2(0.f, 0.f), f2(0.f, 0.f), f2(0.f, 0.f), f2(0.f, 0.f)};   // detector A | B
-#define GB(c) gb2[c].x
-#else
     float gb[5] = {0.f, 0.f, 0.f, 0.f, 0.f};   // FP32 batch sums of the pair terms
-#define GB(c) gb[c]
-#endif
 
     // per-pair gradient terms (reference radiator.py:275-286 in y units)
     auto epilogue = [&](const PairGeom& pg, const Moments& M, const DetDir& dd) {
 #ifdef PAB_ADJ_NOEPI   // tuning builds only: no gradient epilogue (wrong gradients)
-      GB(0) += M.T0 + M.T1 + M.T2 + M.T3 + pg.id + pg.rx;
+      gb[0] += M.T0 + M.T1 + M.T2 + M.T3 + pg.id + pg.rx;
       return;
 #endif
       float dDdr[3] = {0.f, 0.f, 0.f}, dDda0 = 0.f;
@@ -435,11 +329,11 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
           dd, pg.rx * id, pg.ry * id, pg.rz * id, id, acq.dir_param, acq.dir_param, B.inv_a0, dDdr, &dDda0);
       const float base = p0h * id;   // p0 / 2d
       const float s_uG = kap_rs * M.T1;
-      GB(0) = fmaf(D * s_uG, 0.5f * id, GB(0));
+      gb[0] = fmaf(D * s_uG, 0.5f * id, gb[0]);
       if (STAGE >= kStageCoarse) {
         float ga = (base * D) * (kSqrt2Ln2Cubed * res_sign) * M.T3;
         if (DIR == kDirElement) ga = fmaf(base * dDda0, s_uG, ga);
-        GB(1) += ga;
+        gb[1] += ga;
       }
       if (STAGE == kStageFine) {
         const float w = (base * D) * fmaf(res_sign, fmaf(-kTwoLn2, M.T2, M.T0), -id * s_uG) * id;
@@ -450,9 +344,9 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
           gy = fmaf(bs, dDdr[1], gy);
           gz = fmaf(bs, dDdr[2], gz);
         }
-        GB(2) += gx;
-        GB(3) += gy;
-        GB(4) += gz;
+        gb[2] += gx;
+        gb[3] += gy;
+        gb[4] += gz;
       }
     };
     // uniform path, part 1: geometry, covering window, block count
@@ -485,7 +379,7 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       return M;
 #endif
       moments_uniform<STAGE, MASK>(seg_all[warp][buf] + (u.J0 - lo), (u.L + 3) & ~3, (float)(u.J0 * f - u.pg.kc),
-                                   W, u.pg.phi * sc, u.empty ? -1.0f : qmax, M, rec);
+                                   W, u.pg.phi * sc, u.empty ? -1.0f : qmax, M);
       if (!MASK && u.empty) M = {0.f, 0.f, 0.f, 0.f};
       return M;
     };
@@ -536,94 +430,6 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       epilogue(pg, M, dd);
     };
 
-#ifdef PAB_ADJ_PACK2
-    // detectors A and B of a pair side by side in FP32x2 (A in .x, B in .y):
-    // half the FMA-pipe instructions of two scalar setups / epilogues
-    struct USetup2 {
-      PairGeom2 pg;
-      int J0A, J0B, LA, LB;
-      bool eA, eB;
-    };
-    auto usetup2 = [&](const GroupDet& ga, const GroupDet& gb_, int loA_, int loB_) {
-      USetup2 u;
-      u.pg = pair_geom_fast2(ga, gb_, f2(A.dx, A.dx), f2(A.dy, A.dy), f2(A.dz, A.dz), f2(B.r2, B.r2), acq);
-      const float2 kf = f2((float)u.pg.kcA, (float)u.pg.kcB);
-      const float2 lo = __fmul2_rn(__fadd2_rn(kf, __fadd2_rn(u.pg.phi, f2(-rho, -rho))), f2(acq.inv_f, acq.inv_f));
-      const float2 hi = __fmul2_rn(__fadd2_rn(kf, __fadd2_rn(u.pg.phi, f2(rho, rho))), f2(acq.inv_f, acq.inv_f));
-      const int jloA = max(__float2int_rd(lo.x), 0), jhiA = min(__float2int_ru(hi.x), acq.n_out - 1);
-      const int jloB = max(__float2int_rd(lo.y), 0), jhiB = min(__float2int_ru(hi.y), acq.n_out - 1);
-      u.eA = !live || jloA > jhiA;
-      u.eB = !live || jloB > jhiB;
-      u.J0A = u.eA ? loA_ : max(jloA & ~3, loA_);
-      u.J0B = u.eB ? loB_ : max(jloB & ~3, loB_);
-      u.LA = __reduce_max_sync(0xffffffffu, u.eA ? 0 : jhiA - u.J0A + 1);
-      u.LB = __reduce_max_sync(0xffffffffu, u.eB ? 0 : jhiB - u.J0B + 1);
-      if (ops_total && live) {   // exact sample counts for the op counter
-        int elo, ehi;
-        pair_window<true>(u.pg.kcA, u.pg.phi.x, rho, acq, &elo, &ehi);
-        my_ops += (unsigned long long)max(ehi - elo + 1, 0);
-        pair_window<true>(u.pg.kcB, u.pg.phi.y, rho, acq, &elo, &ehi);
-        my_ops += (unsigned long long)max(ehi - elo + 1, 0);
-      }
-      return u;
-    };
-    auto uwalk2 = [&](int J0, int L, int kc, float phi, bool empty, int lo, int buf) {
-      Moments M;
-      PAB_CHECK(J0 - lo >= 0 && J0 - lo + ((L + 3) & ~3) <= kSeg + kPad);
-      moments_uniform<STAGE, MASK>(seg_all[warp][buf] + (J0 - lo), (L + 3) & ~3, (float)(J0 * f - kc), W,
-                                   phi * sc, empty ? -1.0f : qmax, M, rec);
-      if (!MASK && empty) M = {0.f, 0.f, 0.f, 0.f};
-      return M;
-    };
-    // packed epilogue (no directivity / cos^2); other directivities: two scalar epilogues
-    auto epilogue2 = [&](const USetup2& u, const Moments& MA, const Moments& MB, const DetDir& da, const DetDir& db) {
-      const PairGeom2& pg = u.pg;
-      const float2 id = pg.id;
-      const float2 T0 = f2(MA.T0, MB.T0), T1 = f2(MA.T1, MB.T1), T2 = f2(MA.T2, MB.T2), T3 = f2(MA.T3, MB.T3);
-      float2 D = f2(1.0f, 1.0f), dr_x = f2(0.f, 0.f), dr_y = dr_x, dr_z = dr_x;
-      if constexpr (DIR == kDirCos2) {
-        const float2 hx = __fmul2_rn(pg.rx, id), hy = __fmul2_rn(pg.ry, id), hz = __fmul2_rn(pg.rz, id);
-        const float2 fx = f2(da.fx, db.fx), fy = f2(da.fy, db.fy), fz = f2(da.fz, db.fz);
-        float2 c = __fmul2_rn(fx, hx);
-        c = __ffma2_rn(fy, hy, c);
-        c = __ffma2_rn(fz, hz, c);
-        const float2 cp = f2(fmaxf(c.x, 0.0f), fmaxf(c.y, 0.0f));
-        D = __fmul2_rn(cp, cp);
-        if (STAGE == kStageFine) {
-          const float2 sdd = __fmul2_rn(__fadd2_rn(cp, cp), id);   // dD/dc / d
-          const float2 nc = f2(-c.x, -c.y);
-          dr_x = __fmul2_rn(sdd, __ffma2_rn(nc, hx, fx));
-          dr_y = __fmul2_rn(sdd, __ffma2_rn(nc, hy, fy));
-          dr_z = __fmul2_rn(sdd, __ffma2_rn(nc, hz, fz));
-        }
-      }
-      const float2 base = __fmul2_rn(f2(p0h, p0h), id);
-      const float2 s_uG = __fmul2_rn(f2(kap_rs, kap_rs), T1);
-      gb2[0] = __ffma2_rn(__fmul2_rn(D, s_uG), __fmul2_rn(f2(0.5f, 0.5f), id), gb2[0]);
-      const float2 bD = __fmul2_rn(base, D);
-      if (STAGE >= kStageCoarse) {
-        const float k3 = kSqrt2Ln2Cubed * res_sign;
-        gb2[1] = __ffma2_rn(__fmul2_rn(bD, f2(k3, k3)), T3, gb2[1]);
-      }
-      if (STAGE == kStageFine) {
-        const float2 inner = __ffma2_rn(f2(res_sign, res_sign), __ffma2_rn(f2(-kTwoLn2, -kTwoLn2), T2, T0),
-                                        __fmul2_rn(f2(-id.x, -id.y), s_uG));
-        const float2 w = __fmul2_rn(__fmul2_rn(bD, inner), id);
-        float2 gx = __fmul2_rn(w, pg.rx), gy = __fmul2_rn(w, pg.ry), gz = __fmul2_rn(w, pg.rz);
-        if constexpr (DIR == kDirCos2) {
-          const float2 bs = __fmul2_rn(base, s_uG);
-          gx = __ffma2_rn(bs, dr_x, gx);
-          gy = __ffma2_rn(bs, dr_y, gy);
-          gz = __ffma2_rn(bs, dr_z, gz);
-        }
-        gb2[2] = __fadd2_rn(gb2[2], gx);
-        gb2[3] = __fadd2_rn(gb2[3], gy);
-        gb2[4] = __fadd2_rn(gb2[4], gz);
-      }
-    };
-    constexpr bool kPackEpi = DIR == kDirNone || DIR == kDirCos2;
-#endif
-
     // detectors in pairs, four staging buffers per warp: while a pair is
     // processed the next pair's segments are in flight; the two pairs'
     // setups (latency-bound chains) and gradient epilogues are computed side
@@ -662,23 +468,6 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       }
       const bool uA = (fa & kFlagUniform) && la <= ha, uB = two && (fb & kFlagUniform) && lb <= hb;
       APROF_ACC(2, t_st);
-#ifdef PAB_ADJ_PACK2
-      if (uA && uB) {
-        const USetup2 u2 = usetup2(gdA, gdB, la, lb);
-        const Moments MA = uwalk2(u2.J0A, u2.LA, u2.pg.kcA, u2.pg.phi.x, u2.eA, la, bA);
-        const Moments MB = uwalk2(u2.J0B, u2.LB, u2.pg.kcB, u2.pg.phi.y, u2.eB, lb, bB);
-        __syncwarp();
-        if constexpr (kPackEpi) {
-          epilogue2(u2, MA, MB, ddA, ddB);
-        } else {
-          PairGeom pa, pb;
-          pa.id = u2.pg.id.x; pa.rx = u2.pg.rx.x; pa.ry = u2.pg.ry.x; pa.rz = u2.pg.rz.x;
-          pb.id = u2.pg.id.y; pb.rx = u2.pg.rx.y; pb.ry = u2.pg.ry.y; pb.rz = u2.pg.rz.y;
-          epilogue(pa, MA, ddA);
-          epilogue(pb, MB, ddB);
-        }
-      } else
-#endif
       if (uA && uB) {
         APROF_T(t_s);
         const USetup sA = usetup(gdA, la);
@@ -707,14 +496,8 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       }
     }
     __syncwarp();
-#ifdef PAB_ADJ_PACK2
-#pragma unroll
-    for (int c = 0; c < 5; ++c) acc_s[warp][c][lane] += (double)(gb2[c].x + gb2[c].y);
-#else
 #pragma unroll
     for (int c = 0; c < 5; ++c) acc_s[warp][c][lane] += (double)gb[c];
-#endif
-#undef GB
   }
 #ifdef PAB_ADJ_PROF
   APROF_ACC(7, t_all);
