@@ -610,13 +610,14 @@ def main():
         pinned_ms = time_e2e(P.PointCloud(pin(scene.init.positions), pin(scene.init.p0), pin(scene.init.a0)),
                              P.SignalSet(scene.grid, pin(real_full)))
         n = args.n_balls
-        h2d = n * 5 * 8 + det.n_total * acq.n_out * 8
+        h2d = n * 5 * 8 + det.n_total * acq.n_out * 4   # FP64 cloud; supervision narrowed to FP32 while staged
         d2h = (5 * n + E.TAIL) * 8
         e2e = {"value": pairs / (pageable_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": pageable_ms,
                "path": "paper_2601_00551_b200.backward(PointCloud, ForwardContext, SignalSet, 'fine') with pageable "
-                       "host numpy inputs (as a reference caller holds them); cloud and supervision uploaded and "
-                       "loss + gradients downloaded every step",
+                       "host numpy inputs (as a reference caller holds them); cloud and supervision staged through "
+                       "page-locked buffers (threaded chunked copies, DMA per chunk; the supervision upload overlaps "
+                       "the forward kernel) and loss + gradients downloaded every step",
                "pinned": {"value": pairs / (pinned_ms * 1e-3), "ms_per_step": pinned_ms,
                           "path": "same call with page-locked host arrays"}}
 

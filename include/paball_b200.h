@@ -42,6 +42,37 @@ int pab_device_info(int device, int* sm_count, int* cc_major, int* cc_minor, int
 const char* pab_last_cuda_error(void);
 int pab_record_sizes(int* ball_a, int* ball_b, int* group_meta);
 
+/* ---- Host staging of the API edge (no GPU work) ----
+ * Copy `bytes` (resp. narrow n float64 to float32) from a pageable caller
+ * array into a 16-byte aligned page-locked staging buffer with non-temporal
+ * stores on `threads` threads, so the following upload DMA reads DRAM
+ * instead of snooping dirty cache lines.  Return 0, or 1 on a bad argument.
+ * Replaces: the implicit float64 reads of caller arrays (radiator.py:316-332). */
+int pab_host_stage_copy(void* dst, const void* src, size_t bytes, int threads);
+int pab_host_stage_narrow(float* dst, const double* src, size_t n, int threads);
+
+/* Bounds of a cloud on the device: bounds[0..2] = min x, y, z, bounds[3] =
+ * extent (largest side of the bounding box; 1 if degenerate), bounds[4..5] =
+ * min / max a0 (exact min/max: deterministic).  workspace:
+ * pab_cloud_bounds_workspace_bytes().  No host round trip. */
+size_t pab_cloud_bounds_workspace_bytes(void);
+int pab_cloud_bounds(const double* pos, const double* a0, int64_t n, double* bounds, void* workspace, void* stream);
+
+/* pab_morton_keys with the cube and a0 range read from device `bounds`
+ * (pab_cloud_bounds): the same keys, no host round trip. */
+int pab_sort_keys(const double* pos, const double* a0, int64_t n, const double* bounds, int a0_buckets,
+                  int64_t* keys, void* stream);
+
+/* Stable LSD radix sort (five 7-bit passes over key bits [28, 63); the low
+ * 28 bits are the input index, already ascending) of pab_sort_keys /
+ * pab_morton_keys keys; writes perm[k] = index of the k-th smallest key.
+ * `keys` is overwritten (ping-pong buffer).  workspace:
+ * pab_sort_perm_workspace_bytes(n).  n < 2^28.
+ * Replaces: nothing in the reference (it visits balls in input order); the
+ * order only fixes the deterministic FP32 summation order. */
+size_t pab_sort_perm_workspace_bytes(int64_t n);
+int pab_sort_perm(int64_t* keys, int64_t n, int32_t* perm, void* workspace, void* stream);
+
 /* Processing-order sort keys: key[i] = a0_bucket << 58 | hilbert30(pos[i]) << 28 | i
  * (hilbert30: 10-bit-per-axis 3-D Hilbert index of the position in the cube
  * [lo, lo + extent)^3; a0 buckets: a0_buckets equal bins of [a0lo, a0hi]; n < 2^28).

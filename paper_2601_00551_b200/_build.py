@@ -11,8 +11,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libpaball_b200.so")
-SOURCES = ["pab_pack.cu", "pab_forward.cu", "pab_adjoint.cu", "pab_driver.cu", "pab_density.cu", "pab_render.cu",
-           "pab_ubp.cu"]
+SOURCES = ["pab_pack.cu", "pab_sort.cu", "pab_forward.cu", "pab_adjoint.cu", "pab_driver.cu", "pab_density.cu", "pab_render.cu",
+           "pab_ubp.cu", "pab_host.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -57,11 +57,9 @@ __device__ __forceinline__ uint32_t hilbert3(uint32_t x, uint32_t y, uint32_t z)
 // key = a0 bucket (4 bits) << 58 | hilbert30 << 28 | index (28 bits): balls
 // of similar radius share lane groups (equal window lengths: no divergence in
 // the per-lane window loops), spatially compact within a bucket.
-__global__ void morton_keys_kernel(const double* __restrict__ pos, const double* __restrict__ a0, int64_t n,
-                                   double lox, double loy, double loz, double inv_ext, double a0lo,
-                                   double inv_a0span, int nbuckets, int64_t* __restrict__ keys) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+__device__ __forceinline__ int64_t sort_key(const double* __restrict__ pos, const double* __restrict__ a0, int64_t i,
+                                            double lox, double loy, double loz, double inv_ext, double a0lo,
+                                            double inv_a0span, int nbuckets) {
   const double s = 1023.0 * inv_ext;
   const uint32_t qx = (uint32_t)fmin(fmax((pos[3 * i + 0] - lox) * s, 0.0), 1023.0);
   const uint32_t qy = (uint32_t)fmin(fmax((pos[3 * i + 1] - loy) * s, 0.0), 1023.0);
@@ -69,7 +67,27 @@ __global__ void morton_keys_kernel(const double* __restrict__ pos, const double*
   const uint64_t code = (uint64_t)hilbert3(qx, qy, qz);
   int b = 0;
   if (nbuckets > 1) b = (int)fmin(fmax((a0[i] - a0lo) * inv_a0span * nbuckets, 0.0), (double)(nbuckets - 1));
-  keys[i] = (int64_t)(((uint64_t)b << 58) | (code << 28) | ((uint64_t)i & 0xFFFFFFFull));
+  return (int64_t)(((uint64_t)b << 58) | (code << 28) | ((uint64_t)i & 0xFFFFFFFull));
+}
+
+__global__ void morton_keys_kernel(const double* __restrict__ pos, const double* __restrict__ a0, int64_t n,
+                                   double lox, double loy, double loz, double inv_ext, double a0lo,
+                                   double inv_a0span, int nbuckets, int64_t* __restrict__ keys) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  keys[i] = sort_key(pos, a0, i, lox, loy, loz, inv_ext, a0lo, inv_a0span, nbuckets);
+}
+
+// Same keys with the bounds read from device memory (pab_cloud_bounds): no
+// host round trip between the bounds and the keys.
+__global__ void sort_keys_dev_kernel(const double* __restrict__ pos, const double* __restrict__ a0, int64_t n,
+                                     const double* __restrict__ bounds, int nbuckets, int64_t* __restrict__ keys) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double a0lo = bounds[4], a0hi = bounds[5];
+  const int nb = (nbuckets > 1 && a0hi > a0lo) ? nbuckets : 1;
+  keys[i] = sort_key(pos, a0, i, bounds[0], bounds[1], bounds[2], 1.0 / bounds[3], a0lo,
+                     nb > 1 ? 1.0 / (a0hi - a0lo) : 0.0, nb);
 }
 
 __device__ __forceinline__ double warp_min(double v) {
@@ -257,6 +275,16 @@ int pab_morton_keys(const double* pos, const double* a0, int64_t n, double lox, 
   morton_keys_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0, (cudaStream_t)stream>>>(
       pos, a0, n, lox, loy, loz, 1.0 / extent, a0lo, a0_buckets > 1 ? 1.0 / (a0hi - a0lo) : 0.0, a0_buckets,
       keys);
+  return cudaGetLastError() == cudaSuccess ? 0 : 4;
+}
+
+int pab_sort_keys(const double* pos, const double* a0, int64_t n, const double* bounds, int a0_buckets,
+                  int64_t* keys, void* stream) {
+  if (n <= 0) return 0;
+  if (!pos || !a0 || !bounds || !keys || n > (1ll << 28) || a0_buckets < 1 || a0_buckets > 16) return 1;
+  const int threads = 256;
+  sort_keys_dev_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0, (cudaStream_t)stream>>>(
+      pos, a0, n, bounds, a0_buckets, keys);
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 

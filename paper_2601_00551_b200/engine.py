@@ -136,7 +136,6 @@ class DeviceCloud:
         self.buckets = A0_BUCKETS if buckets is None else buckets
         self.perm = None
         self._packed = False
-        self._stats = None
         self._adj = None
 
     def adjoint_cloud(self) -> "DeviceCloud":
@@ -152,8 +151,13 @@ class DeviceCloud:
 
     @classmethod
     def from_host(cls, positions, p0, a0, dev) -> "DeviceCloud":
-        t = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev, non_blocking=False)
-        return cls(t(np.asarray(positions).reshape(-1, 3)), t(p0), t(a0))
+        """Upload caller arrays (FP64 numpy) as one contiguous device buffer
+        through the page-locked staging slot (hostio: streaming-store host
+        copy overlapped with the DMA), on the current stream."""
+        from . import hostio
+        (pos_d, p0_d, a0_d), _ = hostio.stager("cloud").upload(
+            [(np.asarray(positions).reshape(-1, 3), torch.float64), (p0, torch.float64), (a0, torch.float64)], dev)
+        return cls(pos_d, p0_d, a0_d)
 
     @property
     def n(self) -> int:
@@ -166,30 +170,29 @@ class DeviceCloud:
     def invalidate(self, resort: bool = False) -> None:
         """Parameters changed: repack before the next pass (and resort)."""
         self._packed = False
-        self._stats = None
         if self._adj is not None:
             self._adj.invalidate(resort)
         if resort:
             self.perm = None
 
     def sort(self) -> None:
+        """Processing order on the device, no host round trip: cloud bounds,
+        (a0 bucket, Hilbert) keys, stable radix sort -> perm."""
         n = self.n
+        self._ptable_ok = False   # new units: rebuild the pairing table
         if n == 0:
             self.perm = torch.empty(0, dtype=torch.int32, device=self.dev)
-            self._ptable_ok = False
             return
-        lo = torch.amin(self.pos, dim=0)
-        hi = torch.amax(self.pos, dim=0)
-        ext = float(torch.max(hi - lo).item())
-        ext = ext if ext > 0.0 else 1.0
-        lo_h = lo.cpu().numpy()
-        a0lo, a0hi = (float(x) for x in torch.aminmax(self.a0))
-        keys = torch.empty(n, dtype=torch.int64, device=self.dev)
-        call("pab_morton_keys", ptr(self.pos), ptr(self.a0), n, float(lo_h[0]), float(lo_h[1]), float(lo_h[2]),
-             ext, a0lo, a0hi, self.buckets, ptr(keys), _stream())
-        skeys, _ = torch.sort(keys)
-        self.perm = (skeys & 0xFFFFFFF).to(torch.int32)
-        self._ptable_ok = False   # new units: rebuild the pairing table
+        ws = workspace(self.dev)
+        lib = _lib.load()
+        bounds = ws.get("cloud_bounds", 8, torch.float64)
+        bws = ws.get("cloud_bounds_ws", int(lib.pab_cloud_bounds_workspace_bytes()) // 8 + 1, torch.float64)
+        keys = ws.get("sort_keys", n, torch.int64)
+        sws = ws.get("sort_ws", int(lib.pab_sort_perm_workspace_bytes(n)) // 8 + 1, torch.int64)
+        self.perm = torch.empty(n, dtype=torch.int32, device=self.dev)
+        call("pab_cloud_bounds", ptr(self.pos), ptr(self.a0), n, ptr(bounds), ptr(bws), _stream())
+        call("pab_sort_keys", ptr(self.pos), ptr(self.a0), n, ptr(bounds), self.buckets, ptr(keys), _stream())
+        call("pab_sort_perm", ptr(keys), n, ptr(self.perm), ptr(sws), _stream())
 
     def pack(self) -> None:
         if self._packed:
@@ -206,7 +209,6 @@ class DeviceCloud:
             call("pab_pack", ptr(self.pos), ptr(self.p0), ptr(self.a0), ptr(self.perm), self.n,
                  ptr(self.rec_a), ptr(self.rec_b), ptr(self.gmeta), _stream())
         self._packed = True
-        self._stats = None
 
     def pair_table(self) -> torch.Tensor:
         """Dual-walk pairing table: which two balls of a 64-ball unit a lane
@@ -223,20 +225,6 @@ class DeviceCloud:
                 call("pab_pair_table", ptr(self.rec_a), ptr(self.gmeta), self.n_groups, ptr(self.ptable), _stream())
             self._ptable_ok = True
         return self.ptable
-
-    def stats(self) -> tuple[float, float]:
-        """(median lane-group radius, max a0) for launch planning."""
-        if self._stats is None:
-            ng = self.n_groups
-            if ng == 0:
-                self._stats = (0.0, 0.0)
-            else:
-                meta = self.gmeta[: ng * GROUP_META_BYTES].view(torch.float32).view(ng, GROUP_META_BYTES // 4)
-                r = float(torch.median(meta[:, 6]).item())
-                amax = float(torch.max(meta[:, 7]).item())
-                self._stats = (r, amax)
-        return self._stats
-
 
 # ---------------------------------------------------------------------------
 # Workspace and launch planning
@@ -400,6 +388,9 @@ def forward_rows(cloud: DeviceCloud, det: DeviceDetectors, acq: Acq, counters: P
     residual sim - real and the per-row FP64 sum of squares is returned
     (``real_ready``: event the supervision upload records; only the residual
     epilogue waits for it, the forward kernel overlaps the copy).
+    ``real_local`` may also be a callable returning (tensor, event): it is
+    called right after the forward kernel is queued, so a host-side upload
+    of the supervision runs while the GPU simulates.
     Returns (out [J_local, n_out] f32, loss_rows [J_local] f64 or None)."""
     ws = workspace(cloud.dev)
     n_out = acq.n_out
@@ -424,6 +415,8 @@ def forward_rows(cloud: DeviceCloud, det: DeviceDetectors, acq: Acq, counters: P
              plan.tile_rows, ptr(partial), ptr(counters.ops), ptr(counters.status), _stream())
     else:
         partial.zero_()
+    if callable(real_local):
+        real_local, real_ready = real_local()
     if real_ready is not None:
         torch.cuda.current_stream(cloud.dev).wait_event(real_ready)
     _mark("residual", 0)
