@@ -260,7 +260,7 @@ def _acq(ctx, f: int) -> E.Acq:
 
 def _run_model(cloud, ctx, f, real=None, stage="fine"):
     a0 = np.asarray(cloud.a0, dtype=np.float64)
-    if a0.size and a0.min() <= 0.0:   # = np.any(a0 <= 0) of radiator.py:293 (NaN passes both), one pass
+    if a0.size and np.fmin.reduce(a0) <= 0.0:   # = np.any(a0 <= 0) of radiator.py:293 (NaNs ignored), one pass
         raise ValueError("all a0 must be > 0 for forward simulation")
     grid = ctx.grid
     n_out = grid.decimated(f).n_samples if f > 1 else grid.n_samples
