@@ -59,21 +59,23 @@ __global__ void bounds_partial_kernel(const double* __restrict__ pos, const doub
 }
 
 __global__ void bounds_final_kernel(const double* __restrict__ part, int nb, double* __restrict__ bounds) {
-  if (threadIdx.x != 0) return;
-  double lo[4], hi[4];
-  for (int c = 0; c < 4; ++c) { lo[c] = part[c]; hi[c] = part[4 + c]; }
-  for (int b = 1; b < nb; ++b)
-    for (int c = 0; c < 4; ++c) {
-      lo[c] = fmin(lo[c], part[(size_t)b * 8 + c]);
-      hi[c] = fmax(hi[c], part[(size_t)b * 8 + 4 + c]);
-    }
-  const double ext = fmax(fmax(hi[0] - lo[0], hi[1] - lo[1]), hi[2] - lo[2]);
-  bounds[0] = lo[0];
-  bounds[1] = lo[1];
-  bounds[2] = lo[2];
-  bounds[3] = ext > 0.0 ? ext : 1.0;
-  bounds[4] = lo[3];
-  bounds[5] = hi[3];
+  __shared__ double r[8];
+  const int c = threadIdx.x;   // one thread per component (min x, y, z, a0; max x, y, z, a0)
+  if (c < 8) {
+    double v = part[c];
+    for (int b = 1; b < nb; ++b) v = c < 4 ? fmin(v, part[(size_t)b * 8 + c]) : fmax(v, part[(size_t)b * 8 + c]);
+    r[c] = v;
+  }
+  __syncthreads();
+  if (c == 0) {
+    const double ext = fmax(fmax(r[4] - r[0], r[5] - r[1]), r[6] - r[2]);
+    bounds[0] = r[0];
+    bounds[1] = r[1];
+    bounds[2] = r[2];
+    bounds[3] = ext > 0.0 ? ext : 1.0;
+    bounds[4] = r[3];
+    bounds[5] = r[7];
+  }
 }
 
 __global__ void radix_hist_kernel(const unsigned long long* __restrict__ keys, int64_t n, int shift,
