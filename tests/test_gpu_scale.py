@@ -1,9 +1,10 @@
 """Parity at the scales where FP32 accumulation is hardest.
 
-* Config 2 with the FULL 1M-ball cloud on 8 strided detectors: up to
-  1e4-1e5 contributions land on one sample (reference scatter
-  radiator.py:253-255); rows and every ball's fine gradients against the
-  FP64 oracle (north_star: rows rel L2 <= 1e-4, gradients <= 1e-3).
+* Config 2 with the FULL 1M-ball cloud and config 4 with the full 4M-ball
+  slab (element directivity) on 8 strided detectors: up to 1e4-1e5
+  contributions land on one sample (reference scatter radiator.py:253-255);
+  rows and every ball's fine gradients against the FP64 oracle (north_star:
+  rows rel L2 <= 1e-4, gradients <= 1e-3).
 * Zero-gradient filter decisions (reference optimizer.py:230-258) of
   config 3 (96^3 grid, 512 detectors) and config 5 (256^3 grid in the
   ellipsoid, 2048 detectors) at the schedule's first factor f = 4 on
@@ -97,6 +98,61 @@ def test_config2_full_million_ball_cloud(P):
     errs = [rel_l2(g.d_p0, gp0), rel_l2(g.d_a0, ga0), rel_l2(g.d_position, gpos)]
     print(f"config 2 full cloud: loss {Lg:.6e} vs {L:.6e}; gradient rel L2 p0 {errs[0]:.2e} a0 {errs[1]:.2e} "
           f"pos {errs[2]:.2e}")
+    assert abs(Lg - L) <= 1e-4 * L
+    assert max(errs) <= 1e-3
+
+
+@pytest.mark.timeout(1800)
+def test_config4_full_four_million_ball_cloud(P):
+    """Config 4 in full (4M balls in the slab, 0.5 mm square-element
+    directivity, 6144 samples) on 8 strided detectors of the tilted planar
+    array: rows and every ball's fine gradients against the oracle."""
+    from paper_2601_00551_b200 import scenes
+    sc = scenes.planar_config()
+    sel = np.arange(3, 1024, 128)
+    array = P.SensorArray(sc.array.positions[sel], 1500.0, normals=sc.array.normals[sel])
+    ctx = P.ForwardContext(array, sc.grid, directivity=P.Directivity("element", width=0.5e-3))
+    kind = ("element", 0.5e-3)
+    t, c = sc.truth, sc.init
+    real = np.sum(oracle_rows_chunked(t.positions, t.p0, t.a0, array.positions, array.normals, sc.grid.dt,
+                                      sc.grid.n_samples, kind), axis=0)
+    got = P.simulate_signals(t, ctx).data
+    e_rows = rel_l2(got, real)
+    _, L, (gp0, ga0, gpos) = oracle_grads_chunked(c.positions, c.p0, c.a0, array.positions, array.normals,
+                                                  sc.grid.dt, sc.grid.n_samples, kind, real)
+    Lg, g = P.backward(c, ctx, P.SignalSet(sc.grid, real), stage="fine")
+    errs = [rel_l2(g.d_p0, gp0), rel_l2(g.d_a0, ga0), rel_l2(g.d_position, gpos)]
+    print(f"config 4 full cloud: rows rel L2 {e_rows:.2e}; loss {Lg:.6e} vs {L:.6e}; gradient rel L2 p0 "
+          f"{errs[0]:.2e} a0 {errs[1]:.2e} pos {errs[2]:.2e}")
+    assert e_rows <= 1e-4
+    assert abs(Lg - L) <= 1e-4 * L
+    assert max(errs) <= 1e-3
+
+
+@pytest.mark.timeout(2400)
+def test_config5_full_grid_cloud(P):
+    """Config 5's initial cloud in full (the 256^3 grid cropped to the
+    ellipsoid: 8.8M balls, 8192 samples, cos^2 directivity) on 4 strided
+    detectors of the ring cylinder: rows of the 300k-ball truth and of the
+    grid cloud, and every grid ball's fine gradients against the oracle."""
+    from paper_2601_00551_b200 import scenes
+    sc = scenes.mouse_config()
+    sel = np.arange(5, 2048, 512)
+    array = P.SensorArray(sc.array.positions[sel], 1500.0, normals=sc.array.normals[sel])
+    ctx = P.ForwardContext(array, sc.grid, directivity=P.Directivity("cos_power", power=2.0))
+    kind = ("cos_power", 2.0)
+    t, c = sc.truth, sc.init
+    real = np.sum(oracle_rows_chunked(t.positions, t.p0, t.a0, array.positions, array.normals, sc.grid.dt,
+                                      sc.grid.n_samples, kind), axis=0)
+    e_truth = rel_l2(P.simulate_signals(t, ctx).data, real)
+    rows, L, (gp0, ga0, gpos) = oracle_grads_chunked(c.positions, c.p0, c.a0, array.positions, array.normals,
+                                                     sc.grid.dt, sc.grid.n_samples, kind, real, chunk=100000)
+    e_grid = rel_l2(P.simulate_signals(c, ctx).data, rows)
+    Lg, g = P.backward(c, ctx, P.SignalSet(sc.grid, real), stage="fine")
+    errs = [rel_l2(g.d_p0, gp0), rel_l2(g.d_a0, ga0), rel_l2(g.d_position, gpos)]
+    print(f"config 5 full grid cloud ({len(c)} balls): rows rel L2 truth {e_truth:.2e}, grid {e_grid:.2e}; loss "
+          f"{Lg:.6e} vs {L:.6e}; gradient rel L2 p0 {errs[0]:.2e} a0 {errs[1]:.2e} pos {errs[2]:.2e}")
+    assert e_truth <= 1e-4 and e_grid <= 1e-4
     assert abs(Lg - L) <= 1e-4 * L
     assert max(errs) <= 1e-3
 
