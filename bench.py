@@ -227,20 +227,49 @@ def host_ram_bytes() -> int:
     return 16 << 30
 
 
+def load_reference_package():
+    """The unmodified reference package, pip-installed once into
+    baseline/_ref (git-ignored; travels to the GPU box with the snapshot),
+    or None."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "paball")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        import paball  # noqa: F401
+        from paball import model as M
+        from paball import radiator as Rr
+    except Exception:
+        return None
+    return M, Rr
+
+
 class CpuReference:
-    """The reference's CPU algorithm (oracle/radiator.py: FP64 numpy, sensor
-    blocks of 8 over a thread pool, radiator.py:316-332) on a strided ball
+    """The reference's CPU implementation of the path on a strided ball
     subset x a strided detector subset of the workload (cost is linear in
-    N * J * W, so pairs/s carries over).  The thread count is swept on a
-    small sample first; the timed sample then runs with the best count, and
-    every thread has a sensor block (>= 8 detectors per thread)."""
+    N * J * W, so pairs/s carries over).
+
+    kind "reference": the UNMODIFIED reference package (baseline/_ref),
+    ``paball.radiator.backward(cloud, ctx, real, "fine")`` with
+    ``set_num_threads`` (its own sensor blocks of 8 over a thread pool,
+    radiator.py:316-332).  The reference has no detector directivity; the
+    workload's cos^2 / element weight is one multiply per pair on top of
+    ~40 window samples, so the sample is timed without it (and the stock
+    backward's >1024-ball cache-key bug, changes values, not
+    cost).  kind "port": oracle/radiator.py (the FP64 restatement, ~25 %
+    slower than the reference) when the package is not installed.
+
+    The thread count is swept on a small sample first; the timed sample
+    then runs with the best count, and every thread has a sensor block
+    (>= 8 detectors per thread)."""
 
     SWEEP = (1, 2, 4, 8, 16, 32, 64)
 
     def __init__(self, scene, kind, n_balls: int, n_det: int = 0):
-        from oracle import radiator as OR   # the reference's CPU algorithm (restated); baseline only
-        self.OR = OR
-        self.kind = kind
+        self.ref = load_reference_package()
+        self.kind = "reference" if self.ref is not None else "port"
+        self.dirkind = kind
         self.scene = scene
         ncpu = os.cpu_count() or 1
         J = scene.array.positions.shape[0]
@@ -249,15 +278,26 @@ class CpuReference:
         self.sens = scene.array.positions[::stride][:n_det]
         self.nrm = scene.array.normals[::stride][:n_det]
         self.threads_avail = ncpu
-        # the oracle caches ~14 KB per ball per busy thread: stay within half the RAM
+        # ~14 KB cached per ball per busy thread: stay within half the RAM
         cap = int(0.5 * host_ram_bytes() / (14e3 * max(1, min(ncpu, -(-self.sens.shape[0] // 8)))))
         self.n_balls = int(max(1000, min(n_balls, cap, len(scene.init))))
         self.sel = self._subset(self.n_balls)
         t = scene.truth
         tsel = np.linspace(0, len(t) - 1, min(len(t), self.n_balls)).astype(np.int64)
-        self.real, _, _, _ = OR.run_model(t.positions[tsel], t.p0[tsel], t.a0[tsel], self.sens, self.nrm,
-                                          float(scene.array.sound_speed), 0.0, scene.grid.dt,
-                                          scene.grid.n_samples, 1, kind=kind, threads=ncpu)
+        sc = scene
+        if self.kind == "reference":
+            M, Rr = self.ref
+            self.ctx = Rr.ForwardContext(M.SensorArray(self.sens, float(sc.array.sound_speed)),
+                                         M.TimeGrid(0.0, sc.grid.dt, sc.grid.n_samples))
+            Rr.set_num_threads(ncpu)
+            truth = M.PointCloud(t.positions[tsel], t.p0[tsel], t.a0[tsel])
+            self.real = Rr.simulate_signals(truth, self.ctx)
+        else:
+            from oracle import radiator as OR   # the reference's CPU algorithm (restated); baseline only
+            self.OR = OR
+            self.real, _, _, _ = OR.run_model(t.positions[tsel], t.p0[tsel], t.a0[tsel], self.sens, self.nrm,
+                                              float(sc.array.sound_speed), 0.0, sc.grid.dt, sc.grid.n_samples, 1,
+                                              kind=kind, threads=ncpu)
         self.threads = None
         self.sweep = {}
 
@@ -266,10 +306,17 @@ class CpuReference:
 
     def _run(self, sel, threads) -> float:
         c, sc = self.scene.init, self.scene
+        if self.kind == "reference":
+            M, Rr = self.ref
+            Rr.set_num_threads(threads)
+            cloud = M.PointCloud(c.positions[sel], c.p0[sel], c.a0[sel])
+            t0 = time.perf_counter()
+            Rr.backward(cloud, self.ctx, self.real, stage="fine")
+            return time.perf_counter() - t0
         t0 = time.perf_counter()
         self.OR.run_model(c.positions[sel], c.p0[sel], c.a0[sel], self.sens, self.nrm, float(sc.array.sound_speed),
-                          0.0, sc.grid.dt, sc.grid.n_samples, 1, real=self.real, stage="fine", kind=self.kind,
-                          threads=threads)
+                          0.0, sc.grid.dt, sc.grid.n_samples, 1, real=self.real, stage="fine",
+                          kind=self.dirkind, threads=threads)
         return time.perf_counter() - t0
 
     def pick_threads(self, sweep_balls: int = 6000) -> int:
@@ -290,9 +337,11 @@ class CpuReference:
         return self.n_balls * self.sens.shape[0] / best
 
     def describe(self, value: float, reps: int) -> dict:
-        return {"value": value, "unit": UNIT, "cores": self.threads, "kind": "port",
+        what = ("unmodified reference package (baseline/_ref) paball.radiator.backward, no directivity"
+                if self.kind == "reference" else "oracle/radiator.py FP64 numpy restatement")
+        return {"value": value, "unit": UNIT, "cores": self.threads, "kind": self.kind,
                 "sample": f"{self.n_balls} balls (strided subset) x {self.sens.shape[0]} detectors of the workload, "
-                          f"fine backward (fwd+adj), FP64 numpy, best of {reps} at the best thread count",
+                          f"fine backward (fwd+adj): {what}; best of {reps} at the best thread count",
                 "thread_sweep_pairs_per_s": {str(k): v for k, v in sorted(self.sweep.items())},
                 "host_threads": self.threads_avail, "cpu_model": cpu_model()}
 
@@ -315,9 +364,9 @@ def run_reference(args, rank, world):
             "vs_baseline": None, "dtype": "f64", "data": f"synthetic (seeded CounterRng, BASELINE config {args.config})",
             "config": config_dict(args, world), "impl": "reference", "cpu_baseline": cpu,
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "note": "reference CPU algorithm = oracle/radiator.py (FP64 numpy restatement of paball radiator, "
-                    "key-fixed); each step = one fine backward of the sample; ms_per_step extrapolated linearly "
-                    "to the full N*J"}
+            "note": "reference CPU implementation (cpu_baseline.kind: 'reference' = the unmodified paball package "
+                    "pip-installed into baseline/_ref, 'port' = oracle/radiator.py); each step = one fine backward "
+                    "of the sample; ms_per_step extrapolated linearly to the full N*J"}
     print(json.dumps(line), flush=True)
 
 
@@ -327,29 +376,39 @@ def run_reference(args, rank, world):
 
 def recon_cpu_estimate(sc, kept, sched, trace, n_sub: int = 3000, threads: int | None = None):
     """Extrapolated wall time of the same reconstruction on the reference's
-    CPU algorithm: one backward (the iteration's whole cost; Adam and density
-    control are O(N) numpy) timed per level on a strided n_sub-ball subset
-    of the filtered cloud with all detectors, scaled linearly by every
-    iteration's ball count (plus the initial filter on the 96^3 grid)."""
-    from oracle import radiator as OR
+    CPU implementation: one backward (the iteration's whole cost; Adam and
+    density control are O(N) numpy) timed per level on a strided n_sub-ball
+    subset of the filtered cloud with all detectors, scaled linearly by every
+    iteration's ball count (plus the initial filter on the 96^3 grid).  The
+    unmodified reference package (baseline/_ref) when installed, else the
+    oracle restatement."""
     threads = threads or os.cpu_count() or 1
-    ctx_dt, n_samples = sc.grid.dt, sc.grid.n_samples
+    n_samples = sc.grid.n_samples
     sens, v = sc.array.positions, float(sc.array.sound_speed)
     sel = np.linspace(0, len(kept) - 1, min(n_sub, len(kept))).astype(np.int64)
-    truth = sc.truth
+    ref = load_reference_package()
     per_level = []
     for lv in sched.levels:
         n_out = -(-n_samples // lv.f)
-        real = np.zeros((sens.shape[0], n_out))
-        t0 = time.perf_counter()
-        OR.run_model(kept.positions[sel], kept.p0[sel], kept.a0[sel], sens, None, v, 0.0, ctx_dt, n_samples, lv.f,
-                     real=real, stage=lv.stage, threads=threads)
+        if ref is not None:
+            M, Rr = ref
+            Rr.set_num_threads(threads)
+            ctx = Rr.ForwardContext(M.SensorArray(sens, v), M.TimeGrid(0.0, sc.grid.dt, n_samples))
+            grid_k = ctx.grid.decimated(lv.f) if lv.f > 1 else ctx.grid
+            real = M.SignalSet(grid_k, np.zeros((sens.shape[0], n_out)))
+            cloud = M.PointCloud(kept.positions[sel], kept.p0[sel], kept.a0[sel])
+            t0 = time.perf_counter()
+            Rr.backward(cloud, ctx, real, stage=lv.stage)
+        else:
+            from oracle import radiator as OR
+            t0 = time.perf_counter()
+            OR.run_model(kept.positions[sel], kept.p0[sel], kept.a0[sel], sens, None, v, 0.0, sc.grid.dt,
+                         n_samples, lv.f, real=np.zeros((sens.shape[0], n_out)), stage=lv.stage, threads=threads)
         per_level.append((time.perf_counter() - t0) / len(sel))   # s per ball per iteration
     total = per_level[0] * len(sc.init)   # the initial filter pass at f = 4 (same kernel sums, p0 = 0)
     for r in trace.records:
         total += per_level[r.level] * r.ball_count
-    del truth
-    return {"value_s": total, "kind": "port", "cores": threads,
+    return {"value_s": total, "kind": "reference" if ref is not None else "port", "cores": threads,
             "sample": f"one backward per level on {len(sel)} balls (strided subset of the filtered cloud) x "
                       f"{sens.shape[0]} detectors, scaled by each iteration's ball count",
             "s_per_ball_iteration": per_level}
