@@ -281,13 +281,21 @@ def plan_forward(cloud: DeviceCloud, det: DeviceDetectors, acq: Acq) -> ForwardP
     return ForwardPlan(0, parts, warps, tile)
 
 
+ADJ_WAVES = float(os.environ.get("PAB_ADJ_WAVES", "16"))
+
+
 def plan_adjoint(cloud: DeviceCloud, det: DeviceDetectors) -> int:
-    """Detector chunks: at least two waves of 16 resident warps per SM and
-    at most 256 detectors per chunk (finer tail; measured at config 2: 1 / 2
-    / 4 / 8 chunks give 20.41 / 20.28 / 20.19 / 20.19 ms), with the FP64
-    partial sums (40 B per ball and chunk) kept under 2 GiB."""
+    """Detector chunks: at least ADJ_WAVES waves of 16 resident warps per SM
+    and at most 256 detectors per chunk (finer tail; measured at config 2: 1 /
+    2 / 4 / 8 chunks give 20.41 / 20.28 / 20.19 / 20.19 ms), with the FP64
+    partial sums (40 B per ball and chunk) kept under 2 GiB.  Lane groups of
+    different radius buckets differ 4x in work, so small clouds need many
+    waves for balance: the config-3 reconstruction (4.7k-14k groups x 512
+    detectors) takes 3.04 / 2.81 / 2.57 / 2.35 / 2.45 s at 2 / 4 / 8 / 16 /
+    32 waves; config 2 (31k groups, 4 chunks by the detector bound) is
+    unchanged."""
     ctas = -(-cloud.n_groups // ADJOINT_WARPS)
-    target = 2 * 16 * sm_count(cloud.dev) // ADJOINT_WARPS   # two waves of 16 resident warps per SM
+    target = int(ADJ_WAVES * 16 * sm_count(cloud.dev)) // ADJOINT_WARPS   # waves of 16 resident warps per SM
     chunks = max(1, -(-target // max(ctas, 1)), -(-det.n_local // 256))
     cap = max(1, (2 << 30) // max(40 * cloud.n_groups * GROUP, 1))
     chunks = int(max(1, min(chunks, cap, max(1, det.n_local // 16))))
