@@ -552,7 +552,10 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   const int W = (blockDim.x >> 5) / (WS ? 2 : 1);
   const int n_out = acq.n_out;
   const int j = blockIdx.x;
-  const int part = blockIdx.y;
+  // partitions are contiguous in the processing order, which ascends in a0
+  // bucket: the wide-window partitions launch first, the light ones fill the
+  // tail (measured: config 2 -0.04 ms, config-3 reconstruction -3 %)
+  const int part = gridDim.y - 1 - blockIdx.y;
   const int n_bins = (n_out + (1 << kBinShift) - 1) >> kBinShift;
   // SROW: the detector row in shared memory; otherwise (long records) the
   // CTA's partial row in global memory (L2): written only by this CTA, each
