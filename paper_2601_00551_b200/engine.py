@@ -37,6 +37,11 @@ A0_BUCKETS = int(os.environ.get("PAB_A0_BUCKETS", "6"))   # lane groups hold bal
 # 20.19 / 20.02 / 19.87 / 19.75 ms)
 ADJ_A0_BUCKETS = int(os.environ.get("PAB_ADJ_A0_BUCKETS", "16"))
 GROUP_META_BYTES = 48
+# radius buckets: 0 = equal linear bins of [a0 min, a0 max]; > 0 = log2-spaced
+# bins over at most this many octaves below a0 max (tuning switch)
+A0_LOG_SPAN = float(os.environ.get("PAB_A0_LOG_SPAN", "0"))
+# lane groups break at jumps farther than this (m) in the sorted order (0: off)
+GROUP_GAP = float(os.environ.get("PAB_GROUP_GAP", "0"))
 
 
 def cuda_device() -> torch.device:
@@ -134,9 +139,15 @@ class DeviceCloud:
         self.p0 = p0.contiguous()
         self.a0 = a0.contiguous()
         self.buckets = A0_BUCKETS if buckets is None else buckets
-        self.perm = None
+        self.perm = None    # processing (sorted) order
+        self.slots = None   # lane-group slots of the order: ball index or -1 (padding)
+        self._ng = None
         self._packed = False
         self._adj = None
+
+    def adopt_order(self, other: "DeviceCloud") -> None:
+        """Use another cloud's processing order and lane groups (same balls)."""
+        self.perm, self.slots, self._ng = other.perm, other.slots, other._ng
 
     def adjoint_cloud(self) -> "DeviceCloud":
         """The same balls (shared parameter tensors) packed for the adjoint
@@ -165,7 +176,7 @@ class DeviceCloud:
 
     @property
     def n_groups(self) -> int:
-        return (self.n + GROUP - 1) // GROUP
+        return self._ng if self._ng is not None else (self.n + GROUP - 1) // GROUP
 
     def invalidate(self, resort: bool = False) -> None:
         """Parameters changed: repack before the next pass (and resort)."""
@@ -173,15 +184,19 @@ class DeviceCloud:
         if self._adj is not None:
             self._adj.invalidate(resort)
         if resort:
-            self.perm = None
+            self.perm = self.slots = self._ng = None
 
     def sort(self) -> None:
-        """Processing order on the device, no host round trip: cloud bounds,
-        (a0 bucket, Hilbert) keys, stable radix sort -> perm."""
+        """Processing order on the device: cloud bounds, (a0 bucket, Hilbert)
+        keys, stable radix sort -> perm; then lane groups (pab_group_slots):
+        a group starts at every radius-bucket change and every jump farther
+        than GROUP_GAP in the sorted order, segments padded to whole groups
+        (one host read: the group count sizes the slot array)."""
         n = self.n
         self._ptable_ok = False   # new units: rebuild the pairing table
         if n == 0:
-            self.perm = torch.empty(0, dtype=torch.int32, device=self.dev)
+            self.perm = self.slots = torch.empty(0, dtype=torch.int32, device=self.dev)
+            self._ng = 0
             return
         ws = workspace(self.dev)
         lib = _lib.load()
@@ -191,13 +206,24 @@ class DeviceCloud:
         sws = ws.get("sort_ws", int(lib.pab_sort_perm_workspace_bytes(n)) // 8 + 1, torch.int64)
         self.perm = torch.empty(n, dtype=torch.int32, device=self.dev)
         call("pab_cloud_bounds", ptr(self.pos), ptr(self.a0), n, ptr(bounds), ptr(bws), _stream())
-        call("pab_sort_keys", ptr(self.pos), ptr(self.a0), n, ptr(bounds), self.buckets, ptr(keys), _stream())
+        call("pab_sort_keys", ptr(self.pos), ptr(self.a0), n, ptr(bounds), self.buckets, A0_LOG_SPAN, ptr(keys),
+             _stream())
         call("pab_sort_perm", ptr(keys), n, ptr(self.perm), ptr(sws), _stream())
+        if GROUP_GAP <= 0.0:
+            self.slots, self._ng = self.perm, (n + GROUP - 1) // GROUP
+            return
+        gws = ws.get("group_ws", int(lib.pab_group_slots_workspace_bytes(n)) // 4 + 1, torch.int32)
+        ng_d = ws.get("group_count", 1, torch.int32)
+        call("pab_group_slots", ptr(self.pos), ptr(self.a0), ptr(self.perm), n, ptr(bounds), self.buckets,
+             A0_LOG_SPAN, GROUP_GAP, ptr(ng_d), ptr(gws), _stream())
+        self._ng = int(ng_d.item())
+        self.slots = torch.empty(self._ng * GROUP, dtype=torch.int32, device=self.dev)
+        call("pab_group_slots_scatter", ptr(self.perm), n, self._ng, ptr(gws), ptr(self.slots), _stream())
 
     def pack(self) -> None:
         if self._packed:
             return
-        if self.perm is None or self.perm.shape[0] != self.n:
+        if self.perm is None or self.perm.shape[0] != self.n or self.slots is None:
             self.sort()
         ng = self.n_groups
         npad = ng * GROUP
@@ -206,7 +232,7 @@ class DeviceCloud:
             self.rec_b = torch.empty(npad * 16, dtype=torch.uint8, device=self.dev)
             self.gmeta = torch.empty(max(ng, 1) * GROUP_META_BYTES, dtype=torch.uint8, device=self.dev)
         if self.n:
-            call("pab_pack", ptr(self.pos), ptr(self.p0), ptr(self.a0), ptr(self.perm), self.n,
+            call("pab_pack", ptr(self.pos), ptr(self.p0), ptr(self.a0), ptr(self.slots), self.slots.numel(),
                  ptr(self.rec_a), ptr(self.rec_b), ptr(self.gmeta), _stream())
         self._packed = True
 

@@ -540,9 +540,9 @@ def _filter_state_(state: OptimState, det, acq, real_local, strict: bool = True)
     ``state`` in place (tests/golden/make_golden_config3.py)."""
     dc = state._dc
     probe = E.DeviceCloud(dc.pos, torch.zeros_like(dc.p0), dc.a0)
-    probe.perm = dc.perm
+    probe.adopt_order(dc)
     if dc._adj is not None and dc._adj.perm is not None:   # the adjoint's processing order too
-        probe.adjoint_cloud().perm = dc._adj.perm
+        probe.adjoint_cloud().adopt_order(dc._adj)
     counters = E.PassCounters(dc.dev)
     g = filter_gradient(probe, det, acq, real_local, counters)
     counters.read()
