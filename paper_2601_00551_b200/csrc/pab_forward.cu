@@ -1137,24 +1137,49 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
 
     PROF_ADD(pslot + 5, t_e2);
     PROF_T(t_f);
-    // ---- F: groups wider than the tile (rare): warp 0, linear passes ----
-    if (warp == 0) {
-      for (int idx = n_reg; idx < n_all; ++idx) {   // single groups only (a dual entry always fits)
-        const int64_t g = cg0 + (sorted[idx] & 0x7FFF);
-        const GroupMeta gm = gmeta[g];
-        const GroupDet gd = group_det(gm, det.px, det.py, det.pz, acq);
-        int lo, hi;
+    // ---- F: groups wider than the tile (rare in dense clouds; a quarter of
+    // the groups of a sparse filtered cloud): linear passes.  The union of
+    // their sample ranges is split into one time range per walker warp, so
+    // the warps never write the same row (no races, a fixed per-row order)
+    // and share the work (a serial warp 0 left 7 of 8 warps at the barrier:
+    // 71 % of the stall samples of a config-3 f = 1 forward) ----
+    if (warp < W && n_all > n_reg) {
+      auto range_of = [&](int idx, GroupMeta& gm, GroupDet& gd, int& lo, int& hi) {
+        gm = gmeta[cg0 + (sorted[idx] & 0x7FFF)];
+        gd = group_det(gm, det.px, det.py, det.pz, acq);
         group_range(acq, gd, gm, &lo, &hi);
+      };
+      int umin = INT_MAX, umax = INT_MIN;   // union of the wide groups' ranges (every warp alike)
+      for (int i0 = n_reg; i0 < n_all; i0 += kWarp) {
+        int lo = INT_MAX, hi = INT_MIN;
+        if (i0 + lane < n_all) {
+          GroupMeta gm;
+          GroupDet gd;
+          range_of(i0 + lane, gm, gd, lo, hi);
+        }
+        umin = min(umin, __reduce_min_sync(0xffffffffu, lo));
+        umax = max(umax, __reduce_max_sync(0xffffffffu, hi));
+      }
+      const int64_t span = (int64_t)umax - umin + 1;
+      const int t0 = umin + (int)((span * warp) / W), t1 = umin + (int)((span * (warp + 1)) / W);
+      for (int idx = n_reg; idx < n_all; ++idx) {   // single groups only (a dual entry always fits)
+        GroupMeta gm;
+        GroupDet gd;
+        int lo, hi;
+        range_of(idx, gm, gd, lo, hi);
+        const int a = max(lo, t0), b = min(hi, t1 - 1);
+        if (a > b) continue;
+        const int64_t g = cg0 + (sorted[idx] & 0x7FFF);
         const BallA A = ra[g * kWarp + lane];
         const BallB B = rb[g * kWarp + lane];
         const int near = group_near(acq, gd, gm) ? 1 : 0;
-        for (int base = lo - lo % kTile; base <= hi; base += kTile) {
-          const int top = base + kTile - 1;
+        for (int base = a - a % kTile; base <= b; base += kTile) {
+          const int c0 = max(base, a), c1 = min(base + kTile - 1, b);
           unsigned long long ops_once = 0;
-          evaluate_pair<DIR>(tile, lane, acq, gd, gm, det, dd, A, B, near, ops_once, coinc, base, top);
-          if (base + kTile > hi) my_ops += ops_once;   // count each pair once
+          evaluate_pair<DIR>(tile, lane, acq, gd, gm, det, dd, A, B, near, ops_once, coinc, c0, c1);
+          if (c0 == lo) my_ops += ops_once;   // counted once, by the warp whose range holds the group's first row
           __syncwarp();
-          flush_rows(tile, lane, base, min(top + 1, n_out), [&](int r, float v) { row[r] += v; });
+          flush_rows(tile, lane, c0, c1 + 1, [&](int r, float v) { row[r] += v; });
         }
       }
     }
