@@ -42,23 +42,6 @@ int pab_device_info(int device, int* sm_count, int* cc_major, int* cc_minor, int
 const char* pab_last_cuda_error(void);
 int pab_record_sizes(int* ball_a, int* ball_b, int* group_meta);
 
-/* Lane-group segmentation of a sorted cloud (perm from pab_sort_perm): a
- * group starts at every ball whose radius bucket (as pab_sort_keys with
- * a0_buckets / log_span) differs from its predecessor's or that lies farther
- * than `gap` (m) from it, and every 32nd ball of a segment; segments are
- * padded to whole groups.  Two calls: pab_group_slots writes the group count
- * to the device int *n_groups (the caller reads it to size `slots`), then
- * pab_group_slots_scatter fills slots[n_groups * 32] with ball indices and
- * -1 for padding (pab_pack takes it as its `perm`, n = n_groups * 32).
- * workspace: pab_group_slots_workspace_bytes(n), shared by both calls.
- * Replaces: nothing (the reference has no lane groups); keeps groups of
- * sparse clouds spatially compact. */
-size_t pab_group_slots_workspace_bytes(int64_t n);
-int pab_group_slots(const double* pos, const double* a0, const int32_t* perm, int64_t n, const double* bounds,
-                    int a0_buckets, double log_span, double gap, int* n_groups, void* workspace, void* stream);
-int pab_group_slots_scatter(const int32_t* perm, int64_t n, int64_t n_groups, const void* workspace,
-                            int32_t* slots, void* stream);
-
 /* ---- Host staging of the API edge (no GPU work) ----
  * Copy `bytes` (resp. narrow n float64 to float32) from a pageable caller
  * array into a 16-byte aligned page-locked staging buffer with non-temporal
@@ -76,12 +59,9 @@ size_t pab_cloud_bounds_workspace_bytes(void);
 int pab_cloud_bounds(const double* pos, const double* a0, int64_t n, double* bounds, void* workspace, void* stream);
 
 /* pab_morton_keys with the cube and a0 range read from device `bounds`
- * (pab_cloud_bounds), no host round trip.  log_span = 0: the same keys
- * (a0_buckets equal linear bins of [a0lo, a0hi]); log_span > 0: a0_buckets
- * log2-spaced bins of [max(a0lo, a0hi 2^-log_span), a0hi] (equal window-
- * length ratio per bucket, robust to a few outsized balls). */
+ * (pab_cloud_bounds): the same keys, no host round trip. */
 int pab_sort_keys(const double* pos, const double* a0, int64_t n, const double* bounds, int a0_buckets,
-                  double log_span, int64_t* keys, void* stream);
+                  int64_t* keys, void* stream);
 
 /* Stable LSD radix sort (five 7-bit passes over key bits [28, 63); the low
  * 28 bits are the input index, already ascending) of pab_sort_keys /
@@ -104,7 +84,7 @@ int pab_morton_keys(const double* pos /*[n][3]*/, const double* a0, int64_t n, d
 
 /* Pack a cloud (caller order, FP64 SoA) into processing-order records.
  * perm[i] = caller index of the i-th processed ball, or -1 for an inert
- * padding slot (pab_group_slots_scatter).  rec_a/rec_b hold
+ * padding slot.  rec_a/rec_b hold
  * ceil(n/32)*32 records of 16 bytes, group_meta ceil(n/32) records of 48 bytes.
  * Replaces: PointCloud field coercion (model.py:186-205) at the radiator boundary. */
 int pab_pack(const double* pos, const double* p0, const double* a0, const int32_t* perm /*-1: padding*/, int64_t n,

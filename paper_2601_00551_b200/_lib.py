@@ -22,12 +22,9 @@ _SIGS = {
     "pab_morton_keys": ([_vp, _vp, _i64, _d, _d, _d, _d, _d, _d, _i, _vp, _vp], _i),
     "pab_cloud_bounds_workspace_bytes": ([], C.c_size_t),
     "pab_cloud_bounds": ([_vp, _vp, _i64, _vp, _vp, _vp], _i),
-    "pab_sort_keys": ([_vp, _vp, _i64, _vp, _i, _d, _vp, _vp], _i),
+    "pab_sort_keys": ([_vp, _vp, _i64, _vp, _i, _vp, _vp], _i),
     "pab_sort_perm_workspace_bytes": ([_i64], C.c_size_t),
     "pab_sort_perm": ([_vp, _i64, _vp, _vp, _vp], _i),
-    "pab_group_slots_workspace_bytes": ([_i64], C.c_size_t),
-    "pab_group_slots": ([_vp, _vp, _vp, _i64, _vp, _i, _d, _d, _vp, _vp, _vp], _i),
-    "pab_group_slots_scatter": ([_vp, _i64, _i64, _vp, _vp, _vp], _i),
     "pab_pack": ([_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp], _i),
     "pab_forward_smem_bytes": ([_i, _i, _i], C.c_size_t),
     "pab_pair_table_bytes": ([_i64], C.c_size_t),
@@ -97,8 +94,7 @@ def load(path: str = LIB_PATH):
 # its timed region as gpu_launches).  Every launching entry point issues one
 # kernel, except these.
 LAUNCHES = {"kernels": 0}
-_KERNELS_PER_CALL = {"pab_host_stage_copy": 0, "pab_host_stage_narrow": 0, "pab_compact": 3, "pab_sumsq_diff_f64": 2, "pab_cloud_bounds": 2, "pab_sort_perm": 15,
-                     "pab_group_slots": 9, "pab_group_slots_scatter": 2}
+_KERNELS_PER_CALL = {"pab_host_stage_copy": 0, "pab_host_stage_narrow": 0, "pab_compact": 3, "pab_sumsq_diff_f64": 2, "pab_cloud_bounds": 2, "pab_sort_perm": 15}
 
 
 def call(name: str, *args) -> None:

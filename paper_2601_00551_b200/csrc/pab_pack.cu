@@ -81,24 +81,11 @@ __global__ void morton_keys_kernel(const double* __restrict__ pos, const double*
 // Same keys with the bounds read from device memory (pab_cloud_bounds): no
 // host round trip between the bounds and the keys.
 __global__ void sort_keys_dev_kernel(const double* __restrict__ pos, const double* __restrict__ a0, int64_t n,
-                                     const double* __restrict__ bounds, int nbuckets, double log_span,
-                                     int64_t* __restrict__ keys) {
+                                     const double* __restrict__ bounds, int nbuckets, int64_t* __restrict__ keys) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double a0lo = bounds[4], a0hi = bounds[5];
   const int nb = (nbuckets > 1 && a0hi > a0lo) ? nbuckets : 1;
-  if (log_span > 0.0 && nb > 1) {
-    // log2-spaced radius buckets over [max(a0lo, a0hi 2^-span), a0hi]: every
-    // bucket spans the same window-length ratio whatever the outliers (a few
-    // balls grown to 10x the bulk radius no longer squeeze the bulk into one
-    // linear bucket); balls below the range share bucket 0
-    const double llo = log2(fmax(a0lo, a0hi * exp2(-log_span))), lhi = log2(a0hi);
-    const double x = lhi > llo ? (log2(a0[i]) - llo) / (lhi - llo) : 0.0;
-    const int64_t k = sort_key(pos, a0, i, bounds[0], bounds[1], bounds[2], 1.0 / bounds[3], 0.0, 0.0, 1);
-    const int b = (int)fmin(fmax(x * nb, 0.0), (double)(nb - 1));
-    keys[i] = (int64_t)((uint64_t)k | ((uint64_t)b << 58));
-    return;
-  }
   keys[i] = sort_key(pos, a0, i, bounds[0], bounds[1], bounds[2], 1.0 / bounds[3], a0lo,
                      nb > 1 ? 1.0 / (a0hi - a0lo) : 0.0, nb);
 }
@@ -126,7 +113,7 @@ __global__ void pack_kernel(const double* __restrict__ pos, const double* __rest
   const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (g >= n_groups) return;
   const int64_t i = g * kWarp + lane;
-  const int b_in = i < n ? perm[i] : -1;   // -1: padding slot of a segmented order (pab_group_slots)
+  const int b_in = i < n ? perm[i] : -1;   // -1: inert padding slot
   const bool live = b_in >= 0;
   int b = 0;
   double x = 0, y = 0, z = 0, pp = 0, aa = 1.0;
@@ -293,13 +280,12 @@ int pab_morton_keys(const double* pos, const double* a0, int64_t n, double lox, 
 }
 
 int pab_sort_keys(const double* pos, const double* a0, int64_t n, const double* bounds, int a0_buckets,
-                  double log_span, int64_t* keys, void* stream) {
+                  int64_t* keys, void* stream) {
   if (n <= 0) return 0;
-  if (!pos || !a0 || !bounds || !keys || n > (1ll << 28) || a0_buckets < 1 || a0_buckets > 16 || log_span < 0.0)
-    return 1;
+  if (!pos || !a0 || !bounds || !keys || n > (1ll << 28) || a0_buckets < 1 || a0_buckets > 16) return 1;
   const int threads = 256;
   sort_keys_dev_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0, (cudaStream_t)stream>>>(
-      pos, a0, n, bounds, a0_buckets, log_span, keys);
+      pos, a0, n, bounds, a0_buckets, keys);
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 

@@ -165,103 +165,6 @@ __global__ void radix_scatter_kernel(const unsigned long long* __restrict__ kin,
   }
 }
 
-// ---- lane-group segmentation of the sorted order -------------------------
-// Consecutive balls of the sorted order form lane groups of 32.  In a sparse
-// cloud (a filtered reconstruction: balls along vessels) 32 consecutive
-// Hilbert-order balls can straddle a jump between distant structures, and
-// a wide group spans more samples than the forward's tile (it then takes
-// the serial path) and stages a long residual segment in the adjoint.  A
-// new group therefore starts wherever the sorted order crosses a radius
-// bucket or jumps farther than `gap`; segments are padded to whole groups
-// with inert slots (-1).
-
-__device__ __forceinline__ int a0_bucket(double a, const double* bounds, int nbuckets, double log_span) {
-  const double a0lo = bounds[4], a0hi = bounds[5];
-  if (nbuckets <= 1 || !(a0hi > a0lo)) return 0;
-  if (log_span > 0.0) {
-    const double llo = log2(fmax(a0lo, a0hi * exp2(-log_span))), lhi = log2(a0hi);
-    const double x = lhi > llo ? (log2(a) - llo) / (lhi - llo) : 0.0;
-    return (int)fmin(fmax(x * nbuckets, 0.0), (double)(nbuckets - 1));
-  }
-  return (int)fmin(fmax((a - a0lo) / (a0hi - a0lo) * nbuckets, 0.0), (double)(nbuckets - 1));
-}
-
-__global__ void segment_flags_kernel(const double* __restrict__ pos, const double* __restrict__ a0,
-                                     const int32_t* __restrict__ perm, int64_t n, const double* __restrict__ bounds,
-                                     int nbuckets, double log_span, double gap2, int* __restrict__ flags) {
-  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  int f = 1;
-  if (k > 0) {
-    const int64_t b = perm[k], c = perm[k - 1];
-    const double dx = pos[3 * b] - pos[3 * c], dy = pos[3 * b + 1] - pos[3 * c + 1], dz = pos[3 * b + 2] - pos[3 * c + 2];
-    f = (dx * dx + dy * dy + dz * dz > gap2) ||
-        a0_bucket(a0[b], bounds, nbuckets, log_span) != a0_bucket(a0[c], bounds, nbuckets, log_span);
-  }
-  flags[k] = f;
-}
-
-// inclusive scan of ints, 1024 per block (warp shuffles), block totals out
-__global__ void scan_block_kernel(int* __restrict__ a, int64_t m, int* __restrict__ totals) {
-  __shared__ int wsum[32];
-  const int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int x = i < m ? a[i] : 0;
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) wsum[w] = x;
-  __syncthreads();
-  if (w == 0) {
-    int t = wsum[lane];
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, t, o);
-      if (lane >= o) t += y;
-    }
-    wsum[lane] = t;
-  }
-  __syncthreads();
-  if (w > 0) x += wsum[w - 1];
-  if (i < m) a[i] = x;
-  if (threadIdx.x == 1023) totals[blockIdx.x] = x;
-}
-
-__global__ void scan_add_kernel(int* __restrict__ a, int64_t m, const int* __restrict__ offsets) {
-  const int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
-  if (i < m && blockIdx.x > 0) a[i] += offsets[blockIdx.x];
-}
-
-// sid (inclusive scan of the flags) -> start index of every segment
-__global__ void segment_starts_kernel(const int* __restrict__ flags, const int* __restrict__ sid, int64_t n,
-                                      int* __restrict__ start) {
-  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < n && (k == 0 || sid[k] != sid[k - 1])) start[sid[k] - 1] = (int)k;
-  (void)flags;
-}
-
-// 1 where a ball opens a lane group (every 32nd ball of its segment)
-__global__ void group_opens_kernel(const int* __restrict__ sid, const int* __restrict__ start, int64_t n,
-                                   int* __restrict__ open) {
-  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < n) open[k] = ((k - start[sid[k] - 1]) & 31) == 0;
-}
-
-// gid (inclusive scan of the opens) -> slot of every ball; n_groups out
-__global__ void group_slots_kernel(const int32_t* __restrict__ perm, const int* __restrict__ sid,
-                                   const int* __restrict__ start, const int* __restrict__ gid, int64_t n,
-                                   int32_t* __restrict__ slots, int* __restrict__ n_groups) {
-  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  slots[(int64_t)(gid[k] - 1) * 32 + ((k - start[sid[k] - 1]) & 31)] = perm[k];
-  if (k == n - 1 && n_groups) *n_groups = gid[k];
-}
-
-__global__ void fill_i32_kernel(int32_t* __restrict__ a, int64_t m, int32_t v) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < m) a[i] = v;
-}
-
 }  // namespace pab
 
 using namespace pab;
@@ -301,55 +204,6 @@ int pab_sort_perm(int64_t* keys, int64_t n, int32_t* perm, void* workspace, void
     radix_scatter_kernel<<<nb, kSortThreads, 0, s>>>(a, b, n, shift, counts, nb, last ? perm : nullptr);
     if (!last) std::swap(a, b);
   }
-  return cudaGetLastError() == cudaSuccess ? 0 : 4;
-}
-
-// In-place inclusive scan of m ints (3 launches); workspace >= 2 (m / 1024 + 2) ints.
-static void scan_inclusive(int* a, int64_t m, int* ws, cudaStream_t s) {
-  const int64_t nb = (m + 1023) / 1024;
-  scan_block_kernel<<<(unsigned)nb, 1024, 0, s>>>(a, m, ws);
-  if (nb > 1) {
-    radix_scan_kernel<<<1, 1024, 0, s>>>(ws, (int)nb);   // exclusive: offsets of the blocks
-    scan_add_kernel<<<(unsigned)nb, 1024, 0, s>>>(a, m, ws);
-  }
-}
-
-size_t pab_group_slots_workspace_bytes(int64_t n) {
-  return (size_t)(4 * n + 2 * ((n + 1023) / 1024 + 2)) * sizeof(int) + 256;
-}
-
-int pab_group_slots(const double* pos, const double* a0, const int32_t* perm, int64_t n, const double* bounds,
-                    int a0_buckets, double log_span, double gap, int* n_groups, void* workspace, void* stream) {
-  if (n <= 0) return 0;
-  if (!pos || !a0 || !perm || !bounds || !n_groups || !workspace || n > (1ll << 28) || a0_buckets < 1 ||
-      a0_buckets > 16 || log_span < 0.0 || !(gap > 0.0))
-    return 1;
-  const cudaStream_t s = (cudaStream_t)stream;
-  int* flags = static_cast<int*>(workspace);   // -> sid after the scan
-  int* start = flags + n;
-  int* open = start + n;                        // -> gid after the scan
-  int* ws = open + n;
-  const unsigned blocks = (unsigned)((n + 255) / 256);
-  segment_flags_kernel<<<blocks, 256, 0, s>>>(pos, a0, perm, n, bounds, a0_buckets, log_span, gap * gap, flags);
-  scan_inclusive(flags, n, ws, s);
-  segment_starts_kernel<<<blocks, 256, 0, s>>>(flags, flags, n, start);
-  group_opens_kernel<<<blocks, 256, 0, s>>>(flags, start, n, open);
-  scan_inclusive(open, n, ws, s);
-  cudaMemcpyAsync(n_groups, open + (n - 1), sizeof(int), cudaMemcpyDeviceToDevice, s);
-  return cudaGetLastError() == cudaSuccess ? 0 : 4;
-}
-
-int pab_group_slots_scatter(const int32_t* perm, int64_t n, int64_t n_groups, const void* workspace,
-                            int32_t* slots, void* stream) {
-  if (n <= 0) return 0;
-  if (!perm || !workspace || !slots || n_groups < 1) return 1;
-  const cudaStream_t s = (cudaStream_t)stream;
-  const int* sid = static_cast<const int*>(workspace);
-  const int* start = sid + n;
-  const int* gid = start + n;
-  const int64_t m = n_groups * 32;
-  fill_i32_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(slots, m, -1);
-  group_slots_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(perm, sid, start, gid, n, slots, nullptr);
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 

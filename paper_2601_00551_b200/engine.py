@@ -37,11 +37,6 @@ A0_BUCKETS = int(os.environ.get("PAB_A0_BUCKETS", "6"))   # lane groups hold bal
 # 20.19 / 20.02 / 19.87 / 19.75 ms)
 ADJ_A0_BUCKETS = int(os.environ.get("PAB_ADJ_A0_BUCKETS", "16"))
 GROUP_META_BYTES = 48
-# radius buckets: 0 = equal linear bins of [a0 min, a0 max]; > 0 = log2-spaced
-# bins over at most this many octaves below a0 max (tuning switch)
-A0_LOG_SPAN = float(os.environ.get("PAB_A0_LOG_SPAN", "0"))
-# lane groups break at jumps farther than this (m) in the sorted order (0: off)
-GROUP_GAP = float(os.environ.get("PAB_GROUP_GAP", "0"))
 
 
 def cuda_device() -> torch.device:
@@ -187,11 +182,12 @@ class DeviceCloud:
             self.perm = self.slots = self._ng = None
 
     def sort(self) -> None:
-        """Processing order on the device: cloud bounds, (a0 bucket, Hilbert)
-        keys, stable radix sort -> perm; then lane groups (pab_group_slots):
-        a group starts at every radius-bucket change and every jump farther
-        than GROUP_GAP in the sorted order, segments padded to whole groups
-        (one host read: the group count sizes the slot array)."""
+        """Processing order on the device, no host round trip: cloud bounds,
+        (a0 bucket, Hilbert) keys, stable radix sort -> perm; lane group g
+        holds balls perm[32 g .. 32 g + 31].  (Measured and rejected this
+        round: breaking groups at radius-bucket changes and spatial jumps
+        (padded segments) and log2-spaced radius buckets were slower on
+        config 2 and on the config-3 reconstruction at every setting.)"""
         n = self.n
         self._ptable_ok = False   # new units: rebuild the pairing table
         if n == 0:
@@ -206,19 +202,9 @@ class DeviceCloud:
         sws = ws.get("sort_ws", int(lib.pab_sort_perm_workspace_bytes(n)) // 8 + 1, torch.int64)
         self.perm = torch.empty(n, dtype=torch.int32, device=self.dev)
         call("pab_cloud_bounds", ptr(self.pos), ptr(self.a0), n, ptr(bounds), ptr(bws), _stream())
-        call("pab_sort_keys", ptr(self.pos), ptr(self.a0), n, ptr(bounds), self.buckets, A0_LOG_SPAN, ptr(keys),
-             _stream())
+        call("pab_sort_keys", ptr(self.pos), ptr(self.a0), n, ptr(bounds), self.buckets, ptr(keys), _stream())
         call("pab_sort_perm", ptr(keys), n, ptr(self.perm), ptr(sws), _stream())
-        if GROUP_GAP <= 0.0:
-            self.slots, self._ng = self.perm, (n + GROUP - 1) // GROUP
-            return
-        gws = ws.get("group_ws", int(lib.pab_group_slots_workspace_bytes(n)) // 4 + 1, torch.int32)
-        ng_d = ws.get("group_count", 1, torch.int32)
-        call("pab_group_slots", ptr(self.pos), ptr(self.a0), ptr(self.perm), n, ptr(bounds), self.buckets,
-             A0_LOG_SPAN, GROUP_GAP, ptr(ng_d), ptr(gws), _stream())
-        self._ng = int(ng_d.item())
-        self.slots = torch.empty(self._ng * GROUP, dtype=torch.int32, device=self.dev)
-        call("pab_group_slots_scatter", ptr(self.perm), n, self._ng, ptr(gws), ptr(self.slots), _stream())
+        self.slots, self._ng = self.perm, (n + GROUP - 1) // GROUP
 
     def pack(self) -> None:
         if self._packed:
