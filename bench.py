@@ -431,15 +431,20 @@ def run_recon(world: int):
     lr = P.LearningRates.from_spacing(spacing)
     sched = P.Schedule((P.Level(4, 100, "coarse"), P.Level(2, 100, "fine"), P.Level(1, 100, "fine")),
                        duplication_period=100)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    kept, rep = P.zero_gradient_filter(sc.init, ctx, real, f=4)
-    final, trace = P.run_hierarchical(kept, ctx, real, sched, th, lr=lr, seed=103, filter_every=10, plateau=False)
-    torch.cuda.synchronize()
-    wall = max_over_ranks(time.perf_counter() - t0, world)
+    walls = []
+    for _ in range(2):   # the first run pays one-off allocations (workspaces, page-locked buffers): report the second
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        kept, rep = P.zero_gradient_filter(sc.init, ctx, real, f=4)
+        final, trace = P.run_hierarchical(kept, ctx, real, sched, th, lr=lr, seed=103, filter_every=10,
+                                          plateau=False)
+        torch.cuda.synchronize()
+        walls.append(time.perf_counter() - t0)
+    wall = max_over_ranks(walls[-1], world)
     out = {"workload": "config3: 512 det, 96^3 init, 50k-ball truth, 40 MHz x 4096, filter at f=4 then schedule "
                        "4/2/1 x 100 (filter every 10, density control every 100), fp32 kernels",
-           "wall_s": wall, "unit": "s", "higher_is_better": False, "iterations": len(trace.records),
+           "wall_s": wall, "unit": "s", "higher_is_better": False, "cold_run_wall_s": walls[0],
+           "iterations": len(trace.records),
            "n_init": len(sc.init), "n_after_filter": len(kept), "n_final": len(final),
            "loss_first": trace.records[0].loss, "loss_last": trace.records[-1].loss,
            "path": "paper_2601_00551_b200.zero_gradient_filter + run_hierarchical (public API, host wall clock)"}

@@ -425,8 +425,9 @@ def forward_rows(cloud: DeviceCloud, det: DeviceDetectors, acq: Acq, counters: P
     partial = ws.get("partial_rows", plan.partitions * J * n_out, torch.float32)
     loss_rows = ws.get("loss_rows", J, torch.float64) if real_local is not None else None
     if cloud.n_groups > 0:
-        # the dual walk (pairing table) unless PAB_FORWARD_DUAL=0 (single walks: A/B tests)
-        dual = os.environ.get("PAB_FORWARD_DUAL", "1") != "0" and acq.f <= int(os.environ.get("PAB_FORWARD_DUAL_MAXF", "64"))
+        # the dual walk (pairing table) at the native rate (measured on the config-3 reconstruction: single
+        # walks at f >= 2 are 2 % faster; windows of 8-17 samples); PAB_FORWARD_DUAL=0: single walks only
+        dual = os.environ.get("PAB_FORWARD_DUAL", "1") != "0" and acq.f <= int(os.environ.get("PAB_FORWARD_DUAL_MAXF", "1"))
         ptab = ptr(cloud.pair_table()) if dual else None
         call("pab_forward", ptr(cloud.rec_a), ptr(cloud.rec_b), ptr(cloud.gmeta), ptab,
              cloud.n_groups,
