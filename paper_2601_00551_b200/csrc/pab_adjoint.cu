@@ -202,6 +202,11 @@ __device__ __forceinline__ void moments_uniform(const float* seg, int L, float m
   M.T3 = A3.x + A3.y;
 }
 
+#ifndef PAB_ADJ_LEAN
+#define PAB_ADJ_LEAN 1   // XU-free rounding in the pair setup; factored cos^2 fine epilogue
+#endif
+constexpr bool kAdjLean = PAB_ADJ_LEAN != 0;
+
 // flags of a (lane group, detector) pair, computed by the batch lane
 constexpr int kFlagUniform = 1;   // staged uniform walk (far field, fits the segment)
 constexpr int kFlagNear = 2;      // a u+ window may exist
@@ -260,6 +265,7 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   const float qmax = live ? (rho * sc) * (rho * sc) : -1.0f;
   const WalkConst W = walk_const(sc, f);
   const float kap_rs = A.a0 * kSqrt2Ln2 * res_sign;   // kappa * sign
+  const float kap2 = 2.0f * A.a0 * kSqrt2Ln2;         // 2 kappa (factored epilogue)
   const float p0h = 0.5f * B.p0;
   // the uniform walk must stay inside the staged samples + zero padding
   // (cover window <= 2 rho / f + 3 samples, + 3 alignment + 3 rounding)
@@ -320,6 +326,9 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       if (fl & kFlagUniform) cp_async_wait_all();
     };
     float gb[5] = {0.f, 0.f, 0.f, 0.f, 0.f};   // FP32 batch sums of the pair terms
+    // lean cos^2 fine epilogue: per-ball factors taken out of the pair terms
+    // and applied once per batch (gb0 * rs / 4, gb1 * p0/2 k^3 rs, gb2-4 * p0/2 rs)
+    constexpr bool kFactored = kAdjLean && DIR == kDirCos2 && STAGE == kStageFine;
 
     // per-pair gradient terms (reference radiator.py:275-286 in y units)
     auto epilogue = [&](const PairGeom& pg, const Moments& M, const DetDir& dd) {
@@ -327,7 +336,28 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       gb[0] += M.T0 + M.T1 + M.T2 + M.T3 + pg.id + pg.rx;
       return;
 #endif
-      if constexpr (DIR == kDirCos2 && STAGE == kStageFine) {
+      if constexpr (kFactored) {
+        // cos^2, fine, factored: with Q = p0/2 rs, k = 2 kappa T1 and
+        // E = T0 - 2 ln2 T2 the position term of the form below is
+        //   alpha = Q id^2 D (E - 3/2 k id)   (cp c = D: cp = c or D = 0)
+        //   beta  = Q id^2 cp k
+        // and gb0 = rs/4 D k id, gb1 = Q k^3 D id T3 (Q, rs/4 applied per batch)
+        const float id = pg.id;
+        const float c = (dd.fx * pg.rx + dd.fy * pg.ry + dd.fz * pg.rz) * id;
+        const float cp = fmaxf(c, 0.0f);
+        const float D = cp * cp;
+        const float h = id * id;
+        const float k = kap2 * M.T1;
+        const float kid = k * id;
+        const float a = (D * h) * fmaf(-1.5f, kid, fmaf(-kTwoLn2, M.T2, M.T0));
+        const float b = (cp * h) * k;
+        gb[0] = fmaf(D, kid, gb[0]);
+        gb[1] = fmaf(D * id, M.T3, gb[1]);
+        gb[2] = fmaf(a, pg.rx, fmaf(b, dd.fx, gb[2]));
+        gb[3] = fmaf(a, pg.ry, fmaf(b, dd.fy, gb[3]));
+        gb[4] = fmaf(a, pg.rz, fmaf(b, dd.fz, gb[4]));
+        return;
+      } else if constexpr (DIR == kDirCos2 && STAGE == kStageFine) {
         // cos^2, fine: dD/dr = 2 cp (f - c h) / d with h = r / d, so the
         // position term w r + (base s_uG) dD/dr folds into alpha r + beta f
         // (10 fewer FP32 operations per pair than the generic form below)
@@ -382,9 +412,15 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
     };
     auto usetup = [&](const GroupDet& gd, int lo) {
       USetup u;
-      u.pg = pair_geom_fast(gd, A, B, acq);
       int jlo, jhi;
-      pair_window_cover(u.pg.kc, u.pg.phi, rho, acq, &jlo, &jhi);
+      if (kAdjLean) {
+        float kf;
+        u.pg = pair_geom_lean(gd, A, B, acq, &kf);
+        pair_window_cover_lean(kf, u.pg.phi, rho, acq, &jlo, &jhi);
+      } else {
+        u.pg = pair_geom_fast(gd, A, B, acq);
+        pair_window_cover(u.pg.kc, u.pg.phi, rho, acq, &jlo, &jhi);
+      }
       u.empty = !live || jlo > jhi;
       u.J0 = u.empty ? lo : max(jlo & ~3, lo);
       u.L = __reduce_max_sync(0xffffffffu, u.empty ? 0 : jhi - u.J0 + 1);
@@ -403,7 +439,8 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       M = {(float)(u.J0 - lo + buf), (float)u.L, 0.f, 0.f};
       return M;
 #endif
-      moments_uniform<STAGE, MASK>(seg_all[warp][buf] + (u.J0 - lo), (u.L + 3) & ~3, (float)(u.J0 * f - u.pg.kc),
+      moments_uniform<STAGE, MASK>(seg_all[warp][buf] + (u.J0 - lo), (u.L + 3) & ~3,
+                                   kAdjLean ? int_to_float(u.J0 * f - u.pg.kc) : (float)(u.J0 * f - u.pg.kc),
                                    W, u.pg.phi * sc, u.empty ? -1.0f : qmax, M);
       if (!MASK && u.empty) M = {0.f, 0.f, 0.f, 0.f};
       return M;
@@ -521,6 +558,14 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       }
     }
     __syncwarp();
+    if (kFactored) {
+      const float Q = p0h * res_sign;
+      gb[0] *= 0.25f * res_sign;
+      gb[1] *= Q * kSqrt2Ln2Cubed;
+      gb[2] *= Q;
+      gb[3] *= Q;
+      gb[4] *= Q;
+    }
 #pragma unroll
     for (int c = 0; c < 5; ++c) acc_s[warp][c][lane] += (double)gb[c];
   }

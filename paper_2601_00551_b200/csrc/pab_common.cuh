@@ -319,6 +319,60 @@ __device__ __forceinline__ PairGeom pair_geom_fast(const GroupDet& gd, const Bal
   return g;
 }
 
+// Integer rounding on the FMA / ALU pipes instead of the XU (conversion)
+// pipe, which the adjoint's moment walk keeps busy with ex2: for |x| < 2^22,
+// x + 1.5 * 2^23 rounds x to the nearest integer (ties to even, = rintf) in
+// the low mantissa bits.
+constexpr float kRoundMagic = 12582912.0f;   // 1.5 * 2^23
+constexpr int kRoundMagicBits = 0x4B400000;
+__device__ __forceinline__ int rint_to_int(float x, float* xr) {   // rintf(x) as int and as float
+  const float t = __fadd_rn(x, kRoundMagic);
+  *xr = __fadd_rn(t, -kRoundMagic);
+  return __float_as_int(t) - kRoundMagicBits;
+}
+__device__ __forceinline__ int floor_to_int(float x) {   // = __float2int_rd(x), |x| < 2^22
+  float r;
+  const int i = rint_to_int(x, &r);
+  return r > x ? i - 1 : i;
+}
+__device__ __forceinline__ int ceil_to_int(float x) {    // = __float2int_ru(x), |x| < 2^22
+  float r;
+  const int i = rint_to_int(x, &r);
+  return r < x ? i + 1 : i;
+}
+__device__ __forceinline__ float int_to_float(int i) {   // = (float)i, |i| < 2^22
+  return __fadd_rn(__int_as_float(i + kRoundMagicBits), -kRoundMagic);
+}
+
+// pair_geom_fast with the rounding of the arrival time off the XU pipe
+// (bitwise the same result); also returns kf = (float)kc
+__device__ __forceinline__ PairGeom pair_geom_lean(const GroupDet& gd, const BallA& A, const BallB& B,
+                                                   const Acq& a, float* kf) {
+  PairGeom g;
+  g.coincident = 0;
+  const float sd = gd.Sx * A.dx + gd.Sy * A.dy + gd.Sz * A.dz;
+  const float num = B.r2 - 2.0f * sd;
+  const float e1 = fmaf(num * gd.isn, gd.isn, 1.0f);
+  const float dd = (num * gd.isn) * rcp_ftz(1.0f + e1 * rsqrt_ftz(e1));
+  g.d = gd.Sn + dd;
+  const float tr = fmaf(dd, a.inv_vdt_f, gd.phg);
+  g.rx = A.dx - gd.Sx; g.ry = A.dy - gd.Sy; g.rz = A.dz - gd.Sz;
+  float kr;
+  const int ikr = rint_to_int(tr, &kr);
+  g.kc = gd.kg + ikr;
+  g.phi = tr - kr;
+  g.id = rcp_ftz(g.d);
+  *kf = int_to_float(g.kc);
+  return g;
+}
+
+// pair_window_cover without XU conversions (same result)
+__device__ __forceinline__ void pair_window_cover_lean(float kf, float phi, float rho, const Acq& a, int* jlo,
+                                                       int* jhi) {
+  *jlo = max(floor_to_int((kf + (phi - rho)) * a.inv_f), 0);
+  *jhi = min(ceil_to_int((kf + (phi + rho)) * a.inv_f), a.n_out - 1);
+}
+
 // Cover of the u- window for masked walks: jlo' <= jlo and jhi' >= jhi, each
 // off by at most one (float quotient, no exact integer correction); the
 // caller's per-sample mask |x| <= rho selects the exact support.

@@ -531,6 +531,10 @@ __device__ unsigned long long g_fwd_prof[32];
 #define PAB_FWD_DUAL 1   // warp-specialised unmasked sweeps walk two balls per lane (dual walk)
 #endif
 constexpr bool kDual = PAB_FWD_DUAL != 0;
+#ifndef PAB_FWD_WALKERS_HIGH
+#define PAB_FWD_WALKERS_HIGH 0
+#endif
+constexpr bool kWalkersHigh = PAB_FWD_WALKERS_HIGH != 0;
 
 template <int DIR, bool MASK, bool SROW, bool WS, bool DL>
 __global__ void __launch_bounds__(kMaxWarps * 32 * (WS ? 2 : 1), PAB_FWD_MINB)
@@ -581,7 +585,11 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   unsigned long long* mb_full = reinterpret_cast<unsigned long long*>(slot_h + W * kRing);
   unsigned long long* mb_empty = mb_full + W * kRing;
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // logical warp index: with PAB_FWD_WALKERS_HIGH the walkers (logical
+  // warps [0, W)) run on the physically higher warps [W, 2W), which the
+  // warp scheduler prefers when both a walker and a producer are eligible
+  const int warp = (WS && kWalkersHigh) ? (int)((threadIdx.x >> 5) + W) % (2 * W) : (int)(threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   const int tid = threadIdx.x, nthr = blockDim.x;
 
   if (WS && tid == 0) {
@@ -714,12 +722,15 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
     const int n_reg = misc[0];
     const int n_all = misc[1];
 
-    if (tid == 0) {
-      zs[W] = n_out;
-      for (int w = W - 1; w >= 0; --w) {
-        const int s = (int)(((int64_t)n_reg * w) / W), e = (int)(((int64_t)n_reg * (w + 1)) / W);
-        zs[w] = (s < e) ? ((int)gbin[sorted[s] & 0x7FFF] << kBinShift) : zs[w + 1];
+    // zone starts: the first row of each walker's slice (an empty slice takes
+    // the next non-empty one's start; slices are n_reg * w / W, n_reg <= 2^15)
+    if (tid <= W) {
+      int z = n_out;
+      for (int w = tid; w < W; ++w) {
+        const int s = n_reg * w / W, e = n_reg * (w + 1) / W;
+        if (s < e) { z = (int)gbin[sorted[s] & 0x7FFF] << kBinShift; break; }
       }
+      zs[tid] = z;
     }
     __syncthreads();
 
@@ -743,8 +754,8 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       }
     };
     if (!WS || warp < W) {
-      const int s_begin = (int)(((int64_t)n_reg * warp) / W);
-      const int s_end = (int)(((int64_t)n_reg * (warp + 1)) / W);
+      const int s_begin = n_reg * warp / W;
+      const int s_end = n_reg * (warp + 1) / W;
       const int zone_end = zs[warp + 1];
       float* my_stage = stage + warp * kTile;
       auto sink = [&](int r, float v) {
@@ -892,8 +903,8 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       // producer for walker w: pair setups, two side by side, published in
       // slice order through the ring
       const int w = warp - W;
-      const int s_begin = (int)(((int64_t)n_reg * w) / W);
-      const int s_end = (int)(((int64_t)n_reg * (w + 1)) / W);
+      const int s_begin = n_reg * w / W;
+      const int s_end = n_reg * (w + 1) / W;
       const float fs = (float)acq.f;
       auto publish = [&](int i, const PairSetup& p, int blo, int ghi) {
         const int sl = i % kRing;
