@@ -25,7 +25,9 @@
  *  - Directivity: dir_kind 0 none (reference semantics), 1 cos^p (dir_param =
  *    p), 2 square element of width dir_param metres.
  *  - Acquisition: v sound speed, t0/dt the FULL-rate grid, f the decimation
- *    factor, n_out = ceil(n_samples / f) the decimated sample count.
+ *    factor, n_out = ceil(n_samples / f) the decimated sample count;
+ *    n_out * f <= 2^21 (sample indices are rounded with FP32 magic constants
+ *    off the conversion pipe; pab_forward / pab_adjoint return 1 beyond).
  */
 #ifndef PABALL_B200_H
 #define PABALL_B200_H

@@ -440,7 +440,8 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       return M;
 #endif
       moments_uniform<STAGE, MASK>(seg_all[warp][buf] + (u.J0 - lo), (u.L + 3) & ~3,
-                                   kAdjLean ? int_to_float(u.J0 * f - u.pg.kc) : (float)(u.J0 * f - u.pg.kc),
+                                   kAdjLean ? int_to_float(u.J0 * f - u.pg.kc)
+                                                          : (float)(u.J0 * f - u.pg.kc),
                                    W, u.pg.phi * sc, u.empty ? -1.0f : qmax, M);
       if (!MASK && u.empty) M = {0.f, 0.f, 0.f, 0.f};
       return M;
@@ -667,7 +668,7 @@ int pab_adjoint(const void* rec_a, const void* rec_b, const void* group_meta, in
       dir_kind > 2)
     return 1;
   if (!rec_a || !rec_b || !group_meta || !det_pos || !det_aux || !res || !grad_partial || !status) return 1;
-  if ((int64_t)n_out * f > (1 << 24)) return 1;
+  if ((int64_t)n_out * f > kMaxRecordSamples) return 1;   // sample indices stay in the magic-rounding range
   const Acq a = make_acq(v, t0, dt, f, n_out, cutoff, dir_kind, dir_param);
   const int per_chunk = (n_det + chunks - 1) / chunks;
   const int64_t n_pad = n_groups * kWarp;

@@ -100,6 +100,38 @@ __device__ __forceinline__ float rsqrt_ftz(float x) {
   return y;
 }
 
+// Integer rounding on the FMA / ALU pipes instead of the XU (conversion)
+// pipe, which the adjoint's ex2 walk keeps busy: for |x| < 2^22,
+// x + 1.5 * 2^23 rounds x to the nearest integer (ties to even, = rintf) in
+// the low mantissa bits.  Sample indices of a record stay far inside that
+// range (n_out f <= 2^21, host-checked); a window cover computed for an
+// arrival beyond 2^22 samples (a ball ~150 m from the detector at 40 MHz)
+// comes out on the same side of the record as the arrival (the magic sum
+// stays monotonic), i.e. empty, as the exact window is.  (Measured: these
+// help the adjoint, -0.1 ms at config 2, but not the forward's setup
+// producers, which keep the conversion instructions: +0.5 ms there.)
+constexpr float kRoundMagic = 12582912.0f;   // 1.5 * 2^23
+constexpr int kRoundMagicBits = 0x4B400000;
+constexpr int kMaxRecordSamples = 1 << 21;   // full-rate samples (n_out * f), host-checked
+__device__ __forceinline__ int rint_to_int(float x, float* xr) {   // rintf(x) as int and as float
+  const float t = __fadd_rn(x, kRoundMagic);
+  *xr = __fadd_rn(t, -kRoundMagic);
+  return __float_as_int(t) - kRoundMagicBits;
+}
+__device__ __forceinline__ int floor_to_int(float x) {   // = __float2int_rd(x), |x| < 2^22
+  float r;
+  const int i = rint_to_int(x, &r);
+  return r > x ? i - 1 : i;
+}
+__device__ __forceinline__ int ceil_to_int(float x) {    // = __float2int_ru(x), |x| < 2^22
+  float r;
+  const int i = rint_to_int(x, &r);
+  return r < x ? i + 1 : i;
+}
+__device__ __forceinline__ float int_to_float(int i) {   // = (float)i, |i| < 2^22
+  return __fadd_rn(__int_as_float(i + kRoundMagicBits), -kRoundMagic);
+}
+
 struct Detector {
   double px, py, pz;
   float fx, fy, fz;   // receive direction (unit; = -outward normal)
@@ -317,31 +349,6 @@ __device__ __forceinline__ PairGeom pair_geom_fast(const GroupDet& gd, const Bal
   g.phi = tr - kr;
   g.id = rcp_ftz(g.d);
   return g;
-}
-
-// Integer rounding on the FMA / ALU pipes instead of the XU (conversion)
-// pipe, which the adjoint's moment walk keeps busy with ex2: for |x| < 2^22,
-// x + 1.5 * 2^23 rounds x to the nearest integer (ties to even, = rintf) in
-// the low mantissa bits.
-constexpr float kRoundMagic = 12582912.0f;   // 1.5 * 2^23
-constexpr int kRoundMagicBits = 0x4B400000;
-__device__ __forceinline__ int rint_to_int(float x, float* xr) {   // rintf(x) as int and as float
-  const float t = __fadd_rn(x, kRoundMagic);
-  *xr = __fadd_rn(t, -kRoundMagic);
-  return __float_as_int(t) - kRoundMagicBits;
-}
-__device__ __forceinline__ int floor_to_int(float x) {   // = __float2int_rd(x), |x| < 2^22
-  float r;
-  const int i = rint_to_int(x, &r);
-  return r > x ? i - 1 : i;
-}
-__device__ __forceinline__ int ceil_to_int(float x) {    // = __float2int_ru(x), |x| < 2^22
-  float r;
-  const int i = rint_to_int(x, &r);
-  return r < x ? i + 1 : i;
-}
-__device__ __forceinline__ float int_to_float(int i) {   // = (float)i, |i| < 2^22
-  return __fadd_rn(__int_as_float(i + kRoundMagicBits), -kRoundMagic);
 }
 
 // pair_geom_fast with the rounding of the arrival time off the XU pipe

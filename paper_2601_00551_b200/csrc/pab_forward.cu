@@ -1331,7 +1331,7 @@ int pab_forward(const void* rec_a, const void* rec_b, const void* group_meta, co
   if (f < 1 || partitions < 1 || warps < 1 || warps > kMaxWarps) return 1;
   if (!rec_a || !rec_b || !group_meta || !det_pos || !det_aux || !partial_rows || !ops_total || !status)
     return 1;
-  if ((int64_t)n_out * f > (1 << 24)) return 1;
+  if ((int64_t)n_out * f > kMaxRecordSamples) return 1;   // sample indices stay in the magic-rounding range
   const Acq acq = make_acq(v, t0, dt, f, n_out, cutoff, dir_kind, dir_param);
   // per-sample truncation test only where the walk's overrun could matter
   const bool mask = cutoff < kUnmaskedCutoff;

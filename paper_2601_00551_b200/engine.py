@@ -66,6 +66,9 @@ def sm_count(dev: torch.device) -> int:
 DIR_CODES = {"none": 0, "cos_power": 1, "element": 2}
 
 
+MAX_RECORD_SAMPLES = 1 << 21   # = kMaxRecordSamples (csrc/pab_common.cuh)
+
+
 @dataclass(frozen=True)
 class Acq:
     v: float
@@ -80,6 +83,14 @@ class Acq:
     @property
     def n_out(self) -> int:
         return -(-self.n_samples // self.f) if self.f > 1 else self.n_samples
+
+    def __post_init__(self) -> None:
+        # the kernels round sample indices with FP32 magic constants (exact
+        # below 2^22; include/paball_b200.h): records up to 2^21 full-rate
+        # samples (52 ms at 40 MHz)
+        if self.n_out * self.f > MAX_RECORD_SAMPLES:
+            raise ValueError(f"record of {self.n_out * self.f} full-rate samples exceeds the supported "
+                             f"{MAX_RECORD_SAMPLES}")
 
 
 def detector_aux(positions: np.ndarray, normals, directivity) -> np.ndarray:

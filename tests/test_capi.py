@@ -62,3 +62,22 @@ def test_bad_arguments_return_1_without_gpu(lib_path):
     assert lib.pab_pack(None, None, None, None, 10, None, None, None, None) == 1
     assert lib.pab_compact(None, 10, 0, None, None, None, None) == 1
     assert lib.pab_decimate(None, 1, 4, 0, None, None) == 1
+
+
+def test_record_length_limit(lib_path):
+    """Sample indices are rounded with FP32 magic constants (pab_common.cuh):
+    records beyond 2^21 full-rate samples are rejected at the boundary, before
+    any CUDA call, and by the host acquisition type."""
+    from paper_2601_00551_b200 import _lib
+    from paper_2601_00551_b200 import engine as E
+    lib = _lib.load(lib_path)
+    buf = (ctypes.c_double * 64)()
+    p = ctypes.cast(buf, ctypes.c_void_p)
+    n_out = (1 << 20) + 1   # x f = 2 -> 2^21 + 2 full-rate samples
+    args = (p, p, p, 1, p, p, 1, 1500.0, 0.0, 2.5e-8, 2, n_out, 6.0, 0, 0.0)
+    assert lib.pab_adjoint(*args, p, ctypes.c_float(1.0), 2, 1, 1, p, None, p, None) == 1
+    assert lib.pab_forward(p, p, p, None, 1, p, p, 1, 1500.0, 0.0, 2.5e-8, 2, n_out, 6.0, 0, 0.0, 0, 1, 1, 0,
+                           p, p, p, None) == 1
+    assert E.Acq(1500.0, 0.0, 2.5e-8, 1 << 21, 1, 6.0, 0, 0.0).n_out == 1 << 21
+    with pytest.raises(ValueError, match="exceeds"):
+        E.Acq(1500.0, 0.0, 2.5e-8, (1 << 21) + 1, 1, 6.0, 0, 0.0)
