@@ -207,10 +207,13 @@ class DeviceCloud:
             return
         ws = workspace(self.dev)
         lib = _lib.load()
-        bounds = ws.get("cloud_bounds", 8, torch.float64)
-        bws = ws.get("cloud_bounds_ws", int(lib.pab_cloud_bounds_workspace_bytes()) // 8 + 1, torch.float64)
-        keys = ws.get("sort_keys", n, torch.int64)
-        sws = ws.get("sort_ws", int(lib.pab_sort_perm_workspace_bytes(n)) // 8 + 1, torch.int64)
+        # scratch per bucket count: the forward's and the adjoint's packings
+        # of one cloud may sort concurrently on two streams (_run_model)
+        b = self.buckets
+        bounds = ws.get(f"cloud_bounds{b}", 8, torch.float64)
+        bws = ws.get(f"cloud_bounds_ws{b}", int(lib.pab_cloud_bounds_workspace_bytes()) // 8 + 1, torch.float64)
+        keys = ws.get(f"sort_keys{b}", n, torch.int64)
+        sws = ws.get(f"sort_ws{b}", int(lib.pab_sort_perm_workspace_bytes(n)) // 8 + 1, torch.int64)
         self.perm = torch.empty(n, dtype=torch.int32, device=self.dev)
         call("pab_cloud_bounds", ptr(self.pos), ptr(self.a0), n, ptr(bounds), ptr(bws), _stream())
         call("pab_sort_keys", ptr(self.pos), ptr(self.a0), n, ptr(bounds), self.buckets, ptr(keys), _stream())
@@ -232,6 +235,22 @@ class DeviceCloud:
             call("pab_pack", ptr(self.pos), ptr(self.p0), ptr(self.a0), ptr(self.slots), self.slots.numel(),
                  ptr(self.rec_a), ptr(self.rec_b), ptr(self.gmeta), _stream())
         self._packed = True
+
+    def pack_async(self, stream: torch.cuda.Stream) -> torch.cuda.Event:
+        """Sort and pack on ``stream`` (after the work queued so far on the
+        current stream, e.g. the cloud upload); returns the event the
+        consumer's stream waits on.  The packed tensors are marked as used by
+        the current stream too (caching-allocator safety)."""
+        main = torch.cuda.current_stream(self.dev)
+        stream.wait_stream(main)
+        with torch.cuda.stream(stream):
+            self.pack()
+        for t in (self.perm, self.rec_a, self.rec_b, self.gmeta):
+            if t is not None:
+                t.record_stream(main)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        return ev
 
     def pair_table(self) -> torch.Tensor:
         """Dual-walk pairing table: which two balls of a 64-ball unit a lane

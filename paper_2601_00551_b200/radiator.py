@@ -238,7 +238,12 @@ def device_supervision(data: np.ndarray, det: E.DeviceDetectors, defer: bool = F
     dev = det.pos.device
     main = torch.cuda.current_stream(dev)
     side = _side_stream(dev)
-    side.wait_stream(main)
+    # no side.wait_stream(main): the copy writes a fresh buffer of the side
+    # stream's pool (freed only after main's uses, record_stream below) from
+    # a staging slot whose previous DMA the stager waits for, so nothing
+    # orders it after the work already queued on main -- the forward kernel
+    # queued just before this call (round-2 profile: waiting for it left the
+    # 0.3 ms DMA unhidden after the forward)
     (t,), ev = hostio.stager("supervision").upload([(data[det.lo:det.hi], torch.float32)], dev, stream=side)
     t.record_stream(main)
     if defer:
@@ -281,8 +286,15 @@ def _run_model(cloud, ctx, f, real=None, stage="fine"):
     # staged and uploaded only once the forward kernel is queued, so the host
     # copy and its DMA overlap the simulation (the residual waits for it)
     dc = E.DeviceCloud.from_host(cloud.positions, cloud.p0, a0, dev)
+    adj_ready = None
     if need_grad:
         real_local = lambda: device_supervision(real.data, det, defer=True)   # noqa: E731
+        # the adjoint's own packing (its radius buckets: a second sort) on a
+        # side stream, overlapping the forward's sort, packing, coincidence
+        # test and pairing table instead of following the forward
+        adj = dc.adjoint_cloud()
+        if adj is not dc and n > 0:
+            adj_ready = adj.pack_async(_side_stream(dev))
     counters = E.PassCounters(dev)
     if not need_grad:
         local, _ = E.forward_rows(dc, det, acq, counters)
@@ -294,6 +306,8 @@ def _run_model(cloud, ctx, f, real=None, stage="fine"):
     stage_code = 2 if stage == "fine" else 1
     n_total = det.n_total * n_out
     flat = torch.empty(5 * n + E.TAIL, dtype=torch.float64, device=dev)
+    if adj_ready is not None:
+        torch.cuda.current_stream(dev).wait_event(adj_ready)
     # gradients, loss, error flags and op count in one buffer: one
     # all-reduce over detector shards, one copy into page-locked host memory
     # (the returned arrays are views that keep it alive)
