@@ -111,6 +111,10 @@ int pab_pair_table(const void* rec_a, const void* group_meta, int64_t n_groups, 
 
 /* Forward model: partial_rows[partitions][n_det][n_out] (FP32) for the given
  * detector set.  ops_total += in-window samples (the reference op counter).
+ * `wide_list` (device, partitions * n_det * (wide_cap + 1) ints) is scratch
+ * through which the sweep hands the groups wider than its tile to a second
+ * kernel (per detector x partition: a count, then up to wide_cap group
+ * indices; a larger count makes that kernel find them again itself).
  * `warps` = walker warps per CTA (the CTA also runs as many setup-producer
  * warps); `groups_per_cell` and `tile_rows` are reserved (ignored: the tile
  * height is a build constant).  `pair_table` (nullable) enables the dual
@@ -122,7 +126,8 @@ int pab_forward(const void* rec_a, const void* rec_b, const void* group_meta, co
                 const double* det_pos /*[n_det][3]*/, const double* det_aux /*[n_det][9]*/, int n_det,
                 double v, double t0, double dt, int f, int n_out, double cutoff, int dir_kind,
                 double dir_param, int groups_per_cell, int partitions, int warps, int tile_rows,
-                float* partial_rows, unsigned long long* ops_total, int* status, void* stream);
+                float* partial_rows, int* wide_list, int wide_cap, unsigned long long* ops_total, int* status,
+                void* stream);
 
 /* Sum forward partitions; with `real` (nullable) write res = sim - real and
  * per-detector FP64 sum of squares to loss_rows, else write sim.

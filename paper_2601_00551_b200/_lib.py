@@ -30,7 +30,7 @@ _SIGS = {
     "pab_pair_table_bytes": ([_i64], C.c_size_t),
     "pab_pair_table": ([_vp, _vp, _i64, _vp, _vp], _i),
     "pab_forward": ([_vp, _vp, _vp, _vp, _i64, _vp, _vp, _i, _d, _d, _d, _i, _i, _d, _i, _d, _i, _i, _i, _i,
-                     _vp, _vp, _vp, _vp], _i),
+                     _vp, _vp, _i, _vp, _vp, _vp], _i),
     "pab_residual": ([_vp, _i, _i, _i, _vp, _vp, _vp, _vp], _i),
     "pab_adjoint": ([_vp, _vp, _vp, _i64, _vp, _vp, _i, _d, _d, _d, _i, _i, _d, _i, _d, _vp, _f, _i, _i, _i,
                      _vp, _vp, _vp, _vp], _i),

@@ -208,6 +208,69 @@ template <bool MASK>
 __device__ __forceinline__ void rmw_walk(float* tile, int lane, int J0, int L, int lim, float mf, float fs,
                                          const Walk& w);
 
+// Walk with the amplitude as a factor (phase F): Ak y G with Ak folded into
+// a second set of y coefficients (ya = m Ak nsc + Ak c ~ Ak y), so doubling
+// Ak doubles every term exactly -- p0 linearity stays bitwise, as in the
+// reference's amp * u * G (radiator.py:249-251) -- for one more FP32x2
+// operation per sample pair than the exponent-folded walk.
+struct AWalk {
+  float2 nsc2, c0, c1, c2, c3;   // y = m nsc + c
+  float2 an2, a0, a1, a2, a3;    // Ak-scaled coefficients
+  float qmax;
+};
+__device__ __forceinline__ AWalk make_awalk(float nsc, float pss, float fs, float Ak, float qmax) {
+  AWalk w;
+  w.nsc2 = make_float2(nsc, nsc);
+  const float dl = fs * nsc, dl2 = 2.0f * dl;
+  w.c0 = make_float2(pss, pss + dl);
+  w.c1 = __fadd2_rn(w.c0, make_float2(dl2, dl2));
+  w.c2 = __fadd2_rn(w.c1, make_float2(dl2, dl2));
+  w.c3 = __fadd2_rn(w.c2, make_float2(dl2, dl2));
+  const float2 A2 = make_float2(Ak, Ak);
+  w.an2 = __fmul2_rn(A2, w.nsc2);
+  w.a0 = __fmul2_rn(A2, w.c0);
+  w.a1 = __fmul2_rn(A2, w.c1);
+  w.a2 = __fmul2_rn(A2, w.c2);
+  w.a3 = __fmul2_rn(A2, w.c3);
+  w.qmax = qmax;
+  return w;
+}
+template <bool MASK>
+__device__ __forceinline__ float2 rmw_pair_amp(float2 o, float2 m2, float2 c, float2 a, const AWalk& w) {
+  const float2 y = __ffma2_rn(m2, w.nsc2, c);
+  const float2 ya = __ffma2_rn(m2, w.an2, a);
+  const float2 q = __fmul2_rn(y, y);
+  const float2 g = gauss2<MASK>(q, w.qmax);
+  return __ffma2_rn(ya, g, o);
+}
+// L a multiple of 8 from an 8-aligned J0 (blocks never wrap the circular
+// tile); blocks starting past `lim` go to the dump block
+template <bool MASK>
+__device__ __forceinline__ void rmw_walk_amp(float* tile, int lane, int J0, int L, int lim, float mf, float fs,
+                                             const AWalk& w) {
+  float4* const T = reinterpret_cast<float4*>(tile) + lane;
+  const int dump = kTile / 4;
+  const float step = 8.0f * fs;
+  int q = (J0 % kTile) >> 2;
+  PAB_CHECK((J0 & 7) == 0 && (L & 7) == 0);
+#pragma unroll 1
+  for (int Jb = J0; Jb < J0 + L; Jb += 8, mf += step) {
+    const bool live = Jb <= lim;
+    const int qa = live ? q : dump;
+    PAB_CHECK(qa >= 0 && qa + 1 <= dump + 1);
+    const float2 m2 = make_float2(mf, mf);
+    float4 o0 = T[qa * kWarp], o1 = T[(qa + 1) * kWarp];
+    const float2 p0 = rmw_pair_amp<MASK>(make_float2(o0.x, o0.y), m2, w.c0, w.a0, w);
+    const float2 p1 = rmw_pair_amp<MASK>(make_float2(o0.z, o0.w), m2, w.c1, w.a1, w);
+    const float2 p2 = rmw_pair_amp<MASK>(make_float2(o1.x, o1.y), m2, w.c2, w.a2, w);
+    const float2 p3 = rmw_pair_amp<MASK>(make_float2(o1.z, o1.w), m2, w.c3, w.a3, w);
+    T[qa * kWarp] = make_float4(p0.x, p0.y, p1.x, p1.y);
+    T[(qa + 1) * kWarp] = make_float4(p2.x, p2.y, p3.x, p3.y);
+    q += 2;
+    if (q >= kTile / 4) q -= kTile / 4;
+  }
+}
+
 template <bool MASK>
 __device__ __forceinline__ void rmw_uniform(float* tile, int lane, int J0, int L, int lim, float mf, float fs,
                                             float sc, float ps, float Ak, float qmax) {
@@ -513,6 +576,220 @@ __device__ __forceinline__ void evaluate_pair(float* tile, int lane, const Acq& 
     rmw_window(tile, lane, max(nlo, clip_lo), min(nhi, clip_hi), nkc, acq.f, -sc, nphi, Ak);
 }
 
+// Groups wider than the tile (phase F of the sweep: rare in dense clouds, a
+// quarter of the groups of a sparse filtered cloud), in their own kernel
+// after the sweep: grid = detectors x partitions as forward_kernel, 4 warps
+// with a tile each.  Per chunk of the partition the wide groups are found by
+// the sweep's own criterion (bin_of: span beyond the tile, detector within
+// two group radii, u+ window possible), listed in order, and added to the
+// partition's row: the union of their sample ranges is split into one
+// 8-aligned time range per warp (the warps never write the same row: no
+// races, a fixed per-row order); a warp sweeps its range in tile-aligned
+// pieces, per piece every wide group that reaches it is set up (lane-parallel
+// group geometry for 32 groups, then per pair: FP64 geometry near the
+// detector, exact windows, weight) and walked with the vectorised walk from
+// 8-aligned starts clipped to the piece (blocks never straddle a piece or a
+// warp range, the amplitude as a factor: p0 linearity stays bitwise), and
+// the piece is flushed once.  (Round 2 v2 ran this inside the sweep kernel,
+// one warp-uniform group at a time with scalar per-sample walks while the
+// setup warps idled at the barrier: 68 % of the f = 1 forward of the config-3
+// reconstruction; kept inside the sweep kernel the new code cost config 2
+// +0.5 ms through the sweep's register allocation.)
+#ifndef PAB_FWD_WS
+#define PAB_FWD_WS 1   // warp-specialised sweep (setup producers + walkers)
+#endif
+constexpr bool kWS = PAB_FWD_WS != 0;
+
+// An entry (a group, or a dual pair's union) sweeps only if its rows
+// [blo, hi + 7] (4-aligned starts, the last block may run 7 rows past the
+// window) fit the live tile and its pairs take the fast geometry; groups
+// close to the detector (FP64 per-pair geometry) and, warp-specialised,
+// groups that may have a u+ window go to the wide-group kernel too.
+__device__ __forceinline__ bool wide_entry(int l, int h, bool slow, bool near) {
+  const int blo = l & ~((1 << kBinShift) - 1);
+  return h + 7 - blo + 1 > kTile || slow || near;
+}
+
+constexpr int kWideChunk = 4096;   // groups scanned per pass (u8 flags + u16 list in shared memory)
+constexpr int kWideWarps = 4;
+
+// The wide groups of one detector x partition CTA, given by gidx(i) (global
+// group index, i < n_wide, in a fixed order), added to the partition's row.
+template <int DIR, bool MASK, class GIdx>
+__device__ __forceinline__ void wide_pass(float* tile, int lane, int warp, const Acq& acq, const Detector& det,
+                                          const DetDir& dd, const GroupMeta* __restrict__ gmeta,
+                                          const BallA* __restrict__ ra, const BallB* __restrict__ rb, int n_wide,
+                                          GIdx gidx, float* row, unsigned long long& my_ops, int& coinc) {
+  constexpr int W = kWideWarps;
+  const int n_out = acq.n_out;
+  int umin = INT_MAX, umax = INT_MIN;   // union of the wide groups' ranges (every warp alike)
+  for (int i0 = 0; i0 < n_wide; i0 += kWarp) {
+    int lo = INT_MAX, hi = INT_MIN;
+    if (i0 + lane < n_wide) {
+      const GroupMeta gm = gmeta[gidx(i0 + lane)];
+      const GroupDet gd = group_det(gm, det.px, det.py, det.pz, acq);
+      group_range(acq, gd, gm, &lo, &hi);
+    }
+    umin = min(umin, __reduce_min_sync(0xffffffffu, lo));
+    umax = max(umax, __reduce_max_sync(0xffffffffu, hi));
+  }
+  const int ub = umin & ~7;
+  const int nblk = ((umax - ub) >> 3) + 1;   // 8-row blocks of the union
+  const int t0 = ub + 8 * (int)(((int64_t)nblk * warp) / W), t1 = ub + 8 * (int)(((int64_t)nblk * (warp + 1)) / W);
+  const float fs = (float)acq.f;
+  for (int P = t0 - t0 % kTile; P < t1; P += kTile) {   // tile-aligned pieces of [t0, t1)
+    const int c0 = max(P, t0), c1 = min(P + kTile, t1) - 1;   // c0 = 0 mod 8, c1 = 7 mod 8
+    int rlo = INT_MAX, rhi = INT_MIN;   // rows the piece's walks wrote (warp-uniform)
+    for (int i0 = 0; i0 < n_wide; i0 += kWarp) {
+      const int nbat = min(kWarp, n_wide - i0);
+      GroupDet gd_l = empty_gd();
+      int lo_l = 1, hi_l = 0, near_l = 0;
+      int64_t g_l = 0;
+      if (lane < nbat) {
+        g_l = gidx(i0 + lane);
+        const GroupMeta gm = gmeta[g_l];
+        gd_l = group_det(gm, det.px, det.py, det.pz, acq);
+        group_range(acq, gd_l, gm, &lo_l, &hi_l);
+        near_l = group_near(acq, gd_l, gm) ? 1 : 0;
+      }
+      unsigned todo = __ballot_sync(0xffffffffu, lane < nbat && lo_l <= c1 && hi_l >= c0);
+      while (todo) {
+        const int k = __ffs(todo) - 1;
+        todo &= todo - 1;
+        GroupDet gd = shfl_gd_fast(gd_l, k);
+        gd.slow = __shfl_sync(0xffffffffu, gd_l.slow, k);
+        const int64_t g = __shfl_sync(0xffffffffu, g_l, k);
+        const int glo = __shfl_sync(0xffffffffu, lo_l, k);
+        const int near = __shfl_sync(0xffffffffu, near_l, k);
+        const GroupMeta gm = gmeta[g];
+        const BallA A = ra[g * kWarp + lane];
+        const BallB B = rb[g * kWarp + lane];
+        const PairGeom pg = pair_geom(gd, gm, det.px, det.py, det.pz, A, B, acq);
+        coinc |= pg.coincident;
+        const bool live = B.orig >= 0;
+        const float rho = acq.cutoff * A.a0 * acq.inv_vdt_f;
+        const float sc = acq.vdt_f * kSqrtHalfLog2e * B.inv_a0;
+        const float qmax = (rho * sc) * (rho * sc);
+        int jlo = 1, jhi = 0, nlo = 1, nhi = 0, nkc = 0;
+        float nphi = 0.0f;
+        if (live) {
+          pair_window(pg.kc, pg.phi, rho, acq, &jlo, &jhi);
+          if (near) pair_near_window(pg.d, rho, acq, &nlo, &nhi, &nkc, &nphi);
+        }
+        if (glo >= c0 && glo <= c1)   // counted once: the piece of the warp range holding the group's first row
+          my_ops += (unsigned long long)(max(jhi - jlo + 1, 0) + max(nhi - nlo + 1, 0));
+        float D = 1.0f;
+        if (DIR != kDirNone)
+          D = dir_weight<DIR, false>(dd, pg.rx * pg.id, pg.ry * pg.id, pg.rz * pg.id, pg.id, acq.dir_param,
+                                     acq.dir_param, B.inv_a0, nullptr, nullptr);
+        const float Ak = (0.5f * B.p0 * D) * pg.id * (A.a0 * kSqrt2Ln2);
+        // one window clipped to the piece: 8-aligned start >= c0, live
+        // blocks start <= the clipped end (<= c1, so they end <= c1)
+        auto clip_walk = [&](int wlo, int whi, int kc, float s, float ph) {
+          const int a = max(wlo, c0), b = min(whi, c1);
+          const bool empty = a > b;
+          const int J0 = empty ? c0 : (a & ~7);
+          const int L = __reduce_max_sync(0xffffffffu, empty ? 0 : b - J0 + 1);
+          if (L > 0) {
+            rlo = min(rlo, __reduce_min_sync(0xffffffffu, empty ? INT_MAX : J0));
+            rhi = max(rhi, __reduce_max_sync(0xffffffffu, empty ? INT_MIN : (b | 7)));
+          }
+          if (L > 0)
+            rmw_walk_amp<MASK>(tile, lane, J0, (L + 7) & ~7, empty ? -1 : b, (float)(J0 * acq.f - kc), fs,
+                               make_awalk(-s, ph * s, fs, empty ? 0.0f : Ak, qmax));
+        };
+        clip_walk(jlo, jhi, pg.kc, sc, pg.phi);
+        if (__any_sync(0xffffffffu, nlo <= nhi)) clip_walk(nlo, nhi, nkc, -sc, nphi);   // u+ = -kappa y
+        __syncwarp();
+      }
+    }
+    if (rlo <= rhi)   // only the rows the walks wrote (a piece may see no wide group)
+      flush_rows(tile, lane, rlo, min(rhi + 1, n_out), [&](int r, float v) { row[r] += v; });
+  }
+  // walked blocks past the signal end (rows >= n_out) are never flushed
+  for (int i = lane; i < kTile * kWarp / 4; i += kWarp)
+    reinterpret_cast<float4*>(tile)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  __syncwarp();
+}
+
+template <int DIR, bool MASK>
+__global__ void __launch_bounds__(kWideWarps * 32, 2)
+forward_wide_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb, const GroupMeta* __restrict__ gmeta,
+                    int64_t n_groups, const double* __restrict__ det_pos, const double* __restrict__ det_aux,
+                    int n_det, Acq acq, int64_t groups_per_part, float* __restrict__ partial_rows,
+                    const int* __restrict__ wide_list, int wide_cap, unsigned long long* __restrict__ ops_total,
+                    int* __restrict__ status) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int W = kWideWarps;
+  const int j = blockIdx.x;
+  const int part = blockIdx.y;
+  // the sweep listed this CTA's wide groups (count, then up to wide_cap
+  // global group indices in its sort order): nothing to do for most CTAs
+  const int* list = wide_list + ((size_t)part * n_det + j) * (size_t)(wide_cap + 1);
+  const int count = list[0];
+  if (count == 0) return;
+  float* tiles = reinterpret_cast<float*>(smem_raw);
+  unsigned char* flag = smem_raw + (size_t)W * kTileAlloc * kWarp * sizeof(float);
+  unsigned short* wide = reinterpret_cast<unsigned short*>(flag + kWideChunk);
+  __shared__ int n_wide_s;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  const int n_out = acq.n_out;
+  float* row = partial_rows + ((size_t)part * n_det + j) * (size_t)n_out;
+  float* tile = tiles + (size_t)warp * kTileAlloc * kWarp;
+  for (int i = tid; i < W * kTileAlloc * kWarp; i += blockDim.x) tiles[i] = 0.0f;
+  __syncthreads();
+  const Detector det = load_detector(det_pos, det_aux, j);
+  DetDir dd{};
+  if (DIR != kDirNone) dd = load_detdir(det_aux, j);
+  unsigned long long my_ops = 0;
+  int coinc = 0;
+  if (count <= wide_cap) {
+    wide_pass<DIR, MASK>(tile, lane, warp, acq, det, dd, gmeta, ra, rb, count,
+                         [&](int i) -> int64_t { return list[1 + i]; }, row, my_ops, coinc);
+  } else {
+    // list overflow: find them again, chunk by chunk, with the sweep's
+    // phase-A criterion (the same functions: the same groups)
+    const int64_t g_begin = (int64_t)part * groups_per_part;
+    const int64_t g_end = min(n_groups, g_begin + groups_per_part);
+    for (int64_t cg0 = g_begin; cg0 < g_end; cg0 += kWideChunk) {
+      const int cgn = (int)min((int64_t)kWideChunk, g_end - cg0);
+      for (int gl = tid; gl < cgn; gl += blockDim.x) {
+        const GroupMeta gm = gmeta[cg0 + gl];
+        const GroupDet gd = group_det(gm, det.px, det.py, det.pz, acq);
+        int lo, hi;
+        group_range(acq, gd, gm, &lo, &hi);
+        const bool nr = kWS && group_near(acq, gd, gm);
+        flag[gl] = (lo <= hi && wide_entry(lo, hi, gd.slow != 0, nr)) ? 1 : 0;
+      }
+      __syncthreads();
+      if (warp == 0) {   // ordered compaction
+        int n = 0;
+        for (int b0 = 0; b0 < cgn; b0 += kWarp) {
+          const bool f = b0 + lane < cgn && flag[b0 + lane];
+          const unsigned m = __ballot_sync(0xffffffffu, f);
+          if (f) wide[n + __popc(m & ((1u << lane) - 1u))] = (unsigned short)(b0 + lane);
+          n += __popc(m);
+        }
+        if (lane == 0) n_wide_s = n;
+      }
+      __syncthreads();
+      const int n_wide = n_wide_s;
+      if (n_wide > 0)
+        wide_pass<DIR, MASK>(tile, lane, warp, acq, det, dd, gmeta, ra, rb, n_wide,
+                             [&](int i) -> int64_t { return cg0 + wide[i]; }, row, my_ops, coinc);
+      __syncthreads();   // flags / list reused by the next chunk
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    my_ops += __shfl_xor_sync(0xffffffffu, my_ops, o);
+    coinc |= __shfl_xor_sync(0xffffffffu, coinc, o);
+  }
+  if (lane == 0) {
+    if (my_ops) atomicAdd(ops_total, my_ops);
+    if (coinc) atomicOr(status, kStatusCoincident);
+  }
+}
+
 #ifndef PAB_FWD_MINB
 #define PAB_FWD_MINB 2
 #endif
@@ -541,8 +818,8 @@ __global__ void __launch_bounds__(kMaxWarps * 32 * (WS ? 2 : 1), PAB_FWD_MINB)
 forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
                const GroupMeta* __restrict__ gmeta, const unsigned char* __restrict__ ptab, int64_t n_groups,
                const double* __restrict__ det_pos, const double* __restrict__ det_aux, int n_det,
-               Acq acq, int64_t groups_per_part, float* __restrict__ partial_rows,
-               unsigned long long* __restrict__ ops_total, int* __restrict__ status) {
+               Acq acq, int64_t groups_per_part, float* __restrict__ partial_rows, int* __restrict__ wide_list,
+               int wide_cap, unsigned long long* __restrict__ ops_total, int* __restrict__ status) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // WS: warps [0, W) walk (one tile each), warps [W, 2W) compute the pair
   // setups of walker (warp - W)'s slice and hand them over through a
@@ -613,6 +890,8 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   const int64_t g_end = min(n_groups, g_begin + groups_per_part);
   unsigned long long my_ops = 0;
   int coinc = 0;
+  int* const wide_out = wide_list + ((size_t)part * n_det + j) * (size_t)(wide_cap + 1);
+  int wide_count = 0;   // wide entries of this CTA (all chunks)
 
 #ifdef PAB_FWD_PROF
   long long pw_wait = 0, pw_room = 0, pw_walk = 0, pp_setup = 0, pp_pub = 0, pp_geo = 0, pw_lanes = 0, pw_groups = 0;
@@ -649,9 +928,7 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       // the hand-off carries the u- walk only)
       auto bin_of = [&](int l, int h, bool sl, bool n) -> unsigned short {
         if (l > h) return kEmptyBin;
-        const int blo = l & ~((1 << kBinShift) - 1);
-        const bool wide = h + 7 - blo + 1 > kTile;
-        return (wide || sl || n) ? (unsigned short)n_bins : (unsigned short)(l >> kBinShift);
+        return wide_entry(l, h, sl, n) ? (unsigned short)n_bins : (unsigned short)(l >> kBinShift);
       };
       if (DUAL && kUG * gl + 1 < cgn && lo[0] <= hi[0] && lo[kUG - 1] <= hi[kUG - 1]) {
         const unsigned short b = bin_of(min(lo[0], lo[kUG - 1]), max(hi[0], hi[kUG - 1]),
@@ -720,7 +997,14 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
     PROF_T(t_d);
 
     const int n_reg = misc[0];
-    const int n_all = misc[1];
+    {   // the wide entries sorted[n_reg, misc[1]) (single groups) go to forward_wide_kernel's list
+      const int n_all = misc[1];
+      for (int i = n_reg + tid; i < n_all; i += nthr) {
+        const int k = wide_count + (i - n_reg);
+        if (k < wide_cap) wide_out[1 + k] = (int)(cg0 + (sorted[i] & 0x7FFF));
+      }
+      wide_count += n_all - n_reg;
+    }
 
     // zone starts: the first row of each walker's slice (an empty slice takes
     // the next non-empty one's start; slices are n_reg * w / W, n_reg <= 2^15)
@@ -1147,55 +1431,8 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
     }
 
     PROF_ADD(pslot + 5, t_e2);
-    PROF_T(t_f);
-    // ---- F: groups wider than the tile (rare in dense clouds; a quarter of
-    // the groups of a sparse filtered cloud): linear passes.  The union of
-    // their sample ranges is split into one time range per walker warp, so
-    // the warps never write the same row (no races, a fixed per-row order)
-    // and share the work (a serial warp 0 left 7 of 8 warps at the barrier:
-    // 71 % of the stall samples of a config-3 f = 1 forward) ----
-    if (warp < W && n_all > n_reg) {
-      auto range_of = [&](int idx, GroupMeta& gm, GroupDet& gd, int& lo, int& hi) {
-        gm = gmeta[cg0 + (sorted[idx] & 0x7FFF)];
-        gd = group_det(gm, det.px, det.py, det.pz, acq);
-        group_range(acq, gd, gm, &lo, &hi);
-      };
-      int umin = INT_MAX, umax = INT_MIN;   // union of the wide groups' ranges (every warp alike)
-      for (int i0 = n_reg; i0 < n_all; i0 += kWarp) {
-        int lo = INT_MAX, hi = INT_MIN;
-        if (i0 + lane < n_all) {
-          GroupMeta gm;
-          GroupDet gd;
-          range_of(i0 + lane, gm, gd, lo, hi);
-        }
-        umin = min(umin, __reduce_min_sync(0xffffffffu, lo));
-        umax = max(umax, __reduce_max_sync(0xffffffffu, hi));
-      }
-      const int64_t span = (int64_t)umax - umin + 1;
-      const int t0 = umin + (int)((span * warp) / W), t1 = umin + (int)((span * (warp + 1)) / W);
-      for (int idx = n_reg; idx < n_all; ++idx) {   // single groups only (a dual entry always fits)
-        GroupMeta gm;
-        GroupDet gd;
-        int lo, hi;
-        range_of(idx, gm, gd, lo, hi);
-        const int a = max(lo, t0), b = min(hi, t1 - 1);
-        if (a > b) continue;
-        const int64_t g = cg0 + (sorted[idx] & 0x7FFF);
-        const BallA A = ra[g * kWarp + lane];
-        const BallB B = rb[g * kWarp + lane];
-        const int near = group_near(acq, gd, gm) ? 1 : 0;
-        for (int base = a - a % kTile; base <= b; base += kTile) {
-          const int c0 = max(base, a), c1 = min(base + kTile - 1, b);
-          unsigned long long ops_once = 0;
-          evaluate_pair<DIR>(tile, lane, acq, gd, gm, det, dd, A, B, near, ops_once, coinc, c0, c1);
-          if (c0 == lo) my_ops += ops_once;   // counted once, by the warp whose range holds the group's first row
-          __syncwarp();
-          flush_rows(tile, lane, c0, c1 + 1, [&](int r, float v) { row[r] += v; });
-        }
-      }
-    }
-    __syncthreads();
-    PROF_ADD(pslot + 7, t_f);
+    // ---- F: groups wider than the tile (bin n_bins) are left out of the
+    // sweep; forward_wide_kernel adds them afterwards ----
   }
 #ifdef PAB_FWD_PROF
   if (lane == 0) {
@@ -1214,6 +1451,7 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
     float* out = partial_rows + ((size_t)part * n_det + j) * (size_t)n_out;
     for (int i = tid; i < n_out; i += nthr) out[i] = row[i];
   }
+  if (tid == 0) wide_out[0] = wide_count;   // > wide_cap: forward_wide_kernel finds them again
   for (int o = 16; o > 0; o >>= 1) {
     my_ops += __shfl_xor_sync(0xffffffffu, my_ops, o);
     coinc |= __shfl_xor_sync(0xffffffffu, coinc, o);
@@ -1286,10 +1524,6 @@ __global__ void decimate_kernel(const float* __restrict__ src, int n_rows, int n
   dst[i] = src[r * n_in + k * f];
 }
 
-#ifndef PAB_FWD_WS
-#define PAB_FWD_WS 1   // warp-specialised sweep (setup producers + walkers)
-#endif
-constexpr bool kWS = PAB_FWD_WS != 0;
 
 size_t forward_smem(int n_out, int warps, bool srow, bool dual) {
   const size_t n_bins = (size_t)((n_out + (1 << kBinShift) - 1) >> kBinShift);
@@ -1323,13 +1557,14 @@ int pab_forward(const void* rec_a, const void* rec_b, const void* group_meta, co
                 int64_t n_groups,
                 const double* det_pos, const double* det_aux, int n_det, double v, double t0, double dt,
                 int f, int n_out, double cutoff, int dir_kind, double dir_param, int groups_per_cell,
-                int partitions, int warps, int tile_rows, float* partial_rows,
+                int partitions, int warps, int tile_rows, float* partial_rows, int* wide_list, int wide_cap,
                 unsigned long long* ops_total, int* status, void* stream) {
   (void)groups_per_cell;
   (void)tile_rows;
   if (n_det <= 0 || n_out <= 0) return 0;
   if (f < 1 || partitions < 1 || warps < 1 || warps > kMaxWarps) return 1;
-  if (!rec_a || !rec_b || !group_meta || !det_pos || !det_aux || !partial_rows || !ops_total || !status)
+  if (!rec_a || !rec_b || !group_meta || !det_pos || !det_aux || !partial_rows || !wide_list || wide_cap < 0 ||
+      !ops_total || !status)
     return 1;
   if ((int64_t)n_out * f > kMaxRecordSamples) return 1;   // sample indices stay in the magic-rounding range
   const Acq acq = make_acq(v, t0, dt, f, n_out, cutoff, dir_kind, dir_param);
@@ -1350,7 +1585,7 @@ int pab_forward(const void* rec_a, const void* rec_b, const void* group_meta, co
     cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     kernel<<<grid, warps * kWarp * (kWS ? 2 : 1), smem, (cudaStream_t)stream>>>(
         (const BallA*)rec_a, (const BallB*)rec_b, (const GroupMeta*)group_meta, pair_table, n_groups, det_pos, det_aux,
-        n_det, acq, per_part, partial_rows, ops_total, status);
+        n_det, acq, per_part, partial_rows, wide_list, wide_cap, ops_total, status);
   };
   auto by_row = [&](auto k_srow, auto k_grow) { srow ? launch(k_srow) : launch(k_grow); };
   auto by_mask = [&](auto km_s, auto km_g, auto ku_s, auto ku_g, auto kd_s, auto kd_g) {
@@ -1365,6 +1600,20 @@ int pab_forward(const void* rec_a, const void* rec_b, const void* group_meta, co
   else if (dir_kind == kDirCosPower) PAB_FWD_VARIANTS(kDirCosPower);
   else PAB_FWD_VARIANTS(kDirElement);
 #undef PAB_FWD_VARIANTS
+  // groups wider than the tile, added to the same partition rows afterwards
+  const size_t wsmem = (size_t)kWideWarps * kTileAlloc * kWarp * sizeof(float) + 3 * (size_t)kWideChunk;
+  auto launch_wide = [&](auto kernel) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem);
+    kernel<<<grid, kWideWarps * kWarp, wsmem, (cudaStream_t)stream>>>(
+        (const BallA*)rec_a, (const BallB*)rec_b, (const GroupMeta*)group_meta, n_groups, det_pos, det_aux, n_det,
+        acq, per_part, partial_rows, wide_list, wide_cap, ops_total, status);
+  };
+#define PAB_FWD_WIDE(D) mask ? launch_wide(forward_wide_kernel<D, true>) : launch_wide(forward_wide_kernel<D, false>)
+  if (dir_kind == kDirNone) PAB_FWD_WIDE(kDirNone);
+  else if (dir_kind == kDirCosPower && dir_param == 2.0) PAB_FWD_WIDE(kDirCos2);
+  else if (dir_kind == kDirCosPower) PAB_FWD_WIDE(kDirCosPower);
+  else PAB_FWD_WIDE(kDirElement);
+#undef PAB_FWD_WIDE
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 

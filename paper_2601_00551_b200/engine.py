@@ -67,6 +67,9 @@ DIR_CODES = {"none": 0, "cos_power": 1, "element": 2}
 
 
 MAX_RECORD_SAMPLES = 1 << 21   # = kMaxRecordSamples (csrc/pab_common.cuh)
+# groups wider than the forward's tile listed per detector x partition for the
+# wide-group kernel (more: it scans for them itself); 1 KB per CTA
+WIDE_CAP = int(os.environ.get("PAB_WIDE_CAP", "255"))
 
 
 @dataclass(frozen=True)
@@ -459,11 +462,12 @@ def forward_rows(cloud: DeviceCloud, det: DeviceDetectors, acq: Acq, counters: P
         # walks at f >= 2 are 2 % faster; windows of 8-17 samples); PAB_FORWARD_DUAL=0: single walks only
         dual = os.environ.get("PAB_FORWARD_DUAL", "1") != "0" and acq.f <= int(os.environ.get("PAB_FORWARD_DUAL_MAXF", "1"))
         ptab = ptr(cloud.pair_table()) if dual else None
+        wide = ws.get("wide_list", plan.partitions * J * (WIDE_CAP + 1), torch.int32)
         call("pab_forward", ptr(cloud.rec_a), ptr(cloud.rec_b), ptr(cloud.gmeta), ptab,
              cloud.n_groups,
              ptr(det.pos), ptr(det.aux), J, det.sound_speed, acq.t0, acq.dt, acq.f, n_out, acq.cutoff,
              acq.dir_kind, acq.dir_param, plan.groups_per_cell, plan.partitions, plan.warps,
-             plan.tile_rows, ptr(partial), ptr(counters.ops), ptr(counters.status), _stream())
+             plan.tile_rows, ptr(partial), ptr(wide), WIDE_CAP, ptr(counters.ops), ptr(counters.status), _stream())
     else:
         partial.zero_()
     if callable(real_local):

@@ -77,7 +77,7 @@ def test_record_length_limit(lib_path):
     args = (p, p, p, 1, p, p, 1, 1500.0, 0.0, 2.5e-8, 2, n_out, 6.0, 0, 0.0)
     assert lib.pab_adjoint(*args, p, ctypes.c_float(1.0), 2, 1, 1, p, None, p, None) == 1
     assert lib.pab_forward(p, p, p, None, 1, p, p, 1, 1500.0, 0.0, 2.5e-8, 2, n_out, 6.0, 0, 0.0, 0, 1, 1, 0,
-                           p, p, p, None) == 1
+                           p, p, 0, p, p, None) == 1
     assert E.Acq(1500.0, 0.0, 2.5e-8, 1 << 21, 1, 6.0, 0, 0.0).n_out == 1 << 21
     with pytest.raises(ValueError, match="exceeds"):
         E.Acq(1500.0, 0.0, 2.5e-8, (1 << 21) + 1, 1, 6.0, 0, 0.0)

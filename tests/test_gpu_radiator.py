@@ -458,12 +458,17 @@ def test_windows_clipped_at_both_recording_ends(P, f):
     assert rel_l2(gr.d_position, gpos) < GRAD_TOL
 
 
-@pytest.mark.parametrize("a0_mm", [0.2, 0.6])
-def test_sparse_wide_groups_match_oracle(P, a0_mm):
+@pytest.mark.parametrize("a0_mm,wide_cap", [(0.2, None), (0.6, None), (0.2, 0), (0.6, 1)])
+def test_sparse_wide_groups_match_oracle(P, a0_mm, wide_cap, monkeypatch):
     """Lane groups spanning tens of millimetres (arrival ranges far wider
     than the forward's live tile and the adjoint's staged segment) and, at
-    0.6 mm, windows too wide for the uniform walk: the forward's linear-pass
-    path and the adjoint's per-lane fallback, against the oracle."""
+    0.6 mm, windows too wide for the uniform walk: the forward's wide-group
+    kernel and the adjoint's per-lane fallback, against the oracle.
+    wide_cap 0 / 1: the sweep's list of wide groups overflows, the
+    wide-group kernel finds them again itself (its scan path)."""
+    if wide_cap is not None:
+        from paper_2601_00551_b200 import engine as E
+        monkeypatch.setattr(E, "WIDE_CAP", wide_cap)
     rng = np.random.default_rng(31)
     n = 96
     pos = rng.uniform(-15e-3, 15e-3, (n, 3))

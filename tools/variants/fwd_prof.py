@@ -16,7 +16,17 @@ from paper_2601_00551_b200 import engine as E  # noqa: E402
 from paper_2601_00551_b200 import radiator as R  # noqa: E402
 from paper_2601_00551_b200 import scenes  # noqa: E402
 
-if os.environ.get("CONFIG") == "4":
+if os.environ.get("CONFIG") == "recon2":   # the config-3 reconstruction's f = 1 cloud (tools/recon_level2_cloud.py)
+    sc = scenes.schedule_config()
+    ctx = P.ForwardContext(sc.array, sc.grid)
+    import numpy as np
+    d = np.load(os.path.join("gpurun_out", "level2_cloud.npz"))
+
+    class _C:
+        pass
+    sc.init = _C()
+    sc.init.positions, sc.init.p0, sc.init.a0 = d["pos"], d["p0"], d["a0"]
+elif os.environ.get("CONFIG") == "4":
     sc = scenes.planar_config(n_balls=int(os.environ.get("N", "4000000")))
     ctx = P.ForwardContext(sc.array, sc.grid, directivity=P.Directivity(
         "none") if os.environ.get("DIR") == "none" else P.Directivity("element", width=0.5e-3))
