@@ -766,8 +766,8 @@ def main():
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": sampler.summary(),
             "gpu_launches": int(launches),
             "gpu_launches_note": "library kernels issued inside the timed region (counted by _lib.call): per step "
-                                 "pack x2 (forward and adjoint packings), coincidence test, forward, residual, adjoint, finalize, "
-                                 "pass tail",
+                                 "pack x2 (forward and adjoint packings), coincidence test, forward sweep, forward wide groups, residual, "
+                                 "adjoint, finalize, pass tail",
             "kernel_ms_min_median": {"forward+residual": [min(fwd_ms), statistics.median(fwd_ms)],
                                      "adjoint+finalize": [min(adj_ms), statistics.median(adj_ms)]}}
     if world > 1:

@@ -94,7 +94,8 @@ def load(path: str = LIB_PATH):
 # its timed region as gpu_launches).  Every launching entry point issues one
 # kernel, except these.
 LAUNCHES = {"kernels": 0}
-_KERNELS_PER_CALL = {"pab_host_stage_copy": 0, "pab_host_stage_narrow": 0, "pab_compact": 3, "pab_sumsq_diff_f64": 2, "pab_cloud_bounds": 2, "pab_sort_perm": 15}
+_KERNELS_PER_CALL = {"pab_host_stage_copy": 0, "pab_host_stage_narrow": 0, "pab_compact": 3, "pab_sumsq_diff_f64": 2,
+                     "pab_cloud_bounds": 2, "pab_sort_perm": 15, "pab_forward": 2}
 
 
 def call(name: str, *args) -> None:
