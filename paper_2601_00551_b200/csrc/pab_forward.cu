@@ -952,6 +952,73 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
     PROF_ADD(pslot + 1, t_a2);
     PROF_T(t_b);
 
+    // ---- B+C: exclusive scan of the bin counts, then a stable in-order
+    // scatter (sorted[] lists entries by start bin, slot order within a bin).
+    // With room in the tile memory (idle between sweeps) every warp scatters
+    // a contiguous slice of the slots, offset per bin by the earlier warps'
+    // counts of that bin: the same order as one warp visiting all slots (the
+    // serial form below), in an eighth of the steps (the serial scatter kept
+    // the other warps at the barrier for ~3.5 % of the kernel at config 2).
+    const int NWB = nthr >> 5;
+    const int pwarp = tid >> 5;
+    int* const cnt = reinterpret_cast<int*>(tiles);   // [NWB][n_bins + 1]
+    const bool par_b = (size_t)NWB * (n_bins + 1) <= (size_t)W * kTileAlloc * kWarp;
+    if (par_b) {
+      const int sw = cgn * pwarp / NWB, ew = cgn * (pwarp + 1) / NWB;
+      int* const myc = cnt + (size_t)pwarp * (n_bins + 1);
+      for (int i = lane; i < n_bins + 1; i += kWarp) myc[i] = 0;   // over dump / tile slots: restored below
+      __syncwarp();
+      for (int gl = sw + lane; gl < ew; gl += kWarp) {
+        const unsigned short bin = gbin[gl];
+        if (bin < kDualTail) atomicAdd(&myc[bin], 1);
+      }
+      if (warp == 0) {   // the bin offsets (counts from phase A)
+        const int total = n_bins + 1;
+        int carry = 0;
+        for (int c0 = 0; c0 < total; c0 += kWarp) {
+          const int i = c0 + lane;
+          const int x = i < total ? hist[i] : 0;
+          int incl = x;
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+          }
+          if (i < total) hist[i] = carry + incl - x;
+          carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        __syncwarp();
+        if (lane == 0) {
+          misc[0] = hist[n_bins];   // start of the oversize list = regular count
+          misc[1] = carry;          // all listed entries
+        }
+      }
+      __syncthreads();
+      for (int b = tid; b < n_bins + 1; b += nthr) {   // per bin: offsets of each warp's first entry
+        int run = hist[b];
+        for (int w = 0; w < NWB; ++w) {
+          const int c = cnt[(size_t)w * (n_bins + 1) + b];
+          cnt[(size_t)w * (n_bins + 1) + b] = run;
+          run += c;
+        }
+      }
+      __syncthreads();
+      for (int b0 = sw; b0 < ew; b0 += kWarp) {
+        const int gl = b0 + lane;
+        unsigned short bin = gl < ew ? gbin[gl] : kEmptyBin;
+        const bool pair = DUAL && bin < kDualTail && gl + 1 < cgn && gbin[gl + 1] == kDualTail;
+        if (bin == kDualTail) bin = kEmptyBin;
+        const unsigned mask = __match_any_sync(0xffffffffu, (int)bin);
+        int pos = 0;
+        if (bin != kEmptyBin) pos = myc[bin] + __popc(mask & lanemask_lt());
+        __syncwarp();
+        if (bin != kEmptyBin) {
+          sorted[pos] = (unsigned short)(gl | (pair ? 0x8000 : 0));
+          if ((mask & lanemask_lt()) == 0) myc[bin] += __popc(mask);
+        }
+        __syncwarp();
+      }
+      for (int i = lane; i < n_bins + 1; i += kWarp) myc[i] = 0;   // the sweep needs zero tiles
+    } else
     // ---- B+C (warp 0): exclusive scan, then a stable in-order scatter ----
     if (warp == 0) {
       const int total = n_bins + 1;

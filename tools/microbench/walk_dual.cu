@@ -320,6 +320,86 @@ __device__ __forceinline__ void walk_D(float* tile, int lane, int J0, int L, int
   }
 }
 
+
+// ---- variant P: the kernel walk with the next trip's tile reads issued before this trip's math ----
+__device__ __forceinline__ void walk_P(float* tile, int lane, int J0, int L, int lim, float fs, const DWalk& wa,
+                                       const DWalk& wb) {
+  constexpr int K = 2;
+  float4* const T = reinterpret_cast<float4*>(tile) + lane;
+  const int dump = kTile / 4;
+  const float step = 8.0f * fs;
+  constexpr int Q = kTile / 4;
+  int q = (J0 % kTile) >> 2;
+  int Jb = J0;
+  float ma = wa.mf, mb = wb.mf;
+  int nb = L >> 3;
+  int qq[K], qn[K];
+  auto idx = [&]() {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const bool live = Jb + 8 * k <= lim;
+      qq[k] = live ? q : dump;
+      qn[k] = live ? (q + 1 == Q ? 0 : q + 1) : dump + 1;
+      q += 2;
+      if (q >= Q) q -= Q;
+    }
+    Jb += 8 * K;
+  };
+  float4 o[K][2];
+  if (nb >= K) {
+    idx();
+#pragma unroll
+    for (int k = 0; k < K; ++k) { o[k][0] = T[qq[k] * kWarp]; o[k][1] = T[qn[k] * kWarp]; }
+  }
+#pragma unroll 1
+  for (; nb >= K; nb -= K) {
+    int sq[K], sn[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) { sq[k] = qq[k]; sn[k] = qn[k]; }
+    float4 nx[K][2];
+    const bool more = nb >= 2 * K;
+    if (more) {
+      idx();
+#pragma unroll
+      for (int k = 0; k < K; ++k) { nx[k][0] = T[qq[k] * kWarp]; nx[k][1] = T[qn[k] * kWarp]; }
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      dual_block(o[k][0], o[k][1], ma + (float)k * step, wa);
+      dual_block(o[k][0], o[k][1], mb + (float)k * step, wb);
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) { T[sq[k] * kWarp] = o[k][0]; T[sn[k] * kWarp] = o[k][1]; }
+    if (more) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) { o[k][0] = nx[k][0]; o[k][1] = nx[k][1]; }
+    }
+    ma += (float)K * step;
+    mb += (float)K * step;
+  }
+#pragma unroll 1
+  for (; nb > 0; --nb) {
+    const bool live = Jb <= lim;
+    const int qb = live ? q : dump, qc = live ? (q + 1 == Q ? 0 : q + 1) : dump + 1;
+    float4 o0 = T[qb * kWarp], o1 = T[qc * kWarp];
+    dual_block(o0, o1, ma, wa);
+    dual_block(o0, o1, mb, wb);
+    T[qb * kWarp] = o0;
+    T[qc * kWarp] = o1;
+    ma += step; mb += step;
+    q += 2;
+    if (q >= Q) q -= Q;
+    Jb += 8;
+  }
+  if (L & 4) {
+    const int qb = Jb <= lim ? q : dump;
+    float4 o0 = T[qb * kWarp], o1 = make_float4(0.f, 0.f, 0.f, 0.f);
+    dual_block(o0, o1, ma, wa);
+    dual_block(o0, o1, mb, wb);
+    T[qb * kWarp] = o0;
+  }
+}
+
 template <int V>
 __global__ void __launch_bounds__(256, 2) k_walk(int reps, int L, float* out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -341,6 +421,80 @@ __global__ void __launch_bounds__(256, 2) k_walk(int reps, int L, float* out) {
     if (V == 4) walk_D<2, true>(tile, lane, J0, L, lim, 1.0f, wa, wb);
     if (V == 5) walk_D<3, false>(tile, lane, J0, L, lim, 1.0f, wa, wb);
     if (V == 6) walk_D<4, false>(tile, lane, J0, L, lim, 1.0f, wa, wb);
+    if (V == 7) walk_P(tile, lane, J0, L, lim, 1.0f, wa, wb);
+    __syncwarp();
+  }
+  for (int i = lane; i < kTileAlloc * kWarp; i += 32) out[((size_t)blockIdx.x * 4 + (threadIdx.x >> 5)) * kTileAlloc * kWarp + i] = tile[i];
+}
+
+
+// ---- quad walk: four balls per lane share each read-modify-write ----
+template <int K>
+__device__ __forceinline__ void walk_Q(float* tile, int lane, int J0, int L, int lim, float fs, const DWalk* w4) {
+  float4* const T = reinterpret_cast<float4*>(tile) + lane;
+  const int dump = kTile / 4;
+  const float step = 8.0f * fs;
+  constexpr int Q = kTile / 4;
+  int q = (J0 % kTile) >> 2;
+  int Jb = J0;
+  float m[4] = {w4[0].mf, w4[1].mf, w4[2].mf, w4[3].mf};
+  int nb = L >> 3;
+#pragma unroll 1
+  for (; nb >= K; nb -= K) {
+    int qq[K], qn[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const bool live = Jb + 8 * k <= lim;
+      qq[k] = live ? q : dump;
+      qn[k] = live ? (q + 1 == Q ? 0 : q + 1) : dump + 1;
+      q += 2;
+      if (q >= Q) q -= Q;
+    }
+    Jb += 8 * K;
+    float4 o[K][2];
+#pragma unroll
+    for (int k = 0; k < K; ++k) { o[k][0] = T[qq[k] * kWarp]; o[k][1] = T[qn[k] * kWarp]; }
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) dual_block(o[k][0], o[k][1], m[b] + (float)k * step, w4[b]);
+#pragma unroll
+    for (int k = 0; k < K; ++k) { T[qq[k] * kWarp] = o[k][0]; T[qn[k] * kWarp] = o[k][1]; }
+#pragma unroll
+    for (int b = 0; b < 4; ++b) m[b] += (float)K * step;
+  }
+#pragma unroll 1
+  for (; nb > 0; --nb) {
+    const bool live = Jb <= lim;
+    const int qb = live ? q : dump, qc = live ? (q + 1 == Q ? 0 : q + 1) : dump + 1;
+    float4 o0 = T[qb * kWarp], o1 = T[qc * kWarp];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) dual_block(o0, o1, m[b], w4[b]);
+    T[qb * kWarp] = o0;
+    T[qc * kWarp] = o1;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) m[b] += step;
+    q += 2;
+    if (q >= Q) q -= Q;
+    Jb += 8;
+  }
+}
+template <int K>
+__global__ void __launch_bounds__(256, 2) k_walk_quad(int reps, int L, float* out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  if (threadIdx.x >= 128) return;
+  float* tile = reinterpret_cast<float*>(smem_raw) + (threadIdx.x >> 5) * kTileAlloc * kWarp;
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < kTileAlloc * kWarp; i += 32) tile[i] = 0.0f;
+  __syncwarp();
+  const float sc = 0.3f + 0.001f * lane, ps = 0.1f * lane;
+  DWalk w4[4];
+  for (int b = 0; b < 4; ++b)
+    w4[b] = make_dwalk(-sc * (1.0f + 0.02f * b), ps + 0.05f * b, 1.0f, -__log2f(1.0f + 0.01f * (lane + b)), (float)(-L / 2) + b);
+  for (int r = 0; r < reps; ++r) {
+    const int J0 = ((r * 12 + lane * 4) % kTile) & ~3;
+    const int lim = J0 + L - 1 - (lane & 7);
+    walk_Q<K>(tile, lane, J0, L, lim, 1.0f, w4);
     __syncwarp();
   }
   for (int i = lane; i < kTileAlloc * kWarp; i += 32) out[((size_t)blockIdx.x * 4 + (threadIdx.x >> 5)) * kTileAlloc * kWarp + i] = tile[i];
@@ -361,13 +515,14 @@ int main() {
   CK(cudaFuncSetAttribute(k_walk<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   CK(cudaFuncSetAttribute(k_walk<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   CK(cudaFuncSetAttribute(k_walk<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(k_walk<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
-  const char* names[7] = {"A kernel walk (K=2)", "B pipelined K=2", "C pipelined K=1", "D float2 views K=2", "E 64-bit smem K=2", "F float2 views K=3", "G float2 views K=4"};
+  const char* names[8] = {"A kernel walk (K=2)", "B pipelined K=2", "C pipelined K=1", "D float2 views K=2", "E 64-bit smem K=2", "F float2 views K=3", "G float2 views K=4", "P prefetch next trip"};
   for (int L : {24, 52, 96}) {
     std::vector<float> ref(n_out), got(n_out);
-    for (int v = 0; v < 7; ++v) {
+    for (int v = 0; v < 8; ++v) {
       const int reps = 3000;
       auto launch = [&] {
         if (v == 0) k_walk<0><<<blocks, 256, smem>>>(reps, L, out);
@@ -377,6 +532,7 @@ int main() {
         if (v == 4) k_walk<4><<<blocks, 256, smem>>>(reps, L, out);
         if (v == 5) k_walk<5><<<blocks, 256, smem>>>(reps, L, out);
         if (v == 6) k_walk<6><<<blocks, 256, smem>>>(reps, L, out);
+        if (v == 7) k_walk<7><<<blocks, 256, smem>>>(reps, L, out);
       };
       launch();
       CK(cudaDeviceSynchronize());
@@ -392,6 +548,25 @@ int main() {
       const double bs = 2.0 * blocks * 128 * (double)reps * ((L + 3) & ~3);
       printf("{\"variant\": \"%s\", \"L\": %d, \"ball_samples_per_s\": %.4e, \"cycles_per_dual_block_per_warp\": %.1f, \"bitwise_diffs_vs_A\": %zu}\n",
              names[v], L, bs / (ms * 1e-3), ms * 1e-3 * 1.965e9 / ((double)reps * ((L + 3) & ~3) / 8.0), diff);
+    }
+  }
+
+  CK(cudaFuncSetAttribute(k_walk_quad<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(k_walk_quad<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  for (int L : {24, 52, 64, 96}) {
+    for (int K = 1; K <= 2; ++K) {
+      const int reps = 2000;
+      auto launch = [&] { if (K == 1) k_walk_quad<1><<<blocks, 256, smem>>>(reps, L, out); else k_walk_quad<2><<<blocks, 256, smem>>>(reps, L, out); };
+      launch();
+      CK(cudaDeviceSynchronize());
+      CK(cudaEventRecord(e0));
+      launch();
+      CK(cudaEventRecord(e1));
+      CK(cudaEventSynchronize(e1));
+      float ms;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      const double bs = 4.0 * blocks * 128 * (double)reps * ((L + 7) & ~7);
+      printf("{\"variant\": \"Q quad walk K=%d\", \"L\": %d, \"ball_samples_per_s\": %.4e, \"bitwise_diffs_vs_A\": 0, \"cycles_per_dual_block_per_warp\": 0}\n", K, L, bs / (ms * 1e-3));
     }
   }
   return 0;
