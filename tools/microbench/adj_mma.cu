@@ -298,6 +298,12 @@ int main() {
     printf("{\"bench\": \"mma.sync m16n8k8 tf32\", \"mma_per_s\": %.4e, \"tflops\": %.1f, \"mma_per_clk_per_sm_at_1965\": %.3f}\n",
            mmas / (ms * 1e-3), mmas * 2048 / (ms * 1e-3) / 1e12, mmas / (ms * 1e-3) / sms / 1.965e9);
   }
+  for (int wps : {4, 8, 12, 16}) {   // lane-per-ball walk at 1..4 warps per scheduler
+    const int reps = 2000, L = 48, blocks = sms * wps;
+    const double bs = (double)blocks * 32 * reps * L;
+    const float ms = timeit([&] { k_old_walk<<<blocks, 32>>>(d_seg, d_ball, reps, L, d_out); });
+    printf("{\"bench\": \"lane-per-ball walk (current)\", \"warps_per_sm\": %d, \"L\": %d, \"ball_samples_per_s\": %.4e}\n", wps, L, bs / (ms * 1e-3));
+  }
   for (int L : {16, 48, 96}) {
     const int reps = 2000;
     const int blocks = sms * 16;
