@@ -264,6 +264,10 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   const bool live = B.orig >= 0;
   const float qmax = live ? (rho * sc) * (rho * sc) : -1.0f;
   const WalkConst W = walk_const(sc, f);
+  // the conversion-free setup pays where the XU pipe binds (ex2 walk); the
+  // element directivity's sinc terms load the FMA pipe instead (config 4:
+  // lean +0.7 ms)
+  constexpr bool kLean = kAdjLean && DIR != kDirElement;
   const float kap_rs = A.a0 * kSqrt2Ln2 * res_sign;   // kappa * sign
   const float kap2 = 2.0f * A.a0 * kSqrt2Ln2;         // 2 kappa (factored epilogue)
   const float p0h = 0.5f * B.p0;
@@ -413,7 +417,7 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
     auto usetup = [&](const GroupDet& gd, int lo) {
       USetup u;
       int jlo, jhi;
-      if (kAdjLean) {
+      if (kLean) {
         float kf;
         u.pg = pair_geom_lean(gd, A, B, acq, &kf);
         pair_window_cover_lean(kf, u.pg.phi, rho, acq, &jlo, &jhi);
@@ -440,7 +444,7 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       return M;
 #endif
       moments_uniform<STAGE, MASK>(seg_all[warp][buf] + (u.J0 - lo), (u.L + 3) & ~3,
-                                   kAdjLean ? int_to_float(u.J0 * f - u.pg.kc)
+                                   kLean ? int_to_float(u.J0 * f - u.pg.kc)
                                                           : (float)(u.J0 * f - u.pg.kc),
                                    W, u.pg.phi * sc, u.empty ? -1.0f : qmax, M);
       if (!MASK && u.empty) M = {0.f, 0.f, 0.f, 0.f};
