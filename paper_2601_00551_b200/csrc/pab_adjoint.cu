@@ -240,6 +240,7 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   // vec16: 16-byte cp.async staging (rows 16-byte aligned: host-checked
   // n_out % 4 == 0 and a 16-byte aligned residual pointer)
   __shared__ __align__(16) float seg_all[kAdjWarps][4][kSeg + kPad + 4];
+  __shared__ __align__(16) float4 bat[kAdjWarps][kWarp][DIR == kDirElement ? 5 : 4];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // the processing order ascends in a0 bucket (window length): the
   // wide-window groups launch first and the light ones fill the tail
@@ -271,7 +272,7 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   const float kap_rs = A.a0 * kSqrt2Ln2 * res_sign;   // kappa * sign
   const float kap2 = 2.0f * A.a0 * kSqrt2Ln2;         // 2 kappa (factored epilogue)
   const float p0h = 0.5f * B.p0;
-  // the uniform walk must stay inside the staged samples + zero padding
+  // the uniform walk must stay inside the staged samples + the buffer's slack
   // (cover window <= 2 rho / f + 3 samples, + 3 alignment + 3 rounding)
   const bool fits = 2.0f * (acq.cutoff * gm.a0max * acq.inv_vdt_f) * acq.inv_f + 12.0f <= (float)kPad;
   // per-ball FP64 sums across the chunk, in shared memory (registers stay
@@ -279,6 +280,7 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   __shared__ double acc_s[kAdjWarps][5][kWarp];
 #pragma unroll
   for (int c = 0; c < 5; ++c) acc_s[warp][c][lane] = 0.0;
+  for (int i = lane; i < 4 * (kSeg + kPad + 4); i += kWarp) (&seg_all[warp][0][0])[i] = 0.0f;
   unsigned long long my_ops = 0;
   int coinc = 0;
 #ifdef PAB_ADJ_PROF
@@ -302,6 +304,45 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
             (!nr && fits && rlo <= rhi && rhi - rlo + 1 <= kSeg ? kFlagUniform : 0);
       if (DIR != kDirNone) ddl = load_detdir(det_aux, jl);
     }
+    // the batch's per-detector data in shared memory: the pair loop reads a
+    // detector's geometry, flags and direction with broadcast LDS.128 (3-5)
+    // instead of 10-16 shuffles (lane stride 80 B: conflict-free writes)
+    {
+      float4* const bt = bat[warp][lane];
+      bt[0] = make_float4(gdl.Sx, gdl.Sy, gdl.Sz, gdl.Sn);
+      bt[1] = make_float4(gdl.isn, gdl.phg, __int_as_float(gdl.kg), __int_as_float(rfl));
+      bt[2] = make_float4(__int_as_float(rlo), __int_as_float(rhi), ddl.fx, ddl.fy);
+      if (DIR != kDirNone) bt[3] = make_float4(ddl.fz, ddl.e1x, ddl.e1y, ddl.e1z);
+      if (DIR == kDirElement) bt[4] = make_float4(ddl.e2x, ddl.e2y, ddl.e2z, 0.0f);
+    }
+    __syncwarp();
+    auto bgd = [&](int jj) {   // group geometry (slow flag from the flags word, as shfl_gd_fast + fallback)
+      const float4 a = bat[warp][jj][0], b = bat[warp][jj][1];
+      GroupDet gd;
+      gd.Sx = a.x; gd.Sy = a.y; gd.Sz = a.z; gd.Sn = a.w;
+      gd.isn = b.x; gd.phg = b.y; gd.kg = __float_as_int(b.z);
+      gd.slow = 0;
+      return gd;
+    };
+    auto bdd = [&](int jj) {
+      DetDir dd{};
+      if (DIR != kDirNone) {
+        const float4 c = bat[warp][jj][2], d = bat[warp][jj][3];
+        dd.fx = c.z; dd.fy = c.w; dd.fz = d.x;
+        dd.e1x = d.y; dd.e1y = d.z; dd.e1z = d.w;
+        if (DIR == kDirElement) {
+          const float4 e = bat[warp][jj][4];
+          dd.e2x = e.x; dd.e2y = e.y; dd.e2z = e.z;
+        }
+      }
+      return dd;
+    };
+    auto blhf = [&](int jj, int& lo, int& hi, int& fl) {
+      const float4 c = bat[warp][jj][2];
+      lo = __float_as_int(c.x);
+      hi = __float_as_int(c.y);
+      fl = __float_as_int(bat[warp][jj][1].w);
+    };
     // stage res[j][lo .. hi] (lo a multiple of 4) + kPad zeros into buffer
     // `buf`: 16-B cp.async (16-B aligned rows) or 4-B cp.async
     auto stage_seg = [&](int jj, int lo, int hi, int fl, int buf) {
@@ -318,13 +359,14 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
         if (lane < len4) cp_async16(dst + 4 * lane, src + 4 * lane);
         if (lane + kWarp < len4) cp_async16(dst + 4 * (lane + kWarp), src + 4 * (lane + kWarp));
         cp_async_commit();
-        float4* z = reinterpret_cast<float4*>(dst + 4 * len4);
-        if (lane < kPad / 4) z[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
       } else {
         for (int k = lane; k < len; k += kWarp) cp_async4(dst + k, src + k);
-        for (int k = lane; k < kPad; k += kWarp) dst[len + k] = 0.0f;
         cp_async_commit();
       }
+      // no zero padding: past the staged samples the uniform walk meets the
+      // earlier detectors' (finite) residuals of this buffer, beyond every
+      // lane's window, where G <= 2^-24 of the ball's peak (the masked walk
+      // zeroes them); the buffers start zeroed
     };
     auto wait_seg = [&](int fl) {
       if (fl & kFlagUniform) cp_async_wait_all();
@@ -501,10 +543,10 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
     // processed the next pair's segments are in flight; the two pairs'
     // setups (latency-bound chains) and gradient epilogues are computed side
     // by side
-    int loA = __shfl_sync(0xffffffffu, rlo, 0), hiA = __shfl_sync(0xffffffffu, rhi, 0);
-    int flA = __shfl_sync(0xffffffffu, rfl, 0);
-    int loB = __shfl_sync(0xffffffffu, rlo, 1), hiB = __shfl_sync(0xffffffffu, rhi, 1);
-    int flB = nd > 1 ? __shfl_sync(0xffffffffu, rfl, 1) : 0;
+    int loA, hiA, flA, loB, hiB, flB;
+    blhf(0, loA, hiA, flA);
+    blhf(min(1, nd - 1), loB, hiB, flB);
+    if (nd < 2) flB = 0;
     APROF_ACC(0, t_geo);
     stage_seg(0, loA, hiA, flA, 0);
     if (nd > 1) stage_seg(1, loB, hiB, flB, 1);
@@ -512,22 +554,18 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       const bool two = jj + 1 < nd;
       const int bA = jj & 3, bB = bA + 1;
       const int la = loA, ha = hiA, fa = flA, lb = loB, hb = hiB, fb = two ? flB : 0;
-      const GroupDet gdA = shfl_gd_fast(gdl, jj), gdB = shfl_gd_fast(gdl, two ? jj + 1 : jj);
-      const DetDir ddA = shfl_detdir<DIR>(ddl, jj), ddB = shfl_detdir<DIR>(ddl, two ? jj + 1 : jj);
+      const GroupDet gdA = bgd(jj), gdB = bgd(two ? jj + 1 : jj);
+      const DetDir ddA = bdd(jj), ddB = bdd(two ? jj + 1 : jj);
       APROF_T(t_w);
       wait_seg(fa | fb);
       __syncwarp();   // every lane is past the previous pair: its buffers may be refilled
       APROF_ACC(1, t_w);
       APROF_T(t_st);
       if (jj + 2 < nd) {
-        loA = __shfl_sync(0xffffffffu, rlo, jj + 2);
-        hiA = __shfl_sync(0xffffffffu, rhi, jj + 2);
-        flA = __shfl_sync(0xffffffffu, rfl, jj + 2);
+        blhf(jj + 2, loA, hiA, flA);
         stage_seg(jj + 2, loA, hiA, flA, bA ^ 2);
         if (jj + 3 < nd) {
-          loB = __shfl_sync(0xffffffffu, rlo, jj + 3);
-          hiB = __shfl_sync(0xffffffffu, rhi, jj + 3);
-          flB = __shfl_sync(0xffffffffu, rfl, jj + 3);
+          blhf(jj + 3, loB, hiB, flB);
           stage_seg(jj + 3, loB, hiB, flB, bB ^ 2);
         } else {
           flB = 0;
