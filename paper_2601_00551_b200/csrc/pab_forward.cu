@@ -600,6 +600,15 @@ __device__ __forceinline__ void evaluate_pair(float* tile, int lane, const Acq& 
 #endif
 constexpr bool kWS = PAB_FWD_WS != 0;
 
+// Second-group geometry of a setup warp's batch (dual entries), kept in the
+// bin histogram's space while the sweep runs: 2 x float4 per entry, read by
+// broadcast LDS.128 instead of 7 shuffles per entry.
+constexpr int kPTabWords = 8;
+__host__ __device__ inline int hist_ints(int n_bins, int warps, bool dual) {
+  const int t = dual ? warps * kWarp * kPTabWords : 0;
+  return n_bins + 1 > t ? n_bins + 1 : t;
+}
+
 // An entry (a group, or a dual pair's union) sweeps only if its rows
 // [blo, hi + 7] (4-aligned starts, the last block may run 7 rows past the
 // window) fit the live tile and its pairs take the fast geometry; groups
@@ -845,7 +854,9 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   float* tiles = reinterpret_cast<float*>(smem_raw) + (SROW ? ((n_out + 3) & ~3) : 0);
   float* stage = tiles + (size_t)W * kTileAlloc * kWarp;
   int* hist = reinterpret_cast<int*>(stage + W * kTile);        // [n_bins + 1]
-  int* zs = hist + (n_bins + 1);                                // [W + 1]
+  // (DUAL: during the sweep the histogram's space holds the setup warps'
+  // tables of their batches' second-group geometry, kPTabWords per entry)
+  int* zs = hist + hist_ints(n_bins, W, DUAL);                 // [W + 1]
   int* misc = zs + W + 1;                                       // [4]
   unsigned short* sorted = reinterpret_cast<unsigned short*>(misc + 4);
   unsigned short* gbin = sorted + kCU;
@@ -1338,6 +1349,13 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
             word_l = (unsigned)bin | ((unsigned)(ghi - (bin << kBinShift)) << 16) | (pair ? 0x80000000u : 0u);
             cell_l = pair ? pair_cell(gdA_l.Sx, gdA_l.Sy, gdA_l.Sz) : 0;
           }
+          __syncwarp();   // the previous batch's table reads are done
+          {
+            float4* const pt = reinterpret_cast<float4*>(hist) + (size_t)(w * kWarp + lane) * 2;
+            pt[0] = make_float4(gdB_l.Sx, gdB_l.Sy, gdB_l.Sz, gdB_l.Sn);
+            pt[1] = make_float4(gdB_l.isn, gdB_l.phg, __int_as_float(gdB_l.kg), 0.0f);
+          }
+          __syncwarp();
           PROF_ACC(pp_geo, t_g);
           // two-stage prefetch: pairing ids two entries ahead, records one ahead
           auto entry = [&](int k, int64_t& g0, bool& pair, int& cell) {
@@ -1392,7 +1410,14 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
                       make_float4(p.phi * p.sc * sg, nla, p.qmax + nla, 0.0f), make_float2(0.f, 0.f));
               continue;
             }
-            const GroupDet gB = shfl_gd_fast(gdB_l, k);
+            GroupDet gB;
+            {
+              const float4* const pt = reinterpret_cast<const float4*>(hist) + (size_t)(w * kWarp + k) * 2;
+              const float4 a = pt[0], b = pt[1];
+              gB.Sx = a.x; gB.Sy = a.y; gB.Sz = a.z; gB.Sn = a.w;
+              gB.isn = b.x; gB.phg = b.y; gB.kg = __float_as_int(b.z);
+              gB.slow = 0;
+            }
             const PairSetup pa = pair_setup<DIR, false>(acq, (ids & 0xE0u) ? gB : gA, dd, A0, B0, my_ops, blo);
             const PairSetup pb = pair_setup<DIR, false>(acq, (ids & 0xE000u) ? gB : gA, dd, A1, B1, my_ops, blo);
             // walk parameters per ball (sgn(Ak) folded into y; empty balls: y = 0, G = 0)
@@ -1598,8 +1623,8 @@ size_t forward_smem(int n_out, int warps, bool srow, bool dual) {
   const size_t rec_bytes = dual ? 40 : 32;   // hand-off record per lane and ring slot
   const size_t ring = kWS ? 16 + (size_t)warps * kRing * (rec_bytes * kWarp + 16 + 2 * 8) : 0;
   const size_t units = kChunk;
-  return row_bytes + (size_t)warps * kTileAlloc * kWarp * 4 + (size_t)warps * kTile * 4 + (n_bins + 1) * 4 +
-         (size_t)(warps + 1) * 4 + 16 + 2 * units * 2 + 16 + ring;
+  return row_bytes + (size_t)warps * kTileAlloc * kWarp * 4 + (size_t)warps * kTile * 4 +
+         (size_t)hist_ints((int)n_bins, warps, dual) * 4 + (size_t)(warps + 1) * 4 + 16 + 2 * units * 2 + 16 + ring;
 }
 
 }  // namespace pab
