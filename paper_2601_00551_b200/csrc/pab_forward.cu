@@ -44,7 +44,8 @@ constexpr unsigned short kEmptyBin = 0xFFFF;
 constexpr unsigned short kDualTail = 0xFFFE;   // second slot of a dual sort entry
 constexpr int kTile = PAB_FWD_TILE;    // tile rows per warp (circular, slot = J % kTile, multiple of 8)
 constexpr int kMaxWarps = PAB_FWD_MAXWARPS;
-constexpr int kTileAlloc = kTile + 8;  // + one 8-row dump block per warp
+constexpr int kTileAlloc = kTile + 8;  // + one 8-row dump block per warp (wide-group kernel, benches)
+constexpr int kDumpFloats = 8 * kWarp; // the sweep's walkers share one dump block
 #ifndef PAB_FWD_RING
 #define PAB_FWD_RING 2   // hand-off slots per walker (warp-specialised sweep)
 #endif
@@ -206,7 +207,7 @@ __device__ __forceinline__ Walk make_walk(float nsc, float pss, float fs, float 
 
 template <bool MASK>
 __device__ __forceinline__ void rmw_walk(float* tile, int lane, int J0, int L, int lim, float mf, float fs,
-                                         const Walk& w);
+                                         const Walk& w, int dump = kTile / 4);
 
 // Walk with the amplitude as a factor (phase F): Ak y G with Ak folded into
 // a second set of y coefficients (ya = m Ak nsc + Ak c ~ Ak y), so doubling
@@ -273,18 +274,18 @@ __device__ __forceinline__ void rmw_walk_amp(float* tile, int lane, int J0, int 
 
 template <bool MASK>
 __device__ __forceinline__ void rmw_uniform(float* tile, int lane, int J0, int L, int lim, float mf, float fs,
-                                            float sc, float ps, float Ak, float qmax) {
+                                            float sc, float ps, float Ak, float qmax, int dump = kTile / 4) {
   const float sg = Ak < 0.0f ? -1.0f : 1.0f;   // sgn(Ak) folded into y
   const float nla = -__log2f(fabsf(Ak));       // +inf for Ak = 0
-  rmw_walk<MASK>(tile, lane, J0, L, lim, mf, fs, make_walk(-sc * sg, ps * sg, fs, nla, qmax + nla));
+  rmw_walk<MASK>(tile, lane, J0, L, lim, mf, fs, make_walk(-sc * sg, ps * sg, fs, nla, qmax + nla), dump);
 }
 
 template <bool MASK>
 __device__ __forceinline__ void rmw_walk(float* tile, int lane, int J0, int L, int lim, float mf, float fs,
-                                         const Walk& w) {
+                                         const Walk& w, int dump) {
   constexpr int K = PAB_FWD_UNROLL;
   float4* const T = reinterpret_cast<float4*>(tile) + lane;   // quad q of this lane: T[q * 32]
-  const int dump = kTile / 4;                                   // dump block = quads kTile/4, kTile/4 + 1
+  // dump block = quads dump, dump + 1 (relative to this tile)
   const float step = 8.0f * fs;
   constexpr int Q = kTile / 4;
   int q = (J0 % kTile) >> 2;   // first quad of the current block
@@ -417,10 +418,9 @@ __device__ __forceinline__ void dual_block(float4& o0, float4& o1, float m, cons
 // Warp-uniform walk of L samples (multiple of 4) from the lane's 4-aligned
 // union start J0; blocks starting past `lim` go to the dump block.
 __device__ __forceinline__ void rmw_walk_dual(float* tile, int lane, int J0, int L, int lim, float fs,
-                                              const DWalk& wa, const DWalk& wb) {
+                                              const DWalk& wa, const DWalk& wb, int dump = kTile / 4) {
   constexpr int K = PAB_DUAL_UNROLL;
   float4* const T = reinterpret_cast<float4*>(tile) + lane;
-  const int dump = kTile / 4;
   const float step = 8.0f * fs;
   constexpr int Q = kTile / 4;
   int q = (J0 % kTile) >> 2;
@@ -526,12 +526,12 @@ __device__ __forceinline__ PairSetup pair_setup(const Acq& acq, const GroupDet& 
 // windows, which are redirected to the dump block.
 template <bool MASK>
 __device__ __forceinline__ void pair_walk(float* tile, int lane, const Acq& acq, const PairSetup& p, int near,
-                                          unsigned long long& ops, int fp) {
+                                          unsigned long long& ops, int fp, int dump = kTile / 4) {
   const float fs = (float)acq.f;
   const bool empty_u = p.jlo > p.jhi;
   if (p.L > 0)
     rmw_uniform<MASK>(tile, lane, p.J0, (p.L + 3) & ~3, empty_u ? -1 : p.jhi, (float)(p.J0 * acq.f - p.kc), fs,
-                      p.sc, p.phi * p.sc, empty_u ? 0.0f : p.Ak, p.qmax);
+                      p.sc, p.phi * p.sc, empty_u ? 0.0f : p.Ak, p.qmax, dump);
   if (near) {
     int nlo = 1, nhi = 0, nkc = 0;
     float nphi = 0.0f;
@@ -542,7 +542,7 @@ __device__ __forceinline__ void pair_walk(float* tile, int lane, const Acq& acq,
       const int J0 = (empty ? fp : nlo) & ~3;
       const int L = __reduce_max_sync(0xffffffffu, empty ? 0 : nhi - J0 + 1);
       rmw_uniform<MASK>(tile, lane, J0, (L + 3) & ~3, empty ? -1 : nhi, (float)(J0 * acq.f - nkc), fs, -p.sc,
-                        nphi * -p.sc, empty ? 0.0f : p.Ak, p.qmax);
+                        nphi * -p.sc, empty ? 0.0f : p.Ak, p.qmax, dump);
     }
   }
 }
@@ -600,12 +600,13 @@ __device__ __forceinline__ void evaluate_pair(float* tile, int lane, const Acq& 
 #endif
 constexpr bool kWS = PAB_FWD_WS != 0;
 
-// Second-group geometry of a setup warp's batch (dual entries), kept in the
-// bin histogram's space while the sweep runs: 2 x float4 per entry, read by
-// broadcast LDS.128 instead of 7 shuffles per entry.
+// Group geometry of a setup warp's batch (dual entries: the first group's
+// with the entry's bin / span / pair word, then the second group's), kept
+// in the bin histogram's space while the sweep runs: 2 x float4 per group,
+// read by broadcast LDS.128 instead of 7-8 shuffles per group.
 constexpr int kPTabWords = 8;
 __host__ __device__ inline int hist_ints(int n_bins, int warps, bool dual) {
-  const int t = dual ? warps * kWarp * kPTabWords : 0;
+  const int t = dual ? 2 * warps * kWarp * kPTabWords : 0;
   return n_bins + 1 > t ? n_bins + 1 : t;
 }
 
@@ -852,7 +853,9 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   // sample by one warp at a time, in a fixed order
   float* row = SROW ? reinterpret_cast<float*>(smem_raw) : partial_rows + ((size_t)part * n_det + j) * (size_t)n_out;
   float* tiles = reinterpret_cast<float*>(smem_raw) + (SROW ? ((n_out + 3) & ~3) : 0);
-  float* stage = tiles + (size_t)W * kTileAlloc * kWarp;
+  // walker tiles (kTile rows each) and ONE dump block shared by the walkers:
+  // it only takes the write-only overrun of blocks past a lane's window
+  float* stage = tiles + (size_t)W * kTile * kWarp + kDumpFloats;
   int* hist = reinterpret_cast<int*>(stage + W * kTile);        // [n_bins + 1]
   // (DUAL: during the sweep the histogram's space holds the setup warps'
   // tables of their batches' second-group geometry, kPTabWords per entry)
@@ -867,7 +870,7 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   const size_t ring_off = (reinterpret_cast<unsigned char*>(gbin + kCU) - smem_raw + 15) & ~(size_t)15;
   float4* slot_a = reinterpret_cast<float4*>(smem_raw + ring_off);
   float4* slot_b = slot_a + W * kRing * kWarp;
-  float2* slot_c = reinterpret_cast<float2*>(slot_b + W * kRing * kWarp);   // DUAL only
+  float* slot_c = reinterpret_cast<float*>(slot_b + W * kRing * kWarp);   // DUAL only
   int4* slot_h = DUAL ? reinterpret_cast<int4*>(slot_c + W * kRing * kWarp)
                       : reinterpret_cast<int4*>(slot_b + W * kRing * kWarp);
   unsigned long long* mb_full = reinterpret_cast<unsigned long long*>(slot_h + W * kRing);
@@ -889,14 +892,15 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   }
   unsigned ring_par = WS ? (warp < W ? 0u : (1u << kRing) - 1u) : 0u;   // per-slot wait parities (producers start at 1)
   for (int i = tid; i < n_out; i += nthr) row[i] = 0.0f;
-  for (int i = tid; i < W * kTileAlloc * kWarp; i += nthr) tiles[i] = 0.0f;
+  for (int i = tid; i < W * kTile * kWarp + kDumpFloats; i += nthr) tiles[i] = 0.0f;
   static_assert(kTile % 8 == 0, "8-sample blocks must not straddle the circular wrap");
   for (int i = tid; i < W * kTile; i += nthr) stage[i] = 0.0f;
 
   const Detector det = load_detector(det_pos, det_aux, j);
   DetDir dd{};
   if (DIR != kDirNone) dd = load_detdir(det_aux, j);
-  float* tile = tiles + (size_t)(warp < W ? warp : 0) * kTileAlloc * kWarp;
+  float* tile = tiles + (size_t)(warp < W ? warp : 0) * kTile * kWarp;
+  const int dumpq = (W - (warp < W ? warp : 0)) * (kTile / 4);   // the shared dump block, in this tile's quads
   const int64_t g_begin = (int64_t)part * groups_per_part;
   const int64_t g_end = min(n_groups, g_begin + groups_per_part);
   unsigned long long my_ops = 0;
@@ -973,7 +977,7 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
     const int NWB = nthr >> 5;
     const int pwarp = tid >> 5;
     int* const cnt = reinterpret_cast<int*>(tiles);   // [NWB][n_bins + 1]
-    const bool par_b = (size_t)NWB * (n_bins + 1) <= (size_t)W * kTileAlloc * kWarp;
+    const bool par_b = (size_t)NWB * (n_bins + 1) <= (size_t)W * kTile * kWarp;
     if (par_b) {
       const int sw = cgn * pwarp / NWB, ew = cgn * (pwarp + 1) / NWB;
       int* const myc = cnt + (size_t)pwarp * (n_bins + 1);
@@ -1152,13 +1156,13 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
           const float4 ra4 = slot_a[(warp * kRing + sl) * kWarp + lane];
           const float4 rb4 = slot_b[(warp * kRing + sl) * kWarp + lane];
           const int mode = h.w & 3;
-          float2 rc2;
-          if (DUAL && mode != 0) rc2 = slot_c[(warp * kRing + sl) * kWarp + lane];
+          float rc1;
+          if (DUAL && mode != 0) rc1 = slot_c[(warp * kRing + sl) * kWarp + lane];
           mbar_arrive(&mb_empty[warp * kRing + sl]);
           if (DUAL && mode != 0) {
-            // record (40 B per lane): a = (J0a | jha << 16, J0b | jhb << 16, mfa, nsca),
-            // b = (pssa, nlaa, mfb, nscb), c = (pssb, nlab), jh = 0xFFFF: empty;
-            // header (Lu | La, blo, ghi, mode | Lb << 16)
+            // record (36 B per lane): a = (J0a | jha << 16, J0b | jhb << 16,
+            // mfa | mfb << 16 (int16 m-offsets), nsca), b = (pssa, nlaa, nscb, pssb),
+            // c = nlab, jh = 0xFFFF: empty; header (Lu | La, blo, ghi, mode | Lb << 16)
             PROF_T(t_r2);
             make_room(h.y, h.z);
             PROF_ACC(pw_room, t_r2);
@@ -1169,21 +1173,23 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
 #endif
             PROF_T(t_k2);
             const unsigned wa_ = __float_as_uint(ra4.x), wb_ = __float_as_uint(ra4.y);
+            const unsigned wm_ = __float_as_uint(ra4.z);
+            const float mfa = (float)(int)(short)(wm_ & 0xFFFFu), mfb = (float)((int)wm_ >> 16);
             const int J0a = (int)(wa_ & 0xFFFFu), jha = (wa_ >> 16) == 0xFFFFu ? -1 : (int)(wa_ >> 16);
             const int J0b = (int)(wb_ & 0xFFFFu), jhb = (wb_ >> 16) == 0xFFFFu ? -1 : (int)(wb_ >> 16);
             if (mode == 1) {   // dual walk over the lane's union window
               if (h.x > 0) {
                 const int J0u = jha < 0 ? J0b : (jhb < 0 ? J0a : min(J0a, J0b));
-                const DWalk wa = make_dwalk(ra4.w, rb4.x, fs, rb4.y, ra4.z + (float)((J0u - J0a) * acq.f));
-                const DWalk wb = make_dwalk(rb4.w, rc2.x, fs, rc2.y, rb4.z + (float)((J0u - J0b) * acq.f));
-                rmw_walk_dual(tile, lane, J0u, (h.x + 3) & ~3, max(jha, jhb), fs, wa, wb);
+                const DWalk wa = make_dwalk(ra4.w, rb4.x, fs, rb4.y, mfa + (float)((J0u - J0a) * acq.f));
+                const DWalk wb = make_dwalk(rb4.z, rb4.w, fs, rc1, mfb + (float)((J0u - J0b) * acq.f));
+                rmw_walk_dual(tile, lane, J0u, (h.x + 3) & ~3, max(jha, jhb), fs, wa, wb, dumpq);
               }
             } else {           // the pair's windows lie far apart: two single walks
               const int La = h.x, Lb = h.w >> 16;
-              if (La > 0) rmw_walk<false>(tile, lane, J0a, (La + 3) & ~3, jha, ra4.z, fs,
-                                         make_walk(ra4.w, rb4.x, fs, rb4.y, 0.0f));
-              if (Lb > 0) rmw_walk<false>(tile, lane, J0b, (Lb + 3) & ~3, jhb, rb4.z, fs,
-                                         make_walk(rb4.w, rc2.x, fs, rc2.y, 0.0f));
+              if (La > 0) rmw_walk<false>(tile, lane, J0a, (La + 3) & ~3, jha, mfa, fs,
+                                         make_walk(ra4.w, rb4.x, fs, rb4.y, 0.0f), dumpq);
+              if (Lb > 0) rmw_walk<false>(tile, lane, J0b, (Lb + 3) & ~3, jhb, mfb, fs,
+                                         make_walk(rb4.z, rb4.w, fs, rc1, 0.0f), dumpq);
             }
             __syncwarp();
             PROF_ACC(pw_walk, t_k2);
@@ -1203,7 +1209,7 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
           if (h.x > 0)
 #endif
             rmw_walk<MASK>(tile, lane, __float_as_int(ra4.x), (h.x + 3) & ~3, __float_as_int(ra4.y), ra4.z, fs,
-                           make_walk(ra4.w, rb4.x, fs, rb4.y, rb4.z));
+                           make_walk(ra4.w, rb4.x, fs, rb4.y, rb4.z), dumpq);
           __syncwarp();
           PROF_ACC(pw_walk, t_k);
         }
@@ -1247,7 +1253,7 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
             if (h == 1 && !two) break;
             const int blo = h ? blob : bloa, ghi = h ? ghib : ghia;
             make_room(blo, ghi);
-            pair_walk<MASK>(tile, lane, acq, h ? pb : pa, (int)((h ? wordb : worda) >> 31), my_ops, blo);
+            pair_walk<MASK>(tile, lane, acq, h ? pb : pa, (int)((h ? wordb : worda) >> 31), my_ops, blo, dumpq);
             __syncwarp();
           }
         }
@@ -1309,7 +1315,7 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
             B1 = rb[g0 * kWarp + (ids >> 8)];
           }
         };
-        auto publish = [&](int i, int mode, int x, int blo, int ghi, int hw, float4 va, float4 vb, float2 vc) {
+        auto publish = [&](int i, int mode, int x, int blo, int ghi, int hw, float4 va, float4 vb, float vc) {
           const int sl = i % kRing;
           PROF_T(t_pw);
           mbar_wait_backoff(&mb_empty[w * kRing + sl], (ring_par >> sl) & 1u);
@@ -1354,6 +1360,9 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
             float4* const pt = reinterpret_cast<float4*>(hist) + (size_t)(w * kWarp + lane) * 2;
             pt[0] = make_float4(gdB_l.Sx, gdB_l.Sy, gdB_l.Sz, gdB_l.Sn);
             pt[1] = make_float4(gdB_l.isn, gdB_l.phg, __int_as_float(gdB_l.kg), 0.0f);
+            float4* const pa = reinterpret_cast<float4*>(hist) + (size_t)((W + w) * kWarp + lane) * 2;
+            pa[0] = make_float4(gdA_l.Sx, gdA_l.Sy, gdA_l.Sz, gdA_l.Sn);
+            pa[1] = make_float4(gdA_l.isn, gdA_l.phg, __int_as_float(gdA_l.kg), __uint_as_float(word_l));
           }
           __syncwarp();
           PROF_ACC(pp_geo, t_g);
@@ -1390,8 +1399,16 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
                 idn2 = pn2 ? load_ids(gn2, cn2) : 0u;
               }
             }
-            const GroupDet gA = shfl_gd_fast(gdA_l, k);
-            const unsigned word = __shfl_sync(0xffffffffu, word_l, k);
+            GroupDet gA;
+            unsigned word;
+            {
+              const float4* const pa = reinterpret_cast<const float4*>(hist) + (size_t)((W + w) * kWarp + k) * 2;
+              const float4 a = pa[0], b = pa[1];
+              gA.Sx = a.x; gA.Sy = a.y; gA.Sz = a.z; gA.Sn = a.w;
+              gA.isn = b.x; gA.phg = b.y; gA.kg = __float_as_int(b.z);
+              gA.slow = 0;
+              word = __float_as_uint(b.w);
+            }
             const int blo = (int)(word & 0xFFFFu) << kBinShift;
             const int ghi = blo + (int)((word >> 16) & 0x7FFFu);
             PROF_T(t_s);
@@ -1407,7 +1424,7 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
               publish(i0 + k, 0, p.L, blo, ghi, 0,
                       make_float4(__int_as_float(p.J0), __int_as_float(empty_u ? -1 : p.jhi),
                                   (float)(p.J0 * acq.f - p.kc), -p.sc * sg),
-                      make_float4(p.phi * p.sc * sg, nla, p.qmax + nla, 0.0f), make_float2(0.f, 0.f));
+                      make_float4(p.phi * p.sc * sg, nla, p.qmax + nla, 0.0f), 0.0f);
               continue;
             }
             GroupDet gB;
@@ -1452,10 +1469,16 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
 #ifdef PAB_FWD_PROF
             pp_setup += clock64() - t_s;
 #endif
+            // m-offsets as int16 (exact small integers: the unit fits the tile;
+            // an empty ball's is unused)
+            const int mia = min(max((int)mfa, -32768), 32767), mib = min(max((int)mfb, -32768), 32767);
+            PAB_CHECK(ea || (float)mia == mfa);
+            PAB_CHECK(eb || (float)mib == mfb);
             publish(i0 + k, ok ? 1 : 2, ok ? Lu : La, blo, ghi, ok ? 0 : Lb,
                     make_float4(__uint_as_float((unsigned)J0a | ((unsigned)jha << 16)),
-                                __uint_as_float((unsigned)J0b | ((unsigned)jhb << 16)), mfa, nsca),
-                    make_float4(pssa, nlaa, mfb, nscb), make_float2(pssb, nlab));
+                                __uint_as_float((unsigned)J0b | ((unsigned)jhb << 16)),
+                                __uint_as_float(((unsigned)mia & 0xFFFFu) | ((unsigned)mib << 16)), nsca),
+                    make_float4(pssa, nlaa, nscb, pssb), nlab);
           }
         }
       } else
@@ -1620,10 +1643,10 @@ __global__ void decimate_kernel(const float* __restrict__ src, int n_rows, int n
 size_t forward_smem(int n_out, int warps, bool srow, bool dual) {
   const size_t n_bins = (size_t)((n_out + (1 << kBinShift) - 1) >> kBinShift);
   const size_t row_bytes = srow ? (size_t)((n_out + 3) & ~3) * 4 : 0;
-  const size_t rec_bytes = dual ? 40 : 32;   // hand-off record per lane and ring slot
+  const size_t rec_bytes = dual ? 36 : 32;   // hand-off record per lane and ring slot
   const size_t ring = kWS ? 16 + (size_t)warps * kRing * (rec_bytes * kWarp + 16 + 2 * 8) : 0;
   const size_t units = kChunk;
-  return row_bytes + (size_t)warps * kTileAlloc * kWarp * 4 + (size_t)warps * kTile * 4 +
+  return row_bytes + ((size_t)warps * kTile * kWarp + kDumpFloats) * 4 + (size_t)warps * kTile * 4 +
          (size_t)hist_ints((int)n_bins, warps, dual) * 4 + (size_t)(warps + 1) * 4 + 16 + 2 * units * 2 + 16 + ring;
 }
 
