@@ -1359,7 +1359,10 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
           {
             float4* const pt = reinterpret_cast<float4*>(hist) + (size_t)(w * kWarp + lane) * 2;
             pt[0] = make_float4(gdB_l.Sx, gdB_l.Sy, gdB_l.Sz, gdB_l.Sn);
-            pt[1] = make_float4(gdB_l.isn, gdB_l.phg, __int_as_float(gdB_l.kg), 0.0f);
+            // (.w: the entry's chunk slot | direction cell << 16 | pair << 31)
+            pt[1] = make_float4(gdB_l.isn, gdB_l.phg, __int_as_float(gdB_l.kg),
+                                __uint_as_float((unsigned)(g_l - cg0) | ((unsigned)cell_l << 16) |
+                                                (word_l & 0x80000000u)));
             float4* const pa = reinterpret_cast<float4*>(hist) + (size_t)((W + w) * kWarp + lane) * 2;
             pa[0] = make_float4(gdA_l.Sx, gdA_l.Sy, gdA_l.Sz, gdA_l.Sn);
             pa[1] = make_float4(gdA_l.isn, gdA_l.phg, __int_as_float(gdA_l.kg), __uint_as_float(word_l));
@@ -1367,10 +1370,12 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
           __syncwarp();
           PROF_ACC(pp_geo, t_g);
           // two-stage prefetch: pairing ids two entries ahead, records one ahead
-          auto entry = [&](int k, int64_t& g0, bool& pair, int& cell) {
-            g0 = __shfl_sync(0xffffffffu, g_l, k);
-            pair = __shfl_sync(0xffffffffu, word_l, k) >> 31;
-            cell = __shfl_sync(0xffffffffu, cell_l, k);
+          auto entry = [&](int k, int64_t& g0, bool& pair, int& cell) {   // from the table (no shuffles)
+            const unsigned v =
+                __float_as_uint((reinterpret_cast<const float4*>(hist) + (size_t)(w * kWarp + k) * 2 + 1)->w);
+            g0 = cg0 + (int64_t)(v & 0x7FFFu);
+            cell = (int)((v >> 16) & 63u);
+            pair = (v >> 31) != 0;
           };
           int64_t gn, gn2 = 0;
           bool pn, pn2 = false;
