@@ -606,7 +606,8 @@ constexpr bool kWS = PAB_FWD_WS != 0;
 // read by broadcast LDS.128 instead of 7-8 shuffles per group.
 constexpr int kPTabWords = 8;
 __host__ __device__ inline int hist_ints(int n_bins, int warps, bool dual) {
-  const int t = dual ? 2 * warps * kWarp * kPTabWords : 0;
+  // dual: two groups per entry; single-group sweeps: geometry + word + slot (12 words)
+  const int t = dual ? 2 * warps * kWarp * kPTabWords : warps * kWarp * 12;
   return n_bins + 1 > t ? n_bins + 1 : t;
 }
 
@@ -1495,19 +1496,42 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
         PROF_T(t_g);
         batch_geometry(i0, nb, gd_l, g_l, word_l);
         PROF_ACC(pp_geo, t_g);
-        int64_t ga = __shfl_sync(0xffffffffu, g_l, 0), gb = __shfl_sync(0xffffffffu, g_l, min(1, nb - 1));
+        // the batch in a shared-memory table (the histogram's space during
+        // the sweep): geometry, word and slot by broadcast LDS.128, no shuffles
+        __syncwarp();
+        {
+          float4* const pt = reinterpret_cast<float4*>(hist) + (size_t)(w * kWarp + lane) * 3;
+          pt[0] = make_float4(gd_l.Sx, gd_l.Sy, gd_l.Sz, gd_l.Sn);
+          pt[1] = make_float4(gd_l.isn, gd_l.phg, __int_as_float(gd_l.kg), __uint_as_float(word_l));
+          pt[2] = make_float4(__int_as_float((int)(g_l - cg0)), 0.0f, 0.0f, 0.0f);
+        }
+        __syncwarp();
+        auto tgd = [&](int k, unsigned& word) {
+          const float4* const pt = reinterpret_cast<const float4*>(hist) + (size_t)(w * kWarp + k) * 3;
+          const float4 a = pt[0], b = pt[1];
+          GroupDet gd;
+          gd.Sx = a.x; gd.Sy = a.y; gd.Sz = a.z; gd.Sn = a.w;
+          gd.isn = b.x; gd.phg = b.y; gd.kg = __float_as_int(b.z);
+          gd.slow = 0;
+          word = __float_as_uint(b.w);
+          return gd;
+        };
+        auto tg = [&](int k) -> int64_t {
+          return cg0 + __float_as_int((reinterpret_cast<const float4*>(hist) + (size_t)(w * kWarp + k) * 3 + 2)->x);
+        };
+        int64_t ga = tg(0), gb = tg(min(1, nb - 1));
         BallA Aa = ra[ga * kWarp + lane], Ab = ra[gb * kWarp + lane];
         BallB Ba = rb[ga * kWarp + lane], Bb = rb[gb * kWarp + lane];
         for (int k = 0; k < nb; k += 2) {
           const bool two = k + 1 < nb;
           const int kb = two ? k + 1 : k;
-          const GroupDet gda = shfl_gd_fast(gd_l, k), gdb = shfl_gd_fast(gd_l, kb);
-          const unsigned worda = __shfl_sync(0xffffffffu, word_l, k), wordb = __shfl_sync(0xffffffffu, word_l, kb);
+          unsigned worda, wordb;
+          const GroupDet gda = tgd(k, worda), gdb = tgd(kb, wordb);
           const BallA A0 = Aa, A1 = Ab;
           const BallB B0 = Ba, B1 = Bb;
           if (k + 2 < nb) {
-            ga = __shfl_sync(0xffffffffu, g_l, k + 2);
-            gb = __shfl_sync(0xffffffffu, g_l, min(k + 3, nb - 1));
+            ga = tg(k + 2);
+            gb = tg(min(k + 3, nb - 1));
             Aa = ra[ga * kWarp + lane];
             Ab = ra[gb * kWarp + lane];
             Ba = rb[ga * kWarp + lane];
