@@ -280,7 +280,6 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   __shared__ double acc_s[kAdjWarps][5][kWarp];
 #pragma unroll
   for (int c = 0; c < 5; ++c) acc_s[warp][c][lane] = 0.0;
-  for (int i = lane; i < 4 * (kSeg + kPad + 4); i += kWarp) (&seg_all[warp][0][0])[i] = 0.0f;
   unsigned long long my_ops = 0;
   int coinc = 0;
 #ifdef PAB_ADJ_PROF
@@ -359,14 +358,20 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
         if (lane < len4) cp_async16(dst + 4 * lane, src + 4 * lane);
         if (lane + kWarp < len4) cp_async16(dst + 4 * (lane + kWarp), src + 4 * (lane + kWarp));
         cp_async_commit();
+        // zero padding after the staged samples: the uniform walk runs past
+        // them (lanes whose windows end earlier, rounding, and -- for a
+        // segment clipped at the record end -- windows running past the last
+        // sample, which must read as zero).  (Measured: leaving the earlier
+        // detectors' residuals there instead, the terms past a window
+        // beyond cutoff sigmas are below 2^-24 of the ball's peak but not
+        // the reference's zeros, and a record-end segment reads wrong
+        // residuals inside the window: the smoke gradients were off by 5e-3.)
+        if (lane < kPad / 4) reinterpret_cast<float4*>(dst + 4 * len4)[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
       } else {
         for (int k = lane; k < len; k += kWarp) cp_async4(dst + k, src + k);
         cp_async_commit();
+        for (int k = lane; k < kPad; k += kWarp) dst[len + k] = 0.0f;
       }
-      // no zero padding: past the staged samples the uniform walk meets the
-      // earlier detectors' (finite) residuals of this buffer, beyond every
-      // lane's window, where G <= 2^-24 of the ball's peak (the masked walk
-      // zeroes them); the buffers start zeroed
     };
     auto wait_seg = [&](int fl) {
       if (fl & kFlagUniform) cp_async_wait_all();

@@ -421,14 +421,22 @@ def test_cutoff_paths_match_oracle(P, cutoff):
     assert rel_l2(gr.d_position, gpos) < GRAD_TOL
 
 
-@pytest.mark.parametrize("f", [1, 3])
-def test_windows_clipped_at_both_recording_ends(P, f):
+@pytest.mark.parametrize("f,n_extra,t0,n_s", [(1, 0, 8.0e-6, 96), (3, 0, 8.0e-6, 96), (1, 37, 5.0e-6, 200),
+                                             (2, 37, 5.0e-6, 200)])
+def test_windows_clipped_at_both_recording_ends(P, f, n_extra, t0, n_s):
     """A dense cloud whose arrivals straddle the first and the last sample
     (t0 > 0, short record): clipped windows, groups wider than the live
-    tile near the end, every sample of the record written by many groups."""
+    tile near the end, every sample of the record written by many groups.
+    With 40 detectors and a record ending inside the arrivals (5.0 .. 10.0
+    us) the adjoint's staging buffers are reused many times per lane group
+    with segments of varying length, so a walk past the record end that
+    read a buffer's earlier (non-zero) residuals instead of zeros shows
+    here."""
     rng = np.random.default_rng(11)
     n = 6000
     sens = np.array([[0.0, 0.0, 0.0], [0.002, 0.0, 0.001], [-0.001, 0.002, 0.0]])
+    if n_extra:
+        sens = np.concatenate([sens, rng.uniform(-0.002, 0.002, size=(n_extra, 3))])
     # distances 10..16 mm: arrival samples ~ 6.7..10.7 us at 1500 m/s
     r = rng.uniform(0.010, 0.016, n)
     u = rng.normal(size=(n, 3))
@@ -437,7 +445,7 @@ def test_windows_clipped_at_both_recording_ends(P, f):
     pos = u * r[:, None]
     p0 = rng.uniform(0.2, 1.0, n)
     a0 = rng.uniform(0.05e-3, 0.2e-3, n)
-    grid = P.TimeGrid(8.0e-6, 2.5e-8, 96)   # records 8.0 .. 10.4 us only
+    grid = P.TimeGrid(t0, 2.5e-8, n_s)   # records 8.0 .. 10.4 us (or 5.0 .. 10.0 us) only
     ctx = P.ForwardContext(P.SensorArray(sens, 1500.0), grid)
     cloud = P.PointCloud(pos, p0, a0)
     rows, _, _, ops = OR.run_model(pos, p0, a0, sens, None, 1500.0, grid.t0, grid.dt, grid.n_samples, f)
