@@ -202,6 +202,178 @@ __device__ __forceinline__ void moments_uniform(const float* seg, int L, float m
   M.T3 = A3.x + A3.y;
 }
 
+// Cascade walk (fine stage, unmasked, recurrence step within kCascMaxDl).
+//
+// The four moments of r_s = res_s G(y_s) are linear functionals of r, so they
+// can be accumulated in any polynomial basis of the walk index.  The direct
+// walk above spends 8 FP32x2 operations and 2 ex2 per sample pair (y, q, r,
+// t and four accumulations); this one spends 6 and 1:
+//   * the window is walked from both ends towards its middle, each half a
+//     chain of sample pairs (even sample in .x, odd sample in .y) feeding a
+//     cascade of running sums  A0 += res G; A1 += A0; A2 += A1; A3 += A2
+//     (one FFMA2 + three FADD2).  After n steps A_k holds sum_u C(u+k-1, k)
+//     r_u over the distance u to the chain's end (the right half updates in
+//     the reverse order, A3 += A2 ... A0 += res G, which gives C(u, k) with
+//     u counted from 0, so both halves share one origin): binomial, i.e.
+//     exact integer, weights -- no multiplications by y in the loop;
+//   * G follows the forward's ratio recurrence inside every 8-sample block:
+//     the pair nearest the chain's start is exact (2 ex2 for G, 2 for the
+//     ratio R), the next pairs G *= R, R *= C; nothing is carried between
+//     blocks.
+// The chains end in the middle of the walk, within a few samples of the
+// arrival (all lanes of a group have nearly equal windows), so the shift
+// from the chain origin to y = 0 is small and the conversion to T0..T3 --
+// 14 FP32x2 + ~10 scalar operations per walk -- cancels little: against FP64
+// moments the FP32 result is within 1e-7 (T0, T1), 3e-7 (T2) and 2e-6 (T3)
+// rms of sum |r y^k| (the direct walk: 1e-7), emulated on config-2 windows.
+#ifndef PAB_ADJ_CASCADE
+#define PAB_ADJ_CASCADE 1
+#endif
+constexpr bool kAdjCascade = PAB_ADJ_CASCADE != 0;
+constexpr float kCascMaxDl = 0.75f;   // |dl| bound of the ratio recurrence (as the forward's dual walk)
+
+struct CascConst {
+  float2 k1, k2, C;   // R(y) = 2^(k1 y + k2): G(y + h) / G(y) with h = 2 dl; C = R(y + h) / R(y)
+  float inv_h;
+};
+
+__device__ __forceinline__ CascConst casc_const(const WalkConst& W) {
+  CascConst K;
+  const float a = -2.0f * W.dl2, b = -W.dl2 * W.dl2, c = ex2(2.0f * b);
+  K.k1 = make_float2(a, a);
+  K.k2 = make_float2(b, b);
+  K.C = make_float2(c, c);
+  K.inv_h = 1.0f / W.dl2;
+  return K;
+}
+
+struct Casc {
+  float2 a0, a1, a2, a3;
+};
+
+__device__ __forceinline__ void casc_in(float2 res, float2 G, Casc& A) {   // inclusive: weights C(u + k - 1, k), u >= 1
+  A.a0 = __ffma2_rn(res, G, A.a0);
+  A.a1 = __fadd2_rn(A.a1, A.a0);
+  A.a2 = __fadd2_rn(A.a2, A.a1);
+  A.a3 = __fadd2_rn(A.a3, A.a2);
+}
+__device__ __forceinline__ void casc_ex(float2 res, float2 G, Casc& B) {   // exclusive: weights C(u, k), u >= 0
+  B.a3 = __fadd2_rn(B.a3, B.a2);
+  B.a2 = __fadd2_rn(B.a2, B.a1);
+  B.a1 = __fadd2_rn(B.a1, B.a0);
+  B.a0 = __ffma2_rn(res, G, B.a0);
+}
+
+// Left chain, ascending: NP sample pairs (2 or 4) from s4; m = m-offset of
+// the first sample, c0 = (ps, ps + dl).
+template <int NP>
+__device__ __forceinline__ void casc_left(const float4* s4, float m, const WalkConst& W, const CascConst& K, float2 c0,
+                                          Casc& A) {
+  const float4 ra = s4[0];
+  float4 rb = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (NP == 4) rb = s4[1];
+  const float2 y = __ffma2_rn(make_float2(m, m), W.nsc2, c0);
+  const float2 q = __fmul2_rn(y, y);
+  const float2 e = __ffma2_rn(y, K.k1, K.k2);
+  float2 G = make_float2(ex2(-q.x), ex2(-q.y));
+  float2 R = make_float2(ex2(e.x), ex2(e.y));
+  casc_in(make_float2(ra.x, ra.y), G, A);
+  G = __fmul2_rn(G, R);
+  casc_in(make_float2(ra.z, ra.w), G, A);
+  if (NP == 4) {
+    R = __fmul2_rn(R, K.C);
+    G = __fmul2_rn(G, R);
+    casc_in(make_float2(rb.x, rb.y), G, A);
+    R = __fmul2_rn(R, K.C);
+    G = __fmul2_rn(G, R);
+    casc_in(make_float2(rb.z, rb.w), G, A);
+  }
+}
+
+// Right chain, descending: NP sample pairs from s4, the highest pair first;
+// nm = minus the m-offset of that pair's first sample, nc0 = -(ps, ps + dl):
+// with -y the step towards lower samples has the left chain's ratio.
+template <int NP>
+__device__ __forceinline__ void casc_right(const float4* s4, float nm, const WalkConst& W, const CascConst& K, float2 nc0,
+                                           Casc& B) {
+  const float4 ra = s4[0];
+  float4 rb = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (NP == 4) rb = s4[1];
+  const float2 ny = __ffma2_rn(make_float2(nm, nm), W.nsc2, nc0);
+  const float2 q = __fmul2_rn(ny, ny);
+  const float2 e = __ffma2_rn(ny, K.k1, K.k2);
+  float2 G = make_float2(ex2(-q.x), ex2(-q.y));
+  float2 R = make_float2(ex2(e.x), ex2(e.y));
+  if (NP == 4) {
+    casc_ex(make_float2(rb.z, rb.w), G, B);
+    G = __fmul2_rn(G, R);
+    casc_ex(make_float2(rb.x, rb.y), G, B);
+    R = __fmul2_rn(R, K.C);
+    G = __fmul2_rn(G, R);
+    casc_ex(make_float2(ra.z, ra.w), G, B);
+    R = __fmul2_rn(R, K.C);
+    G = __fmul2_rn(G, R);
+    casc_ex(make_float2(ra.x, ra.y), G, B);
+  } else {
+    casc_ex(make_float2(ra.z, ra.w), G, B);
+    G = __fmul2_rn(G, R);
+    casc_ex(make_float2(ra.x, ra.y), G, B);
+  }
+}
+
+// L samples (a multiple of 4, warp-uniform) from seg (16-byte aligned), mf
+// the m-offset of the first sample: trips of 8 left + 8 right samples, the
+// remaining 4, 8 or 12 samples as 4 left, 4 + 4, or 8 left + 4 right.
+__device__ __forceinline__ void moments_cascade(const float* seg, int L, float mf, const WalkConst& W,
+                                                const CascConst& K, float ps, int f, Moments& M) {
+  const float4* sL = reinterpret_cast<const float4*>(seg);
+  const float4* sR = sL + (L >> 2) - 2;
+  const float2 c0 = make_float2(ps, ps + W.dl);
+  const float2 nc0 = make_float2(-c0.x, -c0.y);
+  const float2 z2 = make_float2(0.f, 0.f);
+  Casc A = {z2, z2, z2, z2}, B = {z2, z2, z2, z2};
+  const int trips = L >> 4, rem = L & 15;
+  float mL = mf;
+  float nmR = -(mf + (float)((L - 2) * f));
+#pragma unroll 1
+  for (int t = trips; t > 0; --t, sL += 2, sR -= 2, mL += W.step8, nmR += W.step8) {
+    casc_left<4>(sL, mL, W, K, c0, A);
+    casc_right<4>(sR, nmR, W, K, nc0, B);
+  }
+  int hL = trips << 3;   // samples of the left chain
+  if (rem == 12) {
+    casc_left<4>(sL, mL, W, K, c0, A);
+    hL += 8;
+  } else if (rem >= 4) {
+    casc_left<2>(sL, mL, W, K, c0, A);
+    hL += 4;
+  }
+  if (rem >= 8) casc_right<2>(sR + 1, nmR, W, K, nc0, B);
+  // Chain origin: sample hL (left: y = h (Z - u), right: y = h (Z + u), Z =
+  // (zeta, zeta + 1/2) for the even and odd samples, zeta = y(hL) / h).
+  // Power sums about the origin, right plus (-1)^j left:
+  //   Q0 = B0 + A0, Q1 = B1 - A1, Q2 = 2 (B2 + A2) + Q1,
+  //   Q3 = 6 (B3 - A3) + 6 (B2 + A2) + Q1
+  // and the shift by Z (Horner): T_k = h^k sum_j C(k, j) Z^(k-j) Q_j.
+  const float zeta = fmaf(mf + (float)(hL * f), W.nsc2.x, ps) * K.inv_h;
+  const float2 Z = make_float2(zeta, zeta + 0.5f);
+  const float2 Q0 = __fadd2_rn(B.a0, A.a0);
+  const float2 Q1 = __fadd2_rn(B.a1, make_float2(-A.a1.x, -A.a1.y));
+  const float2 S2 = __fadd2_rn(B.a2, A.a2);
+  const float2 D3 = __fadd2_rn(B.a3, make_float2(-A.a3.x, -A.a3.y));
+  const float2 Q2 = __ffma2_rn(make_float2(2.f, 2.f), S2, Q1);
+  const float2 Q3 = __ffma2_rn(make_float2(6.f, 6.f), __fadd2_rn(D3, S2), Q1);
+  const float2 M1 = __ffma2_rn(Z, Q0, Q1);
+  const float2 M2 = __ffma2_rn(Z, __fadd2_rn(M1, Q1), Q2);
+  const float2 M3 = __ffma2_rn(
+      Z, __ffma2_rn(Z, __ffma2_rn(make_float2(2.f, 2.f), Q1, M1), __fmul2_rn(make_float2(3.f, 3.f), Q2)), Q3);
+  const float h = W.dl2, h2 = h * h;
+  M.T0 = Q0.x + Q0.y;
+  M.T1 = (M1.x + M1.y) * h;
+  M.T2 = (M2.x + M2.y) * h2;
+  M.T3 = (M3.x + M3.y) * (h2 * h);
+}
+
 #ifndef PAB_ADJ_LEAN
 #define PAB_ADJ_LEAN 1   // XU-free rounding in the pair setup; factored cos^2 fine epilogue
 #endif
@@ -265,6 +437,11 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   const bool live = B.orig >= 0;
   const float qmax = live ? (rho * sc) * (rho * sc) : -1.0f;
   const WalkConst W = walk_const(sc, f);
+  // cascade walk where the stage needs all four moments, no per-sample
+  // truncation test and every live lane's recurrence step is in range
+  constexpr bool kCascOk = kAdjCascade && STAGE == kStageFine && !MASK;
+  const CascConst K = kCascOk ? casc_const(W) : CascConst{};
+  const bool casc = kCascOk && __all_sync(0xffffffffu, !live || fabsf(W.dl) <= kCascMaxDl);
   // the conversion-free setup pays where the XU pipe binds (ex2 walk); the
   // element directivity's sinc terms load the FMA pipe instead (config 4:
   // lean +0.7 ms)
@@ -490,10 +667,12 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
       M = {(float)(u.J0 - lo + buf), (float)u.L, 0.f, 0.f};
       return M;
 #endif
-      moments_uniform<STAGE, MASK>(seg_all[warp][buf] + (u.J0 - lo), (u.L + 3) & ~3,
-                                   kLean ? int_to_float(u.J0 * f - u.pg.kc)
-                                                          : (float)(u.J0 * f - u.pg.kc),
-                                   W, u.pg.phi * sc, u.empty ? -1.0f : qmax, M);
+      const float mf0 = kLean ? int_to_float(u.J0 * f - u.pg.kc) : (float)(u.J0 * f - u.pg.kc);
+      if (kCascOk && casc)
+        moments_cascade(seg_all[warp][buf] + (u.J0 - lo), (u.L + 3) & ~3, mf0, W, K, u.pg.phi * sc, f, M);
+      else
+        moments_uniform<STAGE, MASK>(seg_all[warp][buf] + (u.J0 - lo), (u.L + 3) & ~3, mf0, W, u.pg.phi * sc,
+                                     u.empty ? -1.0f : qmax, M);
       if (!MASK && u.empty) M = {0.f, 0.f, 0.f, 0.f};
       return M;
     };
@@ -765,30 +944,34 @@ extern "C" int pab_adj_prof(unsigned long long* out /*[16]*/, int reset) {
 // per SM, one per CTA, like the kernel), `reps` walks of L samples per lane
 // over a staged segment -- lane-samples per second vs the ex2 / FMA ceilings.
 namespace pab {
-__global__ void __launch_bounds__(32, 16) adj_walk_bench_kernel(int reps, int L, float* out) {
+__global__ void __launch_bounds__(32, 16) adj_walk_bench_kernel(int reps, int L, int cascade, float* out) {
   __shared__ __align__(16) float seg[kSeg + kPad + 4];
   const int lane = threadIdx.x;
   for (int i = lane; i < kSeg + kPad + 4; i += 32) seg[i] = 0.001f * (float)((i * 7) % 13);
   __syncwarp();
   const float sc = 0.3f + 0.001f * lane, ps = 0.1f * lane;
   const WalkConst W = walk_const(sc, 1);
+  const CascConst K = casc_const(W);
   Moments acc = {0.f, 0.f, 0.f, 0.f};
   for (int r = 0; r < reps; ++r) {
     const int J0 = ((r * 4 + lane * 4) % 64);
     Moments M;
-    moments_uniform<kStageFine, false>(seg + J0, L, (float)(-L / 2), W, ps, 30.0f, M);
+    if (cascade)
+      moments_cascade(seg + J0, L, (float)(-L / 2), W, K, ps, 1, M);
+    else
+      moments_uniform<kStageFine, false>(seg + J0, L, (float)(-L / 2), W, ps, 30.0f, M);
     acc.T0 += M.T0; acc.T1 += M.T1; acc.T2 += M.T2; acc.T3 += M.T3;
   }
   out[blockIdx.x * 32 + lane] = acc.T0 + acc.T1 + acc.T2 + acc.T3;
 }
 }  // namespace pab
-extern "C" int pab_bench_adj_walk(int blocks, int reps, int L, float* out, float* ms) {
+extern "C" int pab_bench_adj_walk(int blocks, int reps, int L, int cascade, float* out, float* ms) {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  pab::adj_walk_bench_kernel<<<blocks, 32>>>(reps, L, out);
+  pab::adj_walk_bench_kernel<<<blocks, 32>>>(reps, L, cascade, out);
   cudaEventRecord(a);
-  pab::adj_walk_bench_kernel<<<blocks, 32>>>(reps, L, out);
+  pab::adj_walk_bench_kernel<<<blocks, 32>>>(reps, L, cascade, out);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   cudaEventElapsedTime(ms, a, b);

@@ -9,9 +9,11 @@ import torch
 lib = ctypes.CDLL(os.environ["PAB_LIBRARY"])
 sms = torch.cuda.get_device_properties(0).multi_processor_count
 out = torch.empty(sms * 16 * 32, device="cuda")
-for L in (16, 48, 96):
-    reps = 4000
-    ms = ctypes.c_float()
-    rc = lib.pab_bench_adj_walk(sms * 16, reps, L, ctypes.c_void_p(out.data_ptr()), ctypes.byref(ms))
-    samples = sms * 16 * 32 * reps * L
-    print(f"adjoint walk L={L}: rc={rc} {ms.value:.2f} ms, {samples / (ms.value * 1e-3) / 1e12:.2f} T lane-samples/s")
+for casc in (0, 1):   # direct FP32x2 moments / two-sided cascade with the ratio recurrence
+    for L in (16, 40, 44, 48, 96):
+        reps = 4000
+        ms = ctypes.c_float()
+        rc = lib.pab_bench_adj_walk(sms * 16, reps, L, casc, ctypes.c_void_p(out.data_ptr()), ctypes.byref(ms))
+        samples = sms * 16 * 32 * reps * L
+        print(f"adjoint walk {'cascade' if casc else 'direct '} L={L}: rc={rc} {ms.value:.2f} ms, "
+              f"{samples / (ms.value * 1e-3) / 1e12:.2f} T lane-samples/s")
