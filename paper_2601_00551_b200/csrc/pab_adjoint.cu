@@ -231,6 +231,7 @@ __device__ __forceinline__ void moments_uniform(const float* seg, int L, float m
 #endif
 constexpr bool kAdjCascade = PAB_ADJ_CASCADE != 0;
 constexpr float kCascMaxDl = 0.75f;   // |dl| bound of the ratio recurrence (as the forward's dual walk)
+constexpr float kCascMaxExp = 100.0f; // bound on |k1 y|: the ratio stays below 2^127
 
 struct CascConst {
   float2 k1, k2, C;   // R(y) = 2^(k1 y + k2): G(y + h) / G(y) with h = 2 dl; C = R(y + h) / R(y)
@@ -266,7 +267,7 @@ __device__ __forceinline__ void casc_ex(float2 res, float2 G, Casc& B) {   // ex
 
 // Left chain, ascending: NP sample pairs (2 or 4) from s4; m = m-offset of
 // the first sample, c0 = (ps, ps + dl).
-template <int NP>
+template <int NP, bool FIRST = false>
 __device__ __forceinline__ void casc_left(const float4* s4, float m, const WalkConst& W, const CascConst& K, float2 c0,
                                           Casc& A) {
   const float4 ra = s4[0];
@@ -277,7 +278,14 @@ __device__ __forceinline__ void casc_left(const float4* s4, float m, const WalkC
   const float2 e = __ffma2_rn(y, K.k1, K.k2);
   float2 G = make_float2(ex2(-q.x), ex2(-q.y));
   float2 R = make_float2(ex2(e.x), ex2(e.y));
-  casc_in(make_float2(ra.x, ra.y), G, A);
+  if (FIRST) {   // the chain's first step on zero sums: no additions (and no zero registers)
+    A.a0 = __fmul2_rn(make_float2(ra.x, ra.y), G);
+    A.a1 = A.a0;
+    A.a2 = A.a0;
+    A.a3 = A.a0;
+  } else {
+    casc_in(make_float2(ra.x, ra.y), G, A);
+  }
   G = __fmul2_rn(G, R);
   casc_in(make_float2(ra.z, ra.w), G, A);
   if (NP == 4) {
@@ -293,9 +301,10 @@ __device__ __forceinline__ void casc_left(const float4* s4, float m, const WalkC
 // Right chain, descending: NP sample pairs from s4, the highest pair first;
 // nm = minus the m-offset of that pair's first sample, nc0 = -(ps, ps + dl):
 // with -y the step towards lower samples has the left chain's ratio.
-template <int NP>
+template <int NP, bool FIRST = false>
 __device__ __forceinline__ void casc_right(const float4* s4, float nm, const WalkConst& W, const CascConst& K, float2 nc0,
                                            Casc& B) {
+  static_assert(!FIRST || NP == 4, "only a full block opens a chain");
   const float4 ra = s4[0];
   float4 rb = make_float4(0.f, 0.f, 0.f, 0.f);
   if (NP == 4) rb = s4[1];
@@ -304,7 +313,25 @@ __device__ __forceinline__ void casc_right(const float4* s4, float nm, const Wal
   const float2 e = __ffma2_rn(ny, K.k1, K.k2);
   float2 G = make_float2(ex2(-q.x), ex2(-q.y));
   float2 R = make_float2(ex2(e.x), ex2(e.y));
-  if (NP == 4) {
+  if (FIRST) {
+    // the chain's first four steps on zero sums: the sum of order k stays
+    // zero until step k + 1 (9 of the 12 additions drop out)
+    B.a0 = __fmul2_rn(make_float2(rb.z, rb.w), G);
+    G = __fmul2_rn(G, R);
+    B.a1 = B.a0;
+    B.a0 = __ffma2_rn(make_float2(rb.x, rb.y), G, B.a0);
+    R = __fmul2_rn(R, K.C);
+    G = __fmul2_rn(G, R);
+    B.a2 = B.a1;
+    B.a1 = __fadd2_rn(B.a1, B.a0);
+    B.a0 = __ffma2_rn(make_float2(ra.z, ra.w), G, B.a0);
+    R = __fmul2_rn(R, K.C);
+    G = __fmul2_rn(G, R);
+    B.a3 = B.a2;
+    B.a2 = __fadd2_rn(B.a2, B.a1);
+    B.a1 = __fadd2_rn(B.a1, B.a0);
+    B.a0 = __ffma2_rn(make_float2(ra.x, ra.y), G, B.a0);
+  } else if (NP == 4) {
     casc_ex(make_float2(rb.z, rb.w), G, B);
     G = __fmul2_rn(G, R);
     casc_ex(make_float2(rb.x, rb.y), G, B);
@@ -331,14 +358,22 @@ __device__ __forceinline__ void moments_cascade(const float* seg, int L, float m
   const float2 c0 = make_float2(ps, ps + W.dl);
   const float2 nc0 = make_float2(-c0.x, -c0.y);
   const float2 z2 = make_float2(0.f, 0.f);
-  Casc A = {z2, z2, z2, z2}, B = {z2, z2, z2, z2};
+  Casc A, B;
   const int trips = L >> 4, rem = L & 15;
   float mL = mf;
   float nmR = -(mf + (float)((L - 2) * f));
+  if (trips > 0) {   // the first trip opens both chains (no zero sums to add to)
+    casc_left<4, true>(sL, mL, W, K, c0, A);
+    casc_right<4, true>(sR, nmR, W, K, nc0, B);
+    sL += 2, sR -= 2, mL += W.step8, nmR += W.step8;
 #pragma unroll 1
-  for (int t = trips; t > 0; --t, sL += 2, sR -= 2, mL += W.step8, nmR += W.step8) {
-    casc_left<4>(sL, mL, W, K, c0, A);
-    casc_right<4>(sR, nmR, W, K, nc0, B);
+    for (int t = trips - 1; t > 0; --t, sL += 2, sR -= 2, mL += W.step8, nmR += W.step8) {
+      casc_left<4>(sL, mL, W, K, c0, A);
+      casc_right<4>(sR, nmR, W, K, nc0, B);
+    }
+  } else {           // walks shorter than 16 samples: the remainder blocks on zero sums
+    A = {z2, z2, z2, z2};
+    B = {z2, z2, z2, z2};
   }
   int hL = trips << 3;   // samples of the left chain
   if (rem == 12) {
@@ -441,7 +476,13 @@ adjoint_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
   // truncation test and every live lane's recurrence step is in range
   constexpr bool kCascOk = kAdjCascade && STAGE == kStageFine && !MASK;
   const CascConst K = kCascOk ? casc_const(W) : CascConst{};
-  const bool casc = kCascOk && __all_sync(0xffffffffu, !live || fabsf(W.dl) <= kCascMaxDl);
+  // (the ratio R = 2^(k1 y + k2) must stay finite wherever the warp-uniform
+  // walk takes a lane: |y| <= the cutoff + the group's longest walk past the
+  // lane's own window -- groups mixing very different radii fall back)
+  const float walk_max = 2.0f * (acq.cutoff * gm.a0max * acq.inv_vdt_f) * acq.inv_f + 20.0f;
+  const float y_max = sqrtf(fmaxf(qmax, 0.0f)) + walk_max * fabsf(W.dl);
+  const bool casc = kCascOk && __all_sync(0xffffffffu, !live || (fabsf(W.dl) <= kCascMaxDl &&
+                                                                 2.0f * fabsf(W.dl2) * y_max <= kCascMaxExp));
   // the conversion-free setup pays where the XU pipe binds (ex2 walk); the
   // element directivity's sinc terms load the FMA pipe instead (config 4:
   // lean +0.7 ms)

@@ -581,6 +581,41 @@ def test_dual_walk_guards_match_oracle(P, a0_mm, f, n):
     assert abs(P.op_count() - ops) <= 2
 
 
+@pytest.mark.parametrize("a0_lo,a0_hi,n,f", [(0.06, 0.2, 4000, 1), (0.1, 0.2, 4000, 2), (0.045, 0.25, 48, 1),
+                                             (0.03, 0.05, 3000, 1), (0.12, 0.12, 2000, 1)])
+def test_adjoint_cascade_walk_and_guards_match_oracle(P, a0_lo, a0_hi, n, f):
+    """Fine adjoint, cascade walk (two-sided binomial running sums + the
+    Gaussian ratio recurrence; csrc/pab_adjoint.cu moments_cascade): radii
+    spanning every walk-length remainder mod 16, a decimated supervision
+    (f = 2, steps still within the recurrence bound), a 48-ball cloud whose
+    lane groups mix radii 0.045-0.25 mm (the ratio-overflow guard sends it to
+    the direct walk), steps above the recurrence bound (a0 <= 0.05 mm: direct
+    walk) and a single radius; tighter than the north-star bar so that the
+    cascade's conversion error (T3: ~2e-6 rms of sum |r y^3|) stays pinned."""
+    rng = np.random.default_rng(97 + n)
+    pos = rng.uniform(-3e-3, 3e-3, (n, 3))
+    p0 = rng.uniform(0.2, 1.0, n)
+    a0 = np.exp(rng.uniform(np.log(a0_lo * 1e-3), np.log(a0_hi * 1e-3), n))
+    ang = rng.uniform(0, 2 * np.pi, 16)
+    sens = np.column_stack([0.03 * np.cos(ang), 0.03 * np.sin(ang), rng.uniform(-0.01, 0.01, 16)])
+    nrm = sens / np.linalg.norm(sens, axis=1, keepdims=True)   # outward normals (the package's convention)
+    grid = P.TimeGrid(0.0, 2.5e-8, 2048)
+    kind = ("cos_power", 2.0)
+    ctx = P.ForwardContext(P.SensorArray(sens, 1500.0, normals=nrm), grid,
+                           directivity=P.Directivity("cos_power", power=2.0))
+    m = max(n // 3, 16)
+    real, _, _, _ = OR.run_model(pos[:m], p0[:m], 1.3 * a0[:m], sens, nrm, 1500.0, 0.0, grid.dt, grid.n_samples, f,
+                                 kind=kind, threads=4)
+    _, L, (gp0, ga0, gpos), _ = OR.run_model(pos, p0, a0, sens, nrm, 1500.0, 0.0, grid.dt, grid.n_samples, f,
+                                             real=real, stage="fine", kind=kind, threads=4)
+    sup = P.SignalSet(grid.decimated(f) if f > 1 else grid, real)
+    Lg, gr = P.backward(P.PointCloud(pos, p0, a0), ctx, sup, stage="fine")
+    assert abs(Lg - L) <= 1e-4 * L
+    assert rel_l2(gr.d_p0, gp0) < 1e-4
+    assert rel_l2(gr.d_a0, ga0) < 1e-4
+    assert rel_l2(gr.d_position, gpos) < 1e-4
+
+
 def test_stale_pairing_table_after_repack(P):
     """The pairing table survives repacks until the next sort (engine
     DeviceCloud.invalidate without resort): moved balls walked with the old
