@@ -47,8 +47,8 @@ FLOPS_FWD = 7      # per in-window sample
 FLOPS_ADJ_FINE = 12
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from the latest
 # ncu --set full capture of each kernel (profiles/)
-TRAFFIC_BYTES = {"forward_kernel": 172_041_984, "adjoint_kernel": 175_067_392}
-TRAFFIC_SRC = "profiles/r02_v1_ncu_summary.txt"
+TRAFFIC_BYTES = {"forward_kernel": 173_147_392, "adjoint_kernel": 181_777_408}
+TRAFFIC_SRC = "profiles/r02_v8_ncu_summary.txt"
 
 
 def parse():
