@@ -412,6 +412,74 @@ __device__ __forceinline__ void dual_block(float4& o0, float4& o1, float m, cons
   o1 = make_float4(c.x, c.y, d.x, d.y);
 }
 
+// Both balls of a lane added into a block's two row quads (o0, o1), the
+// same operations in the same order as dual_block(a) then dual_block(b)
+// (bitwise the same rows), arranged so that every 64-bit half of a quad is
+// updated in place by one tied asm operand: t = ya ga + o; o = yb gb + t.
+// (FFMA2 never writes its addend's register pair, and with the two FFMA2 as
+// separate operations the register allocation left the sums outside the
+// loaded quads: 16 moves per loop trip to rebuild the four STS.128 sources.)
+#ifndef PAB_DUAL_TIED
+#define PAB_DUAL_TIED 1
+#endif
+struct DState {
+  float2 y, g, r;
+};
+__device__ __forceinline__ DState dual_start(float m, const DWalk& w) {
+  DState s;
+  s.y = __ffma2_rn(make_float2(m, m), w.nsc2, w.c0);
+  const float2 e0 = __ffma2_rn(s.y, s.y, w.nla2);
+  const float2 er = __ffma2_rn(s.y, w.kr2, w.br2);
+  s.g = make_float2(ex2(-e0.x), ex2(-e0.y));
+  s.r = make_float2(ex2(er.x), ex2(er.y));
+  return s;
+}
+template <bool LAST>
+__device__ __forceinline__ void dual_step(DState& s, const DWalk& w) {
+  s.y = __fadd2_rn(s.y, w.d2);
+  s.g = __fmul2_rn(s.g, s.r);
+  if (!LAST) s.r = __fmul2_rn(s.r, w.cc2);
+}
+__device__ __forceinline__ unsigned long long pack2(float2 v) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(v.x), "f"(v.y));
+  return r;
+}
+__device__ __forceinline__ void dual_acc(unsigned long long& o, const DState& a, const DState& b) {
+  asm("{\n\t.reg .b64 t;\n\t"
+      "fma.rn.f32x2 t, %1, %2, %0;\n\t"
+      "fma.rn.f32x2 %0, %3, %4, t;\n\t}"
+      : "+l"(o)
+      : "l"(pack2(a.y)), "l"(pack2(a.g)), "l"(pack2(b.y)), "l"(pack2(b.g)));
+}
+#ifndef PAB_DUAL_ST64
+#define PAB_DUAL_ST64 1
+#endif
+__device__ __forceinline__ void st_quad(ulonglong2* p, const ulonglong2& v) {
+#if PAB_DUAL_ST64   // two 8-byte stores: no register quad to assemble
+  const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+  asm volatile("st.volatile.shared.b64 [%0], %1;\n\tst.volatile.shared.b64 [%0+8], %2;" ::"r"(a), "l"(v.x), "l"(v.y) : "memory");
+#else
+  *p = v;
+#endif
+}
+template <bool HALF = false>
+__device__ __forceinline__ void dual_block2(ulonglong2& o0, ulonglong2& o1, float ma, const DWalk& wa, float mb,
+                                            const DWalk& wb) {
+  DState a = dual_start(ma, wa), b = dual_start(mb, wb);
+  dual_acc(o0.x, a, b);
+  dual_step<HALF>(a, wa);
+  dual_step<HALF>(b, wb);
+  dual_acc(o0.y, a, b);
+  if (HALF) return;
+  dual_step<false>(a, wa);
+  dual_step<false>(b, wb);
+  dual_acc(o1.x, a, b);
+  dual_step<true>(a, wa);
+  dual_step<true>(b, wb);
+  dual_acc(o1.y, a, b);
+}
+
 #ifndef PAB_DUAL_UNROLL
 #define PAB_DUAL_UNROLL 2   // 8-sample blocks per loop trip (each block carries two balls)
 #endif
@@ -439,6 +507,23 @@ __device__ __forceinline__ void rmw_walk_dual(float* tile, int lane, int J0, int
       if (q >= Q) q -= Q;
     }
     Jb += 8 * K;
+#if PAB_DUAL_TIED
+    ulonglong2 o[K][2];
+    ulonglong2* const U = reinterpret_cast<ulonglong2*>(T);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      PAB_CHECK(qq[k] >= 0 && qq[k] <= dump && qn[k] >= 0 && qn[k] <= dump + 1);
+      o[k][0] = U[qq[k] * kWarp];
+      o[k][1] = U[qn[k] * kWarp];
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) dual_block2(o[k][0], o[k][1], ma + (float)k * step, wa, mb + (float)k * step, wb);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      st_quad(&U[qq[k] * kWarp], o[k][0]);
+      st_quad(&U[qn[k] * kWarp], o[k][1]);
+    }
+#else
     float4 o[K][2];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -456,6 +541,7 @@ __device__ __forceinline__ void rmw_walk_dual(float* tile, int lane, int J0, int
       T[qq[k] * kWarp] = o[k][0];
       T[qn[k] * kWarp] = o[k][1];
     }
+#endif
     ma += (float)K * step;
     mb += (float)K * step;
   }
@@ -463,11 +549,19 @@ __device__ __forceinline__ void rmw_walk_dual(float* tile, int lane, int J0, int
   for (; nb > 0; --nb) {
     const bool live = Jb <= lim;
     const int qb = live ? q : dump, qc = live ? (q + 1 == Q ? 0 : q + 1) : dump + 1;
+#if PAB_DUAL_TIED
+    ulonglong2* const U = reinterpret_cast<ulonglong2*>(T);
+    ulonglong2 o0 = U[qb * kWarp], o1 = U[qc * kWarp];
+    dual_block2(o0, o1, ma, wa, mb, wb);
+    st_quad(&U[qb * kWarp], o0);
+    st_quad(&U[qc * kWarp], o1);
+#else
     float4 o0 = T[qb * kWarp], o1 = T[qc * kWarp];
     dual_block(o0, o1, ma, wa);
     dual_block(o0, o1, mb, wb);
     T[qb * kWarp] = o0;
     T[qc * kWarp] = o1;
+#endif
     ma += step;
     mb += step;
     q += 2;
@@ -476,10 +570,17 @@ __device__ __forceinline__ void rmw_walk_dual(float* tile, int lane, int J0, int
   }
   if (L & 4) {   // 4-sample tail: the block's first quad only
     const int qb = Jb <= lim ? q : dump;
+#if PAB_DUAL_TIED
+    ulonglong2* const U = reinterpret_cast<ulonglong2*>(T);
+    ulonglong2 o0 = U[qb * kWarp], o1 = make_ulonglong2(0ull, 0ull);
+    dual_block2<true>(o0, o1, ma, wa, mb, wb);
+    U[qb * kWarp] = o0;
+#else
     float4 o0 = T[qb * kWarp], o1 = make_float4(0.f, 0.f, 0.f, 0.f);
     dual_block(o0, o1, ma, wa);
     dual_block(o0, o1, mb, wb);
     T[qb * kWarp] = o0;
+#endif
   }
 }
 
@@ -1179,7 +1280,11 @@ forward_kernel(const BallA* __restrict__ ra, const BallB* __restrict__ rb,
             const int J0a = (int)(wa_ & 0xFFFFu), jha = (wa_ >> 16) == 0xFFFFu ? -1 : (int)(wa_ >> 16);
             const int J0b = (int)(wb_ & 0xFFFFu), jhb = (wb_ >> 16) == 0xFFFFu ? -1 : (int)(wb_ >> 16);
             if (mode == 1) {   // dual walk over the lane's union window
+#ifdef PAB_FWD_NOWALK   // tuning builds only: time everything but the walk
+              if (false) {
+#else
               if (h.x > 0) {
+#endif
                 const int J0u = jha < 0 ? J0b : (jhb < 0 ? J0a : min(J0a, J0b));
                 const DWalk wa = make_dwalk(ra4.w, rb4.x, fs, rb4.y, mfa + (float)((J0u - J0a) * acq.f));
                 const DWalk wb = make_dwalk(rb4.z, rb4.w, fs, rc1, mfb + (float)((J0u - J0b) * acq.f));
