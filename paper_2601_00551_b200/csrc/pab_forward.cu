@@ -155,6 +155,32 @@ __device__ __forceinline__ void flush_rows(float* tile, int lane, int a, int b, 
 //          2^-24 (cutoff >= 5.77, host-checked), below the FP32 resolution
 //          of the ball's own contribution.
 // Two blocks per iteration (16 independent read-modify-writes in flight).
+// Row quads updated in place (round 2): a lane's quad is read as two 64-bit
+// halves, each half accumulated by an asm FFMA2 whose output operand is tied
+// to its addend, and written back by two volatile 8-byte stores.  With the
+// sums as plain float2 values the register allocation left them outside any
+// aligned register quad and rebuilt every STS.128 source with four moves
+// (16 per loop trip of either walk); bitwise the same rows.
+#ifndef PAB_DUAL_TIED
+#define PAB_DUAL_TIED 1
+#endif
+#ifndef PAB_DUAL_ST64
+#define PAB_DUAL_ST64 1
+#endif
+__device__ __forceinline__ unsigned long long pack2(float2 v) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(v.x), "f"(v.y));
+  return r;
+}
+__device__ __forceinline__ void st_quad(ulonglong2* p, const ulonglong2& v) {
+#if PAB_DUAL_ST64   // two 8-byte stores: no register quad to assemble
+  const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+  asm volatile("st.volatile.shared.b64 [%0], %1;\n\tst.volatile.shared.b64 [%0+8], %2;" ::"r"(a), "l"(v.x), "l"(v.y) : "memory");
+#else
+  *p = v;
+#endif
+}
+
 template <bool MASK>
 __device__ __forceinline__ float2 gauss2(float2 q, float qmax) {
   if (MASK) return make_float2(q.x <= qmax ? ex2(-q.x) : 0.0f, q.y <= qmax ? ex2(-q.y) : 0.0f);
@@ -177,6 +203,19 @@ __device__ __forceinline__ float2 rmw_pair(float2 o, float2 m2, float2 c, const 
   const float2 e = __ffma2_rn(y, y, w.nla2);
   const float2 g = gauss2<MASK>(e, w.qmax);
   return __ffma2_rn(y, g, o);
+}
+
+template <bool MASK>
+__device__ __forceinline__ void rmw_pair_tied(unsigned long long& o, float2 m2, float2 c, const Walk& w) {
+  const float2 y = __ffma2_rn(m2, w.nsc2, c);
+  const float2 e = __ffma2_rn(y, y, w.nla2);
+  const float2 g = gauss2<MASK>(e, w.qmax);
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(o) : "l"(pack2(y)), "l"(pack2(g)));
+}
+template <bool MASK>
+__device__ __forceinline__ void rmw4_tied(ulonglong2& o, float2 m2, float2 ca, float2 cb, const Walk& w) {
+  rmw_pair_tied<MASK>(o.x, m2, ca, w);
+  rmw_pair_tied<MASK>(o.y, m2, cb, w);
 }
 
 __device__ __forceinline__ float4 rmw4(float4 o, float2 m2, float2 ca, float2 cb, const Walk& w,
@@ -244,6 +283,14 @@ __device__ __forceinline__ float2 rmw_pair_amp(float2 o, float2 m2, float2 c, fl
   const float2 g = gauss2<MASK>(q, w.qmax);
   return __ffma2_rn(ya, g, o);
 }
+template <bool MASK>
+__device__ __forceinline__ void rmw_pair_amp_tied(unsigned long long& o, float2 m2, float2 c, float2 a, const AWalk& w) {
+  const float2 y = __ffma2_rn(m2, w.nsc2, c);
+  const float2 ya = __ffma2_rn(m2, w.an2, a);
+  const float2 q = __fmul2_rn(y, y);
+  const float2 g = gauss2<MASK>(q, w.qmax);
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(o) : "l"(pack2(ya)), "l"(pack2(g)));
+}
 // L a multiple of 8 from an 8-aligned J0 (blocks never wrap the circular
 // tile); blocks starting past `lim` go to the dump block
 template <bool MASK>
@@ -260,6 +307,16 @@ __device__ __forceinline__ void rmw_walk_amp(float* tile, int lane, int J0, int 
     const int qa = live ? q : dump;
     PAB_CHECK(qa >= 0 && qa + 1 <= dump + 1);
     const float2 m2 = make_float2(mf, mf);
+#if PAB_DUAL_TIED
+    ulonglong2* const U = reinterpret_cast<ulonglong2*>(T);
+    ulonglong2 o0 = U[qa * kWarp], o1 = U[(qa + 1) * kWarp];
+    rmw_pair_amp_tied<MASK>(o0.x, m2, w.c0, w.a0, w);
+    rmw_pair_amp_tied<MASK>(o0.y, m2, w.c1, w.a1, w);
+    rmw_pair_amp_tied<MASK>(o1.x, m2, w.c2, w.a2, w);
+    rmw_pair_amp_tied<MASK>(o1.y, m2, w.c3, w.a3, w);
+    st_quad(&U[qa * kWarp], o0);
+    st_quad(&U[(qa + 1) * kWarp], o1);
+#else
     float4 o0 = T[qa * kWarp], o1 = T[(qa + 1) * kWarp];
     const float2 p0 = rmw_pair_amp<MASK>(make_float2(o0.x, o0.y), m2, w.c0, w.a0, w);
     const float2 p1 = rmw_pair_amp<MASK>(make_float2(o0.z, o0.w), m2, w.c1, w.a1, w);
@@ -267,6 +324,7 @@ __device__ __forceinline__ void rmw_walk_amp(float* tile, int lane, int J0, int 
     const float2 p3 = rmw_pair_amp<MASK>(make_float2(o1.z, o1.w), m2, w.c3, w.a3, w);
     T[qa * kWarp] = make_float4(p0.x, p0.y, p1.x, p1.y);
     T[(qa + 1) * kWarp] = make_float4(p2.x, p2.y, p3.x, p3.y);
+#endif
     q += 2;
     if (q >= kTile / 4) q -= kTile / 4;
   }
@@ -304,6 +362,26 @@ __device__ __forceinline__ void rmw_walk(float* tile, int lane, int J0, int L, i
     }
     Jb += 8 * K;
     // every block's reads before any block's writes
+#if PAB_DUAL_TIED
+    ulonglong2* const U = reinterpret_cast<ulonglong2*>(T);
+    ulonglong2 o[K][2];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      o[k][0] = U[qq[k] * kWarp];
+      o[k][1] = U[qn[k] * kWarp];
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const float2 m2 = make_float2(mf + (float)k * step, mf + (float)k * step);
+      rmw4_tied<MASK>(o[k][0], m2, w.c0, w.c1, w);
+      rmw4_tied<MASK>(o[k][1], m2, w.c2, w.c3, w);
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      st_quad(&U[qq[k] * kWarp], o[k][0]);
+      st_quad(&U[qn[k] * kWarp], o[k][1]);
+    }
+#else
     float4 o[K][2];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -321,6 +399,7 @@ __device__ __forceinline__ void rmw_walk(float* tile, int lane, int J0, int L, i
       T[qq[k] * kWarp] = o[k][0];
       T[qn[k] * kWarp] = o[k][1];
     }
+#endif
     mf += (float)K * step;
   }
 #pragma unroll 1
@@ -328,9 +407,18 @@ __device__ __forceinline__ void rmw_walk(float* tile, int lane, int J0, int L, i
     const bool live = Jb <= lim;
     const int qb = live ? q : dump, qc = live ? (q + 1 == Q ? 0 : q + 1) : dump + 1;
     const float2 m2 = make_float2(mf, mf);
+#if PAB_DUAL_TIED
+    ulonglong2* const U = reinterpret_cast<ulonglong2*>(T);
+    ulonglong2 a = U[qb * kWarp], b = U[qc * kWarp];
+    rmw4_tied<MASK>(a, m2, w.c0, w.c1, w);
+    rmw4_tied<MASK>(b, m2, w.c2, w.c3, w);
+    st_quad(&U[qb * kWarp], a);
+    st_quad(&U[qc * kWarp], b);
+#else
     const float4 a = T[qb * kWarp], b = T[qc * kWarp];
     T[qb * kWarp] = rmw4(a, m2, w.c0, w.c1, w, rmw_pair<MASK>);
     T[qc * kWarp] = rmw4(b, m2, w.c2, w.c3, w, rmw_pair<MASK>);
+#endif
     mf += step;
     q += 2;
     if (q >= Q) q -= Q;
@@ -339,7 +427,14 @@ __device__ __forceinline__ void rmw_walk(float* tile, int lane, int J0, int L, i
   if (L & 4) {   // 4-sample tail: one quad
     const int qb = Jb <= lim ? q : dump;
     const float2 m2 = make_float2(mf, mf);
+#if PAB_DUAL_TIED
+    ulonglong2* const U = reinterpret_cast<ulonglong2*>(T);
+    ulonglong2 a = U[qb * kWarp];
+    rmw4_tied<MASK>(a, m2, w.c0, w.c1, w);
+    st_quad(&U[qb * kWarp], a);
+#else
     T[qb * kWarp] = rmw4(T[qb * kWarp], m2, w.c0, w.c1, w, rmw_pair<MASK>);
+#endif
   }
 }
 
@@ -419,9 +514,6 @@ __device__ __forceinline__ void dual_block(float4& o0, float4& o1, float m, cons
 // (FFMA2 never writes its addend's register pair, and with the two FFMA2 as
 // separate operations the register allocation left the sums outside the
 // loaded quads: 16 moves per loop trip to rebuild the four STS.128 sources.)
-#ifndef PAB_DUAL_TIED
-#define PAB_DUAL_TIED 1
-#endif
 struct DState {
   float2 y, g, r;
 };
@@ -440,28 +532,12 @@ __device__ __forceinline__ void dual_step(DState& s, const DWalk& w) {
   s.g = __fmul2_rn(s.g, s.r);
   if (!LAST) s.r = __fmul2_rn(s.r, w.cc2);
 }
-__device__ __forceinline__ unsigned long long pack2(float2 v) {
-  unsigned long long r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(v.x), "f"(v.y));
-  return r;
-}
 __device__ __forceinline__ void dual_acc(unsigned long long& o, const DState& a, const DState& b) {
   asm("{\n\t.reg .b64 t;\n\t"
       "fma.rn.f32x2 t, %1, %2, %0;\n\t"
       "fma.rn.f32x2 %0, %3, %4, t;\n\t}"
       : "+l"(o)
       : "l"(pack2(a.y)), "l"(pack2(a.g)), "l"(pack2(b.y)), "l"(pack2(b.g)));
-}
-#ifndef PAB_DUAL_ST64
-#define PAB_DUAL_ST64 1
-#endif
-__device__ __forceinline__ void st_quad(ulonglong2* p, const ulonglong2& v) {
-#if PAB_DUAL_ST64   // two 8-byte stores: no register quad to assemble
-  const unsigned a = (unsigned)__cvta_generic_to_shared(p);
-  asm volatile("st.volatile.shared.b64 [%0], %1;\n\tst.volatile.shared.b64 [%0+8], %2;" ::"r"(a), "l"(v.x), "l"(v.y) : "memory");
-#else
-  *p = v;
-#endif
 }
 template <bool HALF = false>
 __device__ __forceinline__ void dual_block2(ulonglong2& o0, ulonglong2& o1, float ma, const DWalk& wa, float mb,
