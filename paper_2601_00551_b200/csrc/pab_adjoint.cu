@@ -7,17 +7,22 @@
 // Decomposition: a warp owns one lane group (32 balls of similar radius, one
 // per lane, so all lanes walk windows of nearly equal length) and loops over a
 // chunk of detectors in batches of 32.  Lane l of a batch computes detector
-// l's group geometry (FP64) once; per detector it is broadcast by shuffles.
-// The residual segment the group can touch is staged into a double-buffered
-// shared-memory segment with cp.async while the previous detector is being
-// processed; every lane walks its own arrival window accumulating four FP32
-// moments
+// l's group geometry (FP64) once and leaves it in a per-warp shared-memory
+// table; per detector the warp reads it back by broadcast LDS.128.  The
+// residual segment the group can touch is staged into one of four
+// shared-memory segments with cp.async a detector pair ahead; detectors go
+// in pairs whose setups and gradient terms are computed side by side.  Every
+// lane walks its own arrival window accumulating four FP32 moments
 //   T_k = sum_J res[J] G(y_J) y_J^k,  k = 0..3,
-// with paired FP32x2 arithmetic (FFMA2/FMUL2/FADD2), 8 samples per iteration
-// and 64-bit shared loads.  Per-pair gradient terms are summed in FP32 over a
-// batch of 32 detectors and folded into FP64 per-ball accumulators held in
-// registers across the chunk (no atomics).  Detector chunks (grid.y) write
-// partial sums that the finalize pass adds in chunk order.
+// with paired FP32x2 arithmetic (FFMA2/FMUL2/FADD2), 16 samples per iteration
+// and 128-bit shared loads: the fine stage as a two-sided cascade of running
+// sums with the Gaussian by a ratio recurrence (moments_cascade: 6 FP32x2 + 1
+// ex2 per sample pair), the other stages, masked cutoffs and out-of-range
+// steps as the direct walk (moments_uniform: 8 FP32x2 + 2 ex2).  Per-pair
+// gradient terms are summed in FP32 over a batch of 32 detectors and folded
+// into FP64 per-ball accumulators kept in shared memory across the chunk (no
+// atomics).  Detector chunks (grid.y) write partial sums that the finalize
+// pass adds in chunk order.
 #include "pab_common.cuh"
 
 namespace pab {
