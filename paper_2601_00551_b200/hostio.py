@@ -23,7 +23,7 @@ import torch
 from . import _lib
 
 PARTS = 1   # pieces per array (measured, cloud 40 MB: 1 / 2 / 4 / 8 pieces 1.29 / 1.48 / 2.40 / 4.05 ms; pageable .to() 2.74)
-THREADS = max(1, min(8, os.cpu_count() or 1))
+THREADS = int(os.environ.get("PAB_HOST_THREADS", max(1, min(8, os.cpu_count() or 1))))   # staging threads (tuning override)
 
 
 class Stager:
