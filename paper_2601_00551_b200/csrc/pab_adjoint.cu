@@ -424,13 +424,15 @@ constexpr int kFlagUniform = 1;   // staged uniform walk (far field, fits the se
 constexpr int kFlagNear = 2;      // a u+ window may exist
 constexpr int kFlagSlow = 4;      // detector within two group radii: FP64 per-pair geometry
 
-// One warp (lane group) per CTA, 16 CTAs per SM (<= 128 registers): warps
+// One warp (lane group) per CTA, 14 CTAs per SM (<= 144 registers; measured
+// with the cascade walk, config-2 adjoint ms at 12 / 13 / 14 / 15 / 16 / 18 /
+// 20 warps per SM: 17.91 / 16.65 / 16.62 / 16.64 / 16.73 / 17.40 / 17.88): warps
 // retire independently (no CTA tail), measured best of 1/2/4/8 warps per CTA.
 #ifndef PAB_ADJ_WARPS
 #define PAB_ADJ_WARPS 1
 #endif
 #ifndef PAB_ADJ_MINB
-#define PAB_ADJ_MINB (16 / PAB_ADJ_WARPS)
+#define PAB_ADJ_MINB (14 / PAB_ADJ_WARPS)
 #endif
 constexpr int kAdjWarps = PAB_ADJ_WARPS;
 #ifdef PAB_ADJ_PROF   // tuning builds only: per-part clock totals (lane 0 of each warp)
