@@ -47,8 +47,8 @@ FLOPS_FWD = 7      # per in-window sample
 FLOPS_ADJ_FINE = 12
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from the latest
 # ncu --set full capture of each kernel (profiles/)
-TRAFFIC_BYTES = {"forward_kernel": 173_147_392, "adjoint_kernel": 181_777_408}
-TRAFFIC_SRC = "profiles/r02_v8_ncu_summary.txt"
+TRAFFIC_BYTES = {"forward_kernel": 173_180_416, "adjoint_kernel": 174_639_360}
+TRAFFIC_SRC = "profiles/r02_v10_ncu_summary.txt"
 
 
 def parse():

@@ -424,9 +424,11 @@ constexpr int kFlagUniform = 1;   // staged uniform walk (far field, fits the se
 constexpr int kFlagNear = 2;      // a u+ window may exist
 constexpr int kFlagSlow = 4;      // detector within two group radii: FP64 per-pair geometry
 
-// One warp (lane group) per CTA, 14 CTAs per SM (<= 144 registers; measured
-// with the cascade walk, config-2 adjoint ms at 12 / 13 / 14 / 15 / 16 / 18 /
-// 20 warps per SM: 17.91 / 16.65 / 16.62 / 16.64 / 16.73 / 17.40 / 17.88): warps
+// One warp (lane group) per CTA.  The launch bound asks for 14 CTAs per SM
+// (<= 144 registers): ptxas still allocates 128, so 16 warps are resident,
+// but schedules the cascade walk better under the looser bound (measured,
+// config-2 adjoint ms with bounds of 12 / 13 / 14 / 15 / 16 / 18 / 20 CTAs per
+// SM: 17.91 / 16.65 / 16.62 / 16.64 / 16.73 / 17.40 / 17.88).  Warps
 // retire independently (no CTA tail), measured best of 1/2/4/8 warps per CTA.
 #ifndef PAB_ADJ_WARPS
 #define PAB_ADJ_WARPS 1
